@@ -1,0 +1,202 @@
+"""Vertex-patch smoother, V-cycle, CG and GMRES.
+
+PAPER.md l.156-164 (local solver Q^T A_j^{-1} Q (A x - b)), l.165-178
+(multiplicative vertex-patch smoother), l.179 (colouring: patches of one
+colour are independent), l.181 (inconsistent treatment: ghost-penalty
+coupling between patches of one colour is ignored), l.195-212 (partitioned
+smoother: Cartesian patches, then n_c sweeps over cut patches), l.124
+(V-cycle, exact coarse solve), l.217 (one pre- and one post-smoothing step).
+
+The local matrices A_j are the principal submatrices of the assembled A_l at
+the patch interior DoFs (l.156: "obtained by selecting the corresponding rows
+and columns from the matrix A_l") and are inverted densely (numpy.linalg.inv);
+the oracle does not use fast diagonalisation.
+
+Test infrastructure only (see oracle/__init__.py).
+"""
+import math
+
+import numpy as np
+
+from .assemble import Params, assemble_matrix
+from .geometry import CARTESIAN, CUTPATCH, Circle, build_patches, hierarchy
+from .transfer import prolongation_matrix
+
+
+class LevelData:
+    def __init__(self, lv, prm, vertices="active"):
+        self.lv = lv
+        self.A = assemble_matrix(lv, prm)
+        self.patches = build_patches(lv, vertices)
+        self.groups = {(k, c): [] for k in (CARTESIAN, CUTPATCH) for c in range(4)}
+        self.inv = []
+        for idx, pt in enumerate(self.patches):
+            self.groups[(pt.kind, pt.colour)].append(idx)
+            I = pt.interior
+            if I.size == 0:
+                self.inv.append(np.zeros((0, 0)))
+                continue
+            Aj = self.A[I][:, I].toarray()
+            self.inv.append(np.linalg.inv(Aj))
+
+    def colour_step(self, x, b, kind, colour):
+        """One colour of the multiplicative smoother: the residual b - A x is
+        taken at the start of the colour and every patch of the colour is
+        corrected from it."""
+        r = b - self.A @ x
+        for idx in self.groups[(kind, colour)]:
+            I = self.patches[idx].interior
+            if I.size:
+                x[I] += self.inv[idx] @ r[I]
+
+    def smooth(self, x, b, n_c, reverse=False):
+        """S(x, b) of eq. (smoother-split): Cartesian
+        colours 0..3, then n_c sweeps over cut colours 0..3.  reverse=True
+        applies the steps in the opposite order (the adjoint sweep, used as
+        post-smoother; reading R9)."""
+        seq = [(CARTESIAN, c) for c in range(4)] + [(CUTPATCH, c) for _ in range(n_c) for c in range(4)]
+        if reverse:
+            seq = seq[::-1]
+        for kind, c in seq:
+            self.colour_step(x, b, kind, c)
+        return x
+
+
+class Hierarchy:
+    """Levels 0..L of PAPER.md l.65-69 with operators, patches and transfers."""
+
+    def __init__(self, x0, y0, length, n0, n_levels, circle, p, prm=None, n_c=2, symmetric=True, vertices="active"):
+        self.prm = prm if prm is not None else Params()
+        self.p = p
+        self.n_c = n_c
+        self.symmetric = symmetric
+        self.levels = [LevelData(lv, self.prm, vertices) for lv in hierarchy(x0, y0, length, n0, n_levels, circle, p)]
+        self.P = [None] + [prolongation_matrix(self.levels[l - 1].lv, self.levels[l].lv)
+                           for l in range(1, n_levels)]
+        A0 = self.levels[0].A.toarray()
+        self.A0inv = np.linalg.inv(A0)
+
+    @property
+    def fine(self):
+        return self.levels[-1]
+
+    def vcycle(self, l, x, b):
+        """V-cycle (one pre- and one post-smoothing step,
+        l.217; exact solve on level 0)."""
+        if l == 0:
+            x[:] = self.A0inv @ b
+            return x
+        ld = self.levels[l]
+        ld.smooth(x, b, self.n_c)
+        r = b - ld.A @ x
+        bc = self.P[l].T @ r
+        xc = np.zeros_like(bc)
+        self.vcycle(l - 1, xc, bc)
+        x += self.P[l] @ xc
+        ld.smooth(x, b, self.n_c, reverse=self.symmetric)
+        return x
+
+    def precondition(self, r):
+        """One V-cycle with zero initial guess (a fixed linear operator)."""
+        return self.vcycle(len(self.levels) - 1, np.zeros_like(r), r)
+
+    def solve_cg(self, b, tol=1e-8, max_it=500):
+        """Preconditioned CG with the V-cycle; stop when ||r||/||r_0|| <= tol
+        (BASELINE.json north_star "CG+MG").  Returns x, iterations, history."""
+        A = self.fine.A
+        x = np.zeros_like(b)
+        r = b.copy()
+        r0 = np.linalg.norm(r)
+        hist = [r0]
+        if r0 == 0.0:
+            return x, 0, hist
+        z = self.precondition(r)
+        p = z.copy()
+        rho = r @ z
+        it = 0
+        while it < max_it:
+            q = A @ p
+            alpha = rho / (p @ q)
+            x += alpha * p
+            r -= alpha * q
+            it += 1
+            rn = np.linalg.norm(r)
+            hist.append(rn)
+            if rn <= tol * r0:
+                break
+            z = self.precondition(r)
+            rho_new = r @ z
+            p = z + (rho_new / rho) * p
+            rho = rho_new
+        return x, it, hist
+
+    def solve_gmres(self, b, tol=1e-9, max_it=500):
+        """Full (non-restarted) right-preconditioned GMRES with modified
+        Gram-Schmidt (Table 1 caption: "Multigrid preconditioner for
+        GMRES solver, iteration counts to reduce residual by 10^-9")."""
+        A = self.fine.A
+        n = b.size
+        beta = np.linalg.norm(b)
+        hist = [beta]
+        if beta == 0.0:
+            return np.zeros(n), 0, hist
+        V = [b / beta]
+        Z = []
+        H = np.zeros((max_it + 1, max_it))
+        g = np.zeros(max_it + 1); g[0] = beta
+        cs, sn = np.zeros(max_it), np.zeros(max_it)
+        it = 0
+        for k in range(max_it):
+            z = self.precondition(V[k])
+            Z.append(z)
+            w = A @ z
+            for i in range(k + 1):
+                H[i, k] = w @ V[i]
+                w = w - H[i, k] * V[i]
+            H[k + 1, k] = np.linalg.norm(w)
+            for i in range(k):
+                t = cs[i] * H[i, k] + sn[i] * H[i + 1, k]
+                H[i + 1, k] = -sn[i] * H[i, k] + cs[i] * H[i + 1, k]
+                H[i, k] = t
+            den = math.hypot(H[k, k], H[k + 1, k])
+            cs[k], sn[k] = H[k, k] / den, H[k + 1, k] / den
+            H[k, k] = den
+            H[k + 1, k] = 0.0
+            g[k + 1] = -sn[k] * g[k]
+            g[k] = cs[k] * g[k]
+            it = k + 1
+            hist.append(abs(g[k + 1]))
+            if abs(g[k + 1]) <= tol * beta:
+                break
+            V.append(w / (np.linalg.norm(w) if np.linalg.norm(w) > 0 else 1.0))
+        y = np.linalg.solve(np.triu(H[:it, :it]), g[:it])
+        x = sum(y[i] * Z[i] for i in range(it))
+        return x, it, hist
+
+    def solve_vcycle(self, b, tol=1e-9, max_it=500):
+        """Stationary V-cycle iteration x <- x + V(b - A x) (Table 3
+        caption); divergence (||r|| > 10 ||r_0||) is reported as it = None."""
+        A = self.fine.A
+        x = np.zeros_like(b)
+        r0 = np.linalg.norm(b)
+        hist = [r0]
+        for it in range(1, max_it + 1):
+            x += self.precondition(b - A @ x)
+            rn = np.linalg.norm(b - A @ x)
+            hist.append(rn)
+            if rn <= tol * r0:
+                return x, it, hist
+            if rn > 10 * r0 or not np.isfinite(rn):
+                return x, None, hist
+        return x, max_it, hist
+
+
+def fractional_iterations(n_it, r_final, r_0):
+    """n_frac = n_it * (-8) / log10(||r_n|| / ||r_0||)."""
+    return n_it * (-8.0) / math.log10(r_final / r_0)
+
+
+def from_workload(w, prm=None, **kw):
+    """Hierarchy for a workloads.Workload description."""
+    return Hierarchy(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, Circle(w.cx, w.cy, w.r), w.p,
+                     prm=prm, n_c=w.n_c, **kw)

@@ -1,0 +1,68 @@
+"""Seeded synthetic workloads shared by the oracle-side tests and the CUDA path.
+
+This module holds NO arithmetic of the method: only the problem descriptions
+(box, circle, degree, levels, parameters) of the BASELINE.json configs and
+seeded random lattice vectors.  Each side applies its own DoF mask to the
+lattice vectors (the mask itself is pinned bit-exactly by the parity tests).
+
+Lattice layout: a level with n cells per side and
+degree p has NL = n p + 1 lattice nodes per side; vectors are NL*NL fp64 values
+indexed b*NL + a (b = y index, a = x index).
+"""
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    x0: float          # box lower-left corner (square box)
+    y0: float
+    length: float      # box side
+    n_coarse: int      # cells per side on level 0
+    n_levels: int      # levels 0..n_levels-1, n_l = n_coarse 2^l
+    cx: float          # circle centre and radius (analytic level set)
+    cy: float
+    r: float
+    p: int             # Q_p degree
+    n_c: int = 2       # cut-patch sweeps per smoothing step
+    tol: float = 1e-8  # CG relative residual tolerance
+
+    @property
+    def n_fine(self):
+        return self.n_coarse * 2 ** (self.n_levels - 1)
+
+
+# BASELINE.json configs[0]: "2D circle r=0.3 on [-0.5,0.5]^2, Q1, 16x16
+# background mesh, 3-level V(1,1)-CG to 1e-8".
+CONFIG0 = Workload("config0-circle-r0.3-Q1-16x16", -0.5, -0.5, 1.0, 4, 3, 0.0, 0.0, 0.3, 1)
+
+# BASELINE.json configs[1]: "2D circle, Q2, 512x512 background mesh, 1 GPU,
+# fp64".  The circle is the paper's section-4 setup (unit circle, 2x2 coarse
+# mesh, box [-1.105,1.105]^2 -- reading R1 in DESIGN.md).
+CONFIG1 = Workload("config1-circle-Q2-512x512", -1.105, -1.105, 2.21, 2, 9, 0.0, 0.0, 1.0, 2)
+
+
+def paper_level(p, L, n_c=2, tol=1e-9):
+    """PAPER.md section 4 setup at table level L (reading R1): the unit circle
+    in [-1.105,1.105]^2 with a 2x2 coarsest mesh; Q1 uses 2^(L-1) cells per
+    side, Q2/Q3 use 2^(L-2) (the numbering of Fig. 2's data and Table 1)."""
+    n_fine = 2 ** (L - 1) if p == 1 else 2 ** (L - 2)
+    n_levels = int(np.log2(n_fine))  # 2, 4, ..., n_fine
+    return Workload(f"paper-L{L}-Q{p}", -1.105, -1.105, 2.21, 2, n_levels, 0.0, 0.0, 1.0, p, n_c, tol)
+
+
+def lattice_nodes(w, level=None):
+    lvl = w.n_levels - 1 if level is None else level
+    return w.n_coarse * 2 ** lvl * w.p + 1
+
+
+def lattice_vector(w, seed, level=None):
+    """Seeded N(0,1) values on every lattice node of a level (unmasked)."""
+    nl = lattice_nodes(w, level)
+    return np.random.default_rng(seed).standard_normal(nl * nl)
+
+
+def with_degree(w, p):
+    return replace(w, p=p, name=f"{w.name}-Q{p}")
