@@ -1,0 +1,167 @@
+/*
+ * cutfem_mg.h — C ABI of the B200-native CutFEM vertex-patch multigrid path.
+ *
+ * Implements the data-parallel hot path of arxiv 2508.11608:
+ * the multiplicative vertex-patch smoother with Cartesian (fast
+ * diagonalisation) and cut (dense inverse) patches for the Nitsche +
+ * ghost-penalty Poisson problem on an unfitted Cartesian mesh, inside a
+ * V-cycle and preconditioned CG.  Paper citations are "P l.<line>" of
+ * PAPER.md; readings R<n> are listed in DESIGN.md.
+ *
+ * Conventions for every call
+ *  - All functions return 0 on success and a nonzero cutfem_status code on
+ *    failure; cutfem_last_error() then returns a message (thread-local).
+ *    No call aborts the process.  Invalid arguments are detected before any
+ *    device work is queued.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Device work is queued on it asynchronously unless the call
+ *    says otherwise.
+ *  - Vectors are DEVICE pointers to fp64 "lattice vectors" of a level: NL rows
+ *    of LD doubles (cutfem_level_info), entry [b*LD + a] is lattice node
+ *    (a, b) = x-index a, y-index b, at position
+ *    x0 + (a div p + xi_{a mod p}) h (xi = Gauss-Lobatto nodes on [0,1]).
+ *    Entries of nodes that carry no DoF (P l.121: no DoFs on exterior cells)
+ *    and the padding columns a >= NL are ignored on input and written as 0 on
+ *    output.  Vectors are owned by the caller; the library never frees them.
+ *  - The problem handle owns all device memory it allocates (mesh data,
+ *    patch data, local inverses, workspaces); cutfem_destroy releases it.
+ *  - A handle is not thread-safe; calls on one handle must be serialised.
+ */
+#ifndef CUTFEM_MG_H
+#define CUTFEM_MG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cutfem_problem_s* cutfem_problem;
+
+enum cutfem_status {
+  CUTFEM_OK = 0,
+  CUTFEM_ERR_ARG = 1,      /* invalid argument (null pointer, bad level, ...) */
+  CUTFEM_ERR_CUDA = 2,     /* a CUDA runtime call failed */
+  CUTFEM_ERR_STATE = 3,    /* call out of order (e.g. smooth before build_patches) */
+  CUTFEM_ERR_GEOMETRY = 4, /* the hierarchy violates Omega_l ⊆ Omega_{l-1} (P l.128-129) */
+  CUTFEM_ERR_SIZE = 5      /* a size limit was exceeded (coarse DoFs, patch size) */
+};
+
+/* Problem description (P l.43-121, l.217; BASELINE.json configs). */
+typedef struct {
+  double x0, y0;        /* lower-left corner of the square background box */
+  double length;        /* side of the box */
+  int n_coarse;         /* cells per side on level 0 (P l.217: 2) */
+  int n_levels;         /* levels 0..n_levels-1, n_l = n_coarse 2^l cells per side */
+  int degree;           /* p of Q_p, 1..4 (P l.79) */
+  double cx, cy, r;     /* level set phi(x) = |x - c| - r, Omega = {phi < 0} (P l.217) */
+  double gamma_D;       /* Nitsche penalty (P l.85); <= 0 selects 5 p (p+1) (R7) */
+  double gamma_k[4];    /* ghost penalty gamma_1..gamma_p (P l.104-108); < 0 selects 0.1 (R5) */
+  int sigma;            /* ghost scaling h^(2k+sigma) (R5; -1 = H^1 scaling) */
+  int n_q;              /* Gauss points per direction on cut cells; 0 selects p+1 (R6) */
+  int n_c;              /* sweeps over cut patches per smoothing step (P l.203; >= 1) */
+  int symmetric;        /* 1: post-smoother = reverse colour order (R9, needed by CG) */
+} cutfem_params;
+
+/* Per-level sizes and counts. */
+typedef struct {
+  int n;                /* cells per side */
+  int nl;               /* lattice nodes per side = n p + 1 */
+  int ld;               /* row stride of lattice vectors (doubles), even, >= nl */
+  int64_t n_dofs;       /* active DoFs n_l (P l.120) */
+  int n_inside, n_cut;  /* cells of M_{l,Omega} \ M_{l,Gamma} and of M_{l,Gamma} (P l.69) */
+  int n_ghost_faces;    /* |F_G| (P l.97-101) */
+  int n_cart[4];        /* Cartesian patches per colour (R4) */
+  int n_cutp[4];        /* cut patches per colour */
+  int64_t n_vol_qp, n_surf_qp; /* cut-cell quadrature points (R6) */
+  double h;
+} cutfem_level_info;
+
+/* ---- setup ------------------------------------------------------------ */
+
+/* setup_mesh: builds the level hierarchy, classifies cells against the level
+ * set (P l.69, reading R2), marks DoF nodes (P l.121), lists ghost faces
+ * (P l.97-101) and generates cut-cell quadrature (P l.190, reading R6), all
+ * on the device.  Blocks until done.  Returns CUTFEM_ERR_GEOMETRY if a fine
+ * active cell has an inactive parent. */
+int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* out);
+
+/* build_patches: vertex patches at every vertex of an active cell (R3),
+ * Cartesian/cut split (R4), colouring (I mod 2) + 2 (J mod 2) (P l.179),
+ * interior DoF sets, local matrices A_{l,j} of the cut patches assembled
+ * matrix-free and inverted (P l.193, R10), fast-diagonalisation data for the
+ * Cartesian patches (P l.192), and the exact coarse inverse of A_0 (P l.124).
+ * Blocks until done. */
+int cutfem_build_patches(cutfem_problem pb, void* stream);
+
+int cutfem_destroy(cutfem_problem pb);
+const char* cutfem_last_error(void);
+int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out);
+
+/* ---- hot path ----------------------------------------------------------- */
+
+/* y = A_l x, A_l = a_l + g_l (P eq. cutfem-ghost l.92-95), matrix-free:
+ * sum factorisation on uncut cells, quadrature with Nitsche terms on cut
+ * cells, ghost-penalty faces.  x and y must not alias. */
+int cutfem_apply_operator(cutfem_problem pb, int level, const double* x, double* y, void* stream);
+
+/* One smoothing step x <- S(x, b) of eq. (smoother-split) (P l.196-210):
+ * Cartesian colours 0..3, then n_c sweeps over cut colours 0..3; reverse = 1
+ * applies the steps in the opposite order (R9).  In place on x. */
+int cutfem_smooth(cutfem_problem pb, int level, double* x, const double* b, int reverse, void* stream);
+
+/* One colour step of the smoother (P l.179-181, R9): kind 0 = Cartesian,
+ * 1 = cut patches; colour 0..3.  x <- x + sum_j Q_j^T A_j^{-1} Q_j (b - A x)
+ * with the residual taken before the step.  Used by the sampled full-size
+ * parity tests. */
+int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, double* x, const double* b, void* stream);
+
+/* x <- x + V(b - A_L x)-style V-cycle on the finest level with the current x
+ * as initial guess (P l.124, one pre- and one post-smoothing step, l.217).
+ * In place on x. */
+int cutfem_vcycle(cutfem_problem pb, double* x, const double* b, void* stream);
+
+/* CG on the finest level preconditioned by one V-cycle (zero initial guess),
+ * x_0 = 0, stop when ||r_k||_2 <= tol ||b||_2 or after max_it iterations.
+ * Writes the solution to x; iterations and final relative residual to the
+ * host pointers (may be NULL).  Blocks (reads the residual norm each
+ * iteration). */
+int cutfem_solve_cg_mg(cutfem_problem pb, double* x, const double* b, double tol, int max_it,
+                       int* iters, double* rel_res, void* stream);
+
+/* Same as the calls above with HOST (pageable or pinned) lattice vectors:
+ * host->device copy of the inputs, the device call, device->host copy of the
+ * result, all on `stream`; blocks until the result is on the host. */
+int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const double* b_host, int reverse,
+                       void* stream);
+int cutfem_solve_cg_mg_host(cutfem_problem pb, double* x_host, const double* b_host, double tol,
+                            int max_it, int* iters, double* rel_res, void* stream);
+
+/* Intergrid transfer (P l.126-137): x_fine += P x_coarse, and
+ * b_coarse = P^T r_fine, between levels `level` (fine) and level-1. */
+int cutfem_prolongate_add(cutfem_problem pb, int level, const double* x_coarse, double* x_fine, void* stream);
+int cutfem_restrict(cutfem_problem pb, int level, const double* r_fine, double* b_coarse, void* stream);
+
+/* ---- export (host copies, blocking; used by the parity tests) ---------- */
+
+/* cell types [j*n + i]: 0 outside, 1 inside, 2 cut */
+int cutfem_export_cell_types(cutfem_problem pb, int level, int8_t* host_out);
+/* DoF mask of the lattice [b*nl + a] (1 = node carries a DoF) */
+int cutfem_export_dof_mask(cutfem_problem pb, int level, uint8_t* host_out);
+/* patch vertices of one (kind, colour) list, kind 0 = Cartesian, 1 = cut,
+ * packed I + (n+1) J, in list order; returns the count in *count.  host_out
+ * may be NULL to query the count. */
+int cutfem_export_patches(cutfem_problem pb, int level, int kind, int colour, int32_t* host_out, int* count);
+/* interior DoF sets of the cut patches in (colour, list) order: offsets
+ * (n_cut_patches + 1) and lattice indices b*nl + a.  NULL pointers query the
+ * sizes through *n_patches and *n_entries. */
+int cutfem_export_cut_interior(cutfem_problem pb, int level, int64_t* host_offsets, int32_t* host_nodes,
+                               int* n_patches, int64_t* n_entries);
+/* number of kernels this library has launched since load (for the bench's
+ * gpu_launches claim) */
+int64_t cutfem_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CUTFEM_MG_H */

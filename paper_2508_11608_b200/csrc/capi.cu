@@ -1,0 +1,286 @@
+// capi.cu — extern "C" boundary of libcutfem_mg.so (include/cutfem_mg.h).
+// Argument validation, exception -> status-code translation, host-pointer
+// variants.  Single translation unit: includes the kernels and the host
+// orchestration.
+#include "../../include/cutfem_mg.h"
+#include "problem.cuh"
+
+struct cutfem_problem_s {
+  cf::Problem p;
+};
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return CUTFEM_OK;
+  } catch (const cf::Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CUTFEM_ERR_STATE;
+  }
+}
+
+static void check_level(cutfem_problem pb, int level) {
+  cf::require(pb != nullptr, cf::ERR_ARG, "null problem handle");
+  cf::require(level >= 0 && level < (int)pb->p.lv.size(), cf::ERR_ARG, "level out of range");
+}
+static void check_built(cutfem_problem pb) {
+  cf::require(pb != nullptr, cf::ERR_ARG, "null problem handle");
+  cf::require(pb->p.built, cf::ERR_STATE, "cutfem_build_patches has not been called");
+}
+static void use_stream(cutfem_problem pb, void* stream) { pb->p.st = (cudaStream_t)stream; }
+
+extern "C" {
+
+const char* cutfem_last_error(void) { return g_err.c_str(); }
+int64_t cutfem_launch_count(void) { return cf::g_launches; }
+
+int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* out) {
+  return guarded([&]() {
+    cf::require(prm != nullptr && out != nullptr, cf::ERR_ARG, "null argument");
+    cf::require(prm->degree >= 1 && prm->degree <= CF_MAXP, cf::ERR_ARG, "degree must be 1..4");
+    cf::require(prm->n_coarse >= 1 && prm->n_levels >= 1 && prm->n_levels <= 16, cf::ERR_ARG, "bad level counts");
+    cf::require(((int64_t)prm->n_coarse << (prm->n_levels - 1)) * prm->degree < 60000, cf::ERR_SIZE,
+                "finest lattice too large");
+    cf::require(prm->length > 0 && prm->r > 0, cf::ERR_ARG, "box length and radius must be positive");
+    cf::require(prm->n_q >= 0 && prm->n_q <= CF_MAXNQ, cf::ERR_ARG, "n_q must be 0..12");
+    cf::require(prm->n_c >= 1, cf::ERR_ARG, "n_c must be >= 1");
+    *out = nullptr;
+    auto* pb = new cutfem_problem_s();
+    cf::Params& P = pb->p.prm;
+    P.x0 = prm->x0;
+    P.y0 = prm->y0;
+    P.length = prm->length;
+    P.cx = prm->cx;
+    P.cy = prm->cy;
+    P.r = prm->r;
+    P.n_coarse = prm->n_coarse;
+    P.n_levels = prm->n_levels;
+    P.p = prm->degree;
+    P.gamma_D = prm->gamma_D > 0 ? prm->gamma_D : 5.0 * P.p * (P.p + 1);
+    for (int k = 0; k < CF_MAXP; ++k) P.gamma_k[k] = prm->gamma_k[k] >= 0 ? prm->gamma_k[k] : 0.1;
+    P.sigma = prm->sigma;
+    P.n_q = prm->n_q > 0 ? prm->n_q : P.p + 1;
+    P.n_c = prm->n_c;
+    P.symmetric = prm->symmetric;
+    use_stream(pb, stream);
+    try {
+      pb->p.setup_mesh();
+    } catch (...) {
+      delete pb;
+      throw;
+    }
+    *out = pb;
+  });
+}
+
+int cutfem_build_patches(cutfem_problem pb, void* stream) {
+  return guarded([&]() {
+    cf::require(pb != nullptr, cf::ERR_ARG, "null problem handle");
+    cf::require(!pb->p.built, cf::ERR_STATE, "patches already built");
+    use_stream(pb, stream);
+    pb->p.build_patches();
+  });
+}
+
+int cutfem_destroy(cutfem_problem pb) {
+  return guarded([&]() { delete pb; });
+}
+
+int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(out != nullptr, cf::ERR_ARG, "null output");
+    const cf::LevelData& D = pb->p.lv[level];
+    out->n = D.a.n;
+    out->nl = D.a.nl;
+    out->ld = D.a.ld;
+    out->n_dofs = D.n_dofs;
+    out->n_inside = D.n_inside;
+    out->n_cut = D.a.n_cut;
+    out->n_ghost_faces = D.a.n_ghost;
+    for (int c = 0; c < 4; ++c) {
+      out->n_cart[c] = D.n_cart[c];
+      out->n_cutp[c] = D.n_cutp[c];
+    }
+    out->n_vol_qp = D.n_vq;
+    out->n_surf_qp = D.n_sq;
+    out->h = D.a.h;
+  });
+}
+
+int cutfem_apply_operator(cutfem_problem pb, int level, const double* x, double* y, void* stream) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(x && y && x != y, cf::ERR_ARG, "x, y must be distinct non-null device pointers");
+    use_stream(pb, stream);
+    pb->p.apply(level, x, y, nullptr);
+  });
+}
+
+int cutfem_smooth(cutfem_problem pb, int level, double* x, const double* b, int reverse, void* stream) {
+  return guarded([&]() {
+    check_built(pb);
+    check_level(pb, level);
+    cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
+    use_stream(pb, stream);
+    pb->p.graphed(1, x, b, level * 2 + (reverse ? 1 : 0), [&]() { pb->p.smooth(level, x, b, reverse); });
+  });
+}
+
+int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, double* x, const double* b, void* stream) {
+  return guarded([&]() {
+    check_built(pb);
+    check_level(pb, level);
+    cf::require((kind == 0 || kind == 1) && colour >= 0 && colour < 4, cf::ERR_ARG, "bad kind/colour");
+    cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
+    use_stream(pb, stream);
+    if (kind == 0) pb->p.cart_step(level, colour, x, b);
+    else pb->p.cut_step(level, colour, x, b);
+  });
+}
+
+int cutfem_vcycle(cutfem_problem pb, double* x, const double* b, void* stream) {
+  return guarded([&]() {
+    check_built(pb);
+    cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
+    use_stream(pb, stream);
+    const int L = pb->p.prm.n_levels - 1;
+    pb->p.graphed(2, x, b, 0, [&]() { pb->p.vcycle(L, x, b); });
+  });
+}
+
+int cutfem_solve_cg_mg(cutfem_problem pb, double* x, const double* b, double tol, int max_it, int* iters,
+                       double* rel_res, void* stream) {
+  return guarded([&]() {
+    check_built(pb);
+    cf::require(x && b, cf::ERR_ARG, "null vector");
+    cf::require(tol >= 0 && max_it >= 0, cf::ERR_ARG, "tol and max_it must be non-negative");
+    use_stream(pb, stream);
+    pb->p.solve_cg(x, b, tol, max_it, iters, rel_res);
+  });
+}
+
+static void host_buffers(cutfem_problem pb) {
+  if (!pb->p.hx) {
+    const cf::LevelArgs& F = pb->p.lv.back().a;
+    pb->p.hx = pb->p.alloc<double>((int64_t)F.nl * F.ld);
+    pb->p.hb = pb->p.alloc<double>((int64_t)F.nl * F.ld);
+  }
+}
+
+int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const double* b_host, int reverse,
+                       void* stream) {
+  return guarded([&]() {
+    check_built(pb);
+    check_level(pb, level);
+    cf::require(x_host && b_host, cf::ERR_ARG, "null vector");
+    use_stream(pb, stream);
+    host_buffers(pb);
+    const cf::LevelArgs& L = pb->p.lv[level].a;
+    const size_t bytes = (size_t)L.nl * L.ld * sizeof(double);
+    CF_CUDA(cudaMemcpyAsync(pb->p.hx, x_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
+    CF_CUDA(cudaMemcpyAsync(pb->p.hb, b_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
+    double* dx = pb->p.hx;
+    const double* db = pb->p.hb;
+    pb->p.graphed(1, dx, db, level * 2 + (reverse ? 1 : 0), [&]() { pb->p.smooth(level, dx, db, reverse); });
+    CF_CUDA(cudaMemcpyAsync(x_host, pb->p.hx, bytes, cudaMemcpyDeviceToHost, pb->p.st));
+    pb->p.sync();
+  });
+}
+
+int cutfem_solve_cg_mg_host(cutfem_problem pb, double* x_host, const double* b_host, double tol, int max_it,
+                            int* iters, double* rel_res, void* stream) {
+  return guarded([&]() {
+    check_built(pb);
+    cf::require(x_host && b_host, cf::ERR_ARG, "null vector");
+    use_stream(pb, stream);
+    host_buffers(pb);
+    const cf::LevelArgs& F = pb->p.lv.back().a;
+    const size_t bytes = (size_t)F.nl * F.ld * sizeof(double);
+    CF_CUDA(cudaMemcpyAsync(pb->p.hb, b_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
+    pb->p.solve_cg(pb->p.hx, pb->p.hb, tol, max_it, iters, rel_res);
+    CF_CUDA(cudaMemcpyAsync(x_host, pb->p.hx, bytes, cudaMemcpyDeviceToHost, pb->p.st));
+    pb->p.sync();
+  });
+}
+
+int cutfem_prolongate_add(cutfem_problem pb, int level, const double* x_coarse, double* x_fine, void* stream) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(level >= 1, cf::ERR_ARG, "level must be >= 1");
+    cf::require(x_coarse && x_fine, cf::ERR_ARG, "null vector");
+    use_stream(pb, stream);
+    pb->p.prolongate_add(level, x_coarse, x_fine);
+  });
+}
+
+int cutfem_restrict(cutfem_problem pb, int level, const double* r_fine, double* b_coarse, void* stream) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(level >= 1, cf::ERR_ARG, "level must be >= 1");
+    cf::require(r_fine && b_coarse, cf::ERR_ARG, "null vector");
+    use_stream(pb, stream);
+    pb->p.restrict_(level, r_fine, b_coarse);
+  });
+}
+
+int cutfem_export_cell_types(cutfem_problem pb, int level, int8_t* host_out) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(host_out != nullptr, cf::ERR_ARG, "null output");
+    const cf::LevelData& D = pb->p.lv[level];
+    CF_CUDA(cudaMemcpy(host_out, D.ctype, (size_t)D.a.n * D.a.n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int cutfem_export_dof_mask(cutfem_problem pb, int level, uint8_t* host_out) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(host_out != nullptr, cf::ERR_ARG, "null output");
+    const cf::LevelArgs& L = pb->p.lv[level].a;
+    CF_CUDA(cudaMemcpy2D(host_out, L.nl, pb->p.lv[level].mask, L.ld, L.nl, L.nl, cudaMemcpyDeviceToHost));
+  });
+}
+
+int cutfem_export_patches(cutfem_problem pb, int level, int kind, int colour, int32_t* host_out, int* count) {
+  return guarded([&]() {
+    check_built(pb);
+    check_level(pb, level);
+    cf::require((kind == 0 || kind == 1) && colour >= 0 && colour < 4 && count, cf::ERR_ARG, "bad kind/colour");
+    const cf::LevelData& D = pb->p.lv[level];
+    const int* off = kind == 0 ? D.cart_off : D.cutp_off;
+    const int* list = kind == 0 ? D.cart_list : D.cutp_list;
+    *count = off[colour + 1] - off[colour];
+    if (host_out && *count)
+      CF_CUDA(cudaMemcpy(host_out, list + off[colour], sizeof(int) * (*count), cudaMemcpyDeviceToHost));
+  });
+}
+
+int cutfem_export_cut_interior(cutfem_problem pb, int level, int64_t* host_offsets, int32_t* host_nodes,
+                               int* n_patches, int64_t* n_entries) {
+  return guarded([&]() {
+    check_built(pb);
+    check_level(pb, level);
+    const cf::LevelData& D = pb->p.lv[level];
+    const int ncp = D.cutp_off[4];
+    if (n_patches) *n_patches = ncp;
+    if (n_entries) *n_entries = D.n_ent;
+    if (host_offsets) CF_CUDA(cudaMemcpy(host_offsets, D.cutp_ent, sizeof(int64_t) * (ncp + 1), cudaMemcpyDeviceToHost));
+    if (host_nodes && D.n_ent) {
+      std::vector<int32_t> tmp(D.n_ent);
+      CF_CUDA(cudaMemcpy(tmp.data(), D.ent_node, sizeof(int32_t) * D.n_ent, cudaMemcpyDeviceToHost));
+      for (int64_t e = 0; e < D.n_ent; ++e) {
+        int b = tmp[e] / D.a.ld, a = tmp[e] % D.a.ld;
+        host_nodes[e] = b * D.a.nl + a;
+      }
+    }
+  });
+}
+
+}  // extern "C"

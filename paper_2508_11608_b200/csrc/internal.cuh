@@ -1,0 +1,150 @@
+// internal.cuh — shared definitions of the CutFEM multigrid CUDA path.
+//
+// Layout: lattice vectors of a level are NL rows of
+// LD doubles, node (a, b) at [b*LD + a]; cells are indexed j*n + i.  The
+// per-degree 1D tables live in __constant__ memory (broadcast reads inside
+// the sum-factorisation loops); per-level scalars and pointers travel by
+// value in LevelArgs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#define CF_MAXP 4
+#define CF_MAXNQ 12
+
+namespace cf {
+
+enum CellType : int8_t { OUTSIDE = 0, INSIDE = 1, CUT = 2 };
+enum VertexKind : uint8_t { V_NONE = 0, V_CART = 1, V_CUT = 2 };
+
+// 1D tables of Q_p on the reference interval [0,1] (P l.79), computed on the
+// host in tables.cuh and uploaded once per process for p = 1..4.
+struct Tab {
+  double gll[CF_MAXP + 1];                       // Gauss-Lobatto nodes
+  double lc[CF_MAXP + 1][CF_MAXP + 1];           // L_i(xi) = sum_m lc[i][m] xi^m
+  double dc[CF_MAXP + 1][CF_MAXP + 1];           // L_i'(xi) = sum_m dc[i][m] xi^m
+  double Kref[CF_MAXP + 1][CF_MAXP + 1];         // int_0^1 L_i' L_j'
+  double Mref[CF_MAXP + 1][CF_MAXP + 1];         // int_0^1 L_i L_j
+  double d0[CF_MAXP + 1][CF_MAXP + 1];           // d0[k][i] = L_i^(k)(0)
+  double d1[CF_MAXP + 1][CF_MAXP + 1];           // d1[k][i] = L_i^(k)(1)
+  double Kp[2 * CF_MAXP + 1][2 * CF_MAXP + 1];   // two-cell patch stiffness (2p+1 nodes)
+  double Mp[2 * CF_MAXP + 1][2 * CF_MAXP + 1];   // two-cell patch mass
+  double S[2 * CF_MAXP - 1][2 * CF_MAXP - 1];    // K_int S = M_int S diag(lam), S^T M_int S = I
+  double lam[2 * CF_MAXP - 1];
+  double tw[CF_MAXP][4 * CF_MAXP + 1];           // restriction: coarse basis of local node m at fine offset d+2p
+  double pw[2 * CF_MAXP + 1][CF_MAXP + 1];       // prolongation: L_m at fine offset d in [0,2p] of a coarse cell
+};
+
+// single translation unit (capi.cu): the tables are defined here
+__constant__ Tab c_tab[CF_MAXP + 1];
+__constant__ double c_gx[CF_MAXNQ + 1][CF_MAXNQ];  // Gauss-Legendre points on [0,1], c_gx[n][i]
+__constant__ double c_gw[CF_MAXNQ + 1][CF_MAXNQ];
+
+// Per-level arguments passed by value to every kernel.
+struct LevelArgs {
+  int n, p, nl, ld;
+  double h, x0, y0;
+  double cx, cy, r;
+  double gDh;                        // gamma_D / h
+  double gs[CF_MAXP + 1];            // ghost scale gamma_k h^(sigma+1) / (k!)^2 (index k = 1..p)
+  const int8_t* ctype;               // n*n
+  const uint8_t* mask;               // nl*ld DoF mask
+  const int* cut_id;                 // n*n -> cut cell index or -1
+  const int* cut_list;               // packed i + n*j
+  int n_cut;
+  const int* q_off;                  // n_cut+1, volume points
+  const double *qx, *qy, *qw;        // reference coordinates, physical weight
+  const int* s_off;                  // n_cut+1, surface points
+  const double *sx, *sy, *sw, *snx, *sny;
+  const int* gx_id;                  // face (i,j)|(i+1,j) -> ghost id or -1, index j*n+i
+  const int* gy_id;                  // face (i,j)|(i,j+1)
+  const int* ghost_list;             // packed axis | i << 1 | j << 16... see setup
+  int n_ghost;
+  double* ycut;                      // n_cut * (p+1)^2 scratch (operator apply)
+  double* jm;                        // n_ghost * p * (p+1) scratch (operator apply)
+};
+
+// Per-level device data owned by the problem.
+struct LevelData {
+  LevelArgs a;
+  int64_t n_dofs = 0;
+  int n_inside = 0;
+  int8_t* ctype = nullptr;
+  uint8_t* mask = nullptr;
+  int* cut_id = nullptr;
+  int* cut_list = nullptr;
+  int* q_off = nullptr;
+  double* qbuf = nullptr;            // qx|qy|qw
+  int* s_off = nullptr;
+  double* sbuf = nullptr;            // sx|sy|sw|snx|sny
+  int64_t n_vq = 0, n_sq = 0;
+  int* gx_id = nullptr;
+  int* gy_id = nullptr;
+  int* ghost_list = nullptr;
+  double* ycut = nullptr;
+  double* jm = nullptr;
+  // patches
+  uint8_t* vkind = nullptr;          // (n+1)^2
+  int n_cart[4] = {0, 0, 0, 0};
+  int* cart_list = nullptr;          // all colours concatenated, packed I + (n+1) J
+  int cart_off[5] = {0, 0, 0, 0, 0};
+  int n_cart_tiles[4] = {0, 0, 0, 0};
+  int* cart_tiles = nullptr;         // per colour concatenated, packed ti + 65536 tj
+  int cart_tile_off[5] = {0, 0, 0, 0, 0};
+  int n_cutp[4] = {0, 0, 0, 0};
+  int cutp_off[5] = {0, 0, 0, 0, 0};
+  int* cutp_list = nullptr;          // packed I + (n+1) J
+  int64_t* cutp_ent = nullptr;       // n_cutp+1 offsets into entry arrays
+  int32_t* ent_node = nullptr;       // lattice index of each interior DoF
+  uint8_t* ent_loc = nullptr;        // local index in the (2p+1)^2 block
+  int32_t* ent_patch = nullptr;      // owning patch of each entry
+  int64_t n_ent = 0;
+  int64_t ent_col_off[5] = {0, 0, 0, 0, 0};  // host copy of cutp_ent at the colour boundaries
+  int64_t* cutp_inv = nullptr;       // n_cutp+1 offsets into inverse storage
+  double* inv = nullptr;             // local inverses, m_j^2 each, row-major (symmetric)
+  int64_t n_inv = 0;
+  double* zbuf = nullptr;            // n_ent corrections (two-phase cut colour step)
+  // workspace lattice vectors for the V-cycle
+  double *x = nullptr, *b = nullptr, *r = nullptr;
+};
+
+struct Params {
+  double x0, y0, length, cx, cy, r, gamma_D, gamma_k[CF_MAXP];
+  int n_coarse, n_levels, p, sigma, n_q, n_c, symmetric;
+};
+
+// launch accounting for the bench's gpu_launches claim
+extern int64_t g_launches;
+
+#define CF_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw cf::Error(cf::ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define CF_LAUNCHED()                                                                   \
+  do {                                                                                  \
+    ++cf::g_launches;                                                                   \
+    cudaError_t _e = cudaGetLastError();                                                \
+    if (_e != cudaSuccess)                                                              \
+      throw cf::Error(cf::ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+enum { ERR_ARG = 1, ERR_CUDA = 2, ERR_STATE = 3, ERR_GEOMETRY = 4, ERR_SIZE = 5 };
+
+struct Error {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+inline void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace cf

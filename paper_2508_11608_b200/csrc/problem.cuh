@@ -1,0 +1,607 @@
+// problem.cuh — host orchestration: setup of the hierarchy (P l.65-69),
+// patches (P l.141-179), V-cycle (P l.124), CG; CUDA-graph caching of the
+// launch sequences.  Every arithmetic step runs in the kernels of
+// kernels.cuh / setup.cuh; the host only sequences launches.
+#pragma once
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <vector>
+
+#include "internal.cuh"
+#include "kernels.cuh"
+#include "tables.cuh"
+
+namespace cf {
+
+int64_t g_launches = 0;
+
+#define CF_DISPATCH(p, ...)                               \
+  switch (p) {                                            \
+    case 1: { constexpr int P = 1; __VA_ARGS__; } break;  \
+    case 2: { constexpr int P = 2; __VA_ARGS__; } break;  \
+    case 3: { constexpr int P = 3; __VA_ARGS__; } break;  \
+    case 4: { constexpr int P = 4; __VA_ARGS__; } break;  \
+    default: throw Error(ERR_ARG, "degree must be 1..4"); \
+  }
+
+template <int P> constexpr int cart_tp() { return P <= 2 ? 16 : 8; }
+constexpr int CUT_WPB = 4;
+
+struct GraphRec {
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
+struct Problem {
+  Params prm;
+  std::vector<LevelData> lv;
+  cudaStream_t st = nullptr;
+  cudaStream_t cap_st = nullptr;
+  bool built = false;
+  // coarse
+  int n0 = 0;
+  int* c_nodes = nullptr;
+  double* c_inv = nullptr;
+  // CG
+  double *cg_x = nullptr, *cg_r = nullptr, *cg_z = nullptr, *cg_p = nullptr, *cg_q = nullptr;
+  double *part = nullptr, *sc = nullptr, *sc_host = nullptr;
+  // host-pointer entry points
+  double *hx = nullptr, *hb = nullptr;
+  // scratch
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int* d_count = nullptr;
+  std::vector<void*> allocs;
+  std::map<std::tuple<int, const void*, const void*, int>, GraphRec> graphs;
+
+  ~Problem() {
+    for (auto& g : graphs)
+      if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+    for (void* p : allocs) cudaFree(p);
+    if (sc_host) cudaFreeHost(sc_host);
+    if (cap_st) cudaStreamDestroy(cap_st);
+  }
+
+  template <class T>
+  T* alloc(int64_t n) {
+    void* p = nullptr;
+    if (n <= 0) n = 1;
+    CF_CUDA(cudaMalloc(&p, (size_t)n * sizeof(T)));
+    allocs.push_back(p);
+    return (T*)p;
+  }
+  void* scratch(size_t bytes) {
+    if (bytes > tmp_bytes) {
+      if (tmp) cudaFree(tmp);
+      tmp = nullptr;
+      CF_CUDA(cudaMalloc(&tmp, bytes));
+      tmp_bytes = bytes;
+    }
+    return tmp;
+  }
+  void sync() { CF_CUDA(cudaStreamSynchronize(st)); }
+
+  int read_count() {
+    int h = 0;
+    CF_CUDA(cudaMemcpyAsync(&h, d_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    sync();
+    return h;
+  }
+
+  // indices i in [0, n) with flag[i] != 0, in increasing order
+  int select(const uint8_t* flags, int n, int* out) {
+    size_t bytes = 0;
+    thrust::counting_iterator<int> it(0);
+    CF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, n, st));
+    CF_CUDA(cub::DeviceSelect::Flagged(scratch(bytes), bytes, it, flags, out, d_count, n, st));
+    return read_count();
+  }
+  // exclusive scan of n ints into n+1 int64 offsets; returns the total
+  int64_t scan64(const int* in, int n, int64_t* out) {
+    size_t bytes = 0;
+    CF_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
+    if (n == 0) return 0;
+    CF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out + 1, n, st));
+    CF_CUDA(cub::DeviceScan::InclusiveSum(scratch(bytes), bytes, in, out + 1, n, st));
+    int64_t tot = 0;
+    CF_CUDA(cudaMemcpyAsync(&tot, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    sync();
+    return tot;
+  }
+  int64_t scan32(const int* in, int n, int* out) {
+    size_t bytes = 0;
+    CF_CUDA(cudaMemsetAsync(out, 0, sizeof(int), st));
+    if (n == 0) return 0;
+    CF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out + 1, n, st));
+    CF_CUDA(cub::DeviceScan::InclusiveSum(scratch(bytes), bytes, in, out + 1, n, st));
+    int tot = 0;
+    CF_CUDA(cudaMemcpyAsync(&tot, out + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    sync();
+    return tot;
+  }
+
+  // ---------------------------------------------------------------- setup
+  void setup_mesh() {
+    host::upload_tables();
+    d_count = alloc<int>(1);
+    const int p = prm.p;
+    lv.resize(prm.n_levels);
+    for (int l = 0; l < prm.n_levels; ++l) {
+      LevelData& D = lv[l];
+      LevelArgs& L = D.a;
+      std::memset(&L, 0, sizeof(L));
+      L.n = prm.n_coarse << l;
+      L.p = p;
+      L.nl = L.n * p + 1;
+      L.ld = (L.nl + 1) & ~1;
+      L.h = prm.length / L.n;
+      L.x0 = prm.x0;
+      L.y0 = prm.y0;
+      L.cx = prm.cx;
+      L.cy = prm.cy;
+      L.r = prm.r;
+      L.gDh = prm.gamma_D / L.h;
+      for (int k = 1; k <= p; ++k) {
+        double f = 1.0;
+        for (int q = 2; q <= k; ++q) f *= q;
+        L.gs[k] = prm.gamma_k[k - 1] * std::pow(L.h, prm.sigma + 1) / (f * f);
+      }
+      const int n = L.n;
+      dim3 b2(16, 16), gcell(ceil_div(n, 16), ceil_div(n, 16));
+      D.ctype = alloc<int8_t>((int64_t)n * n);
+      k_classify<<<gcell, b2, 0, st>>>(L, D.ctype);
+      CF_LAUNCHED();
+      L.ctype = D.ctype;
+      D.mask = alloc<uint8_t>((int64_t)L.nl * L.ld);
+      CF_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int), st));
+      k_mask<<<dim3(ceil_div(L.ld, 16), ceil_div(L.nl, 16)), b2, 0, st>>>(L, D.ctype, D.mask, d_count);
+      CF_LAUNCHED();
+      L.mask = D.mask;
+      D.n_dofs = read_count();
+      if (l > 0) {
+        CF_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int), st));
+        k_parent_check<<<gcell, b2, 0, st>>>(L, D.ctype, lv[l - 1].a.n, lv[l - 1].ctype, d_count);
+        CF_LAUNCHED();
+        require(read_count() == 0, ERR_GEOMETRY, "a fine active cell has an inactive parent (Omega_l not in Omega_{l-1})");
+      }
+      // cut cells and inside count
+      uint8_t* flags = alloc<uint8_t>(2 * (int64_t)n * n);
+      int* tmpi = alloc<int>(2 * (int64_t)n * n);
+      k_iota_flags_cells<<<ceil_div((int64_t)n * n, 256), 256, 0, st>>>(n, D.ctype, INSIDE, flags);
+      CF_LAUNCHED();
+      D.n_inside = select(flags, n * n, tmpi);
+      k_iota_flags_cells<<<ceil_div((int64_t)n * n, 256), 256, 0, st>>>(n, D.ctype, CUT, flags);
+      CF_LAUNCHED();
+      L.n_cut = select(flags, n * n, tmpi);
+      D.cut_list = alloc<int>(L.n_cut);
+      CF_CUDA(cudaMemcpyAsync(D.cut_list, tmpi, sizeof(int) * L.n_cut, cudaMemcpyDeviceToDevice, st));
+      L.cut_list = D.cut_list;
+      D.cut_id = alloc<int>((int64_t)n * n);
+      k_fill<<<ceil_div((int64_t)n * n, 256), 256, 0, st>>>(D.cut_id, (int64_t)n * n, -1);
+      CF_LAUNCHED();
+      if (L.n_cut) {
+        k_scatter_id<<<ceil_div(L.n_cut, 256), 256, 0, st>>>(D.cut_list, L.n_cut, D.cut_id);
+        CF_LAUNCHED();
+      }
+      L.cut_id = D.cut_id;
+      // ghost faces
+      k_ghost_flags<<<ceil_div(2 * (int64_t)n * n, 256), 256, 0, st>>>(L, D.ctype, flags);
+      CF_LAUNCHED();
+      L.n_ghost = select(flags, 2 * n * n, tmpi);
+      D.ghost_list = alloc<int>(L.n_ghost);
+      CF_CUDA(cudaMemcpyAsync(D.ghost_list, tmpi, sizeof(int) * L.n_ghost, cudaMemcpyDeviceToDevice, st));
+      L.ghost_list = D.ghost_list;
+      D.gx_id = alloc<int>((int64_t)n * n);
+      D.gy_id = alloc<int>((int64_t)n * n);
+      k_fill<<<ceil_div((int64_t)n * n, 256), 256, 0, st>>>(D.gx_id, (int64_t)n * n, -1);
+      CF_LAUNCHED();
+      k_fill<<<ceil_div((int64_t)n * n, 256), 256, 0, st>>>(D.gy_id, (int64_t)n * n, -1);
+      CF_LAUNCHED();
+      if (L.n_ghost) {
+        k_ghost_maps<<<ceil_div(L.n_ghost, 256), 256, 0, st>>>(D.ghost_list, L.n_ghost, n, D.gx_id, D.gy_id);
+        CF_LAUNCHED();
+      }
+      L.gx_id = D.gx_id;
+      L.gy_id = D.gy_id;
+      // cut-cell quadrature (R6)
+      D.q_off = alloc<int>(L.n_cut + 1);
+      D.s_off = alloc<int>(L.n_cut + 1);
+      int* vc = tmpi;
+      int* scn = tmpi + n * n;
+      if (L.n_cut) {
+        k_cut_count<<<ceil_div(L.n_cut, 128), 128, 0, st>>>(L, prm.n_q, vc, scn);
+        CF_LAUNCHED();
+      }
+      D.n_vq = scan32(vc, L.n_cut, D.q_off);
+      D.n_sq = scan32(scn, L.n_cut, D.s_off);
+      L.q_off = D.q_off;
+      L.s_off = D.s_off;
+      D.qbuf = alloc<double>(3 * D.n_vq);
+      D.sbuf = alloc<double>(5 * D.n_sq);
+      L.qx = D.qbuf;
+      L.qy = D.qbuf + D.n_vq;
+      L.qw = D.qbuf + 2 * D.n_vq;
+      L.sx = D.sbuf;
+      L.sy = D.sbuf + D.n_sq;
+      L.sw = D.sbuf + 2 * D.n_sq;
+      L.snx = D.sbuf + 3 * D.n_sq;
+      L.sny = D.sbuf + 4 * D.n_sq;
+      if (L.n_cut) {
+        k_cut_fill<<<ceil_div(L.n_cut, 128), 128, 0, st>>>(L, prm.n_q, D.qbuf, D.qbuf + D.n_vq, D.qbuf + 2 * D.n_vq,
+                                                           D.sbuf, D.sbuf + D.n_sq, D.sbuf + 2 * D.n_sq,
+                                                           D.sbuf + 3 * D.n_sq, D.sbuf + 4 * D.n_sq);
+        CF_LAUNCHED();
+      }
+      D.ycut = alloc<double>((int64_t)L.n_cut * (p + 1) * (p + 1));
+      D.jm = alloc<double>((int64_t)L.n_ghost * p * (p + 1));
+      L.ycut = D.ycut;
+      L.jm = D.jm;
+      const int64_t nv = (int64_t)L.nl * L.ld;
+      D.x = alloc<double>(nv);
+      D.b = alloc<double>(nv);
+      D.r = alloc<double>(nv);
+      CF_CUDA(cudaMemsetAsync(D.x, 0, nv * 8, st));
+      CF_CUDA(cudaMemsetAsync(D.b, 0, nv * 8, st));
+      CF_CUDA(cudaMemsetAsync(D.r, 0, nv * 8, st));
+      sync();
+      cudaFree(flags);
+      cudaFree(tmpi);
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), (void*)flags), allocs.end());
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), (void*)tmpi), allocs.end());
+    }
+  }
+
+  void build_patches() {
+    const int p = prm.p;
+    for (int l = 0; l < prm.n_levels; ++l) {
+      LevelData& D = lv[l];
+      LevelArgs& L = D.a;
+      const int n = L.n, nv = (n + 1) * (n + 1);
+      D.vkind = alloc<uint8_t>(nv);
+      k_vertex_kind<<<dim3(ceil_div(n + 1, 16), ceil_div(n + 1, 16)), dim3(16, 16), 0, st>>>(L, D.ctype, D.vkind);
+      CF_LAUNCHED();
+      uint8_t* fl = alloc<uint8_t>(nv);
+      int* tmpi = alloc<int>(nv);
+      for (int kind = V_CART; kind <= V_CUT; ++kind) {
+        std::vector<int> all;
+        int* off = kind == V_CART ? D.cart_off : D.cutp_off;
+        int* cnt = kind == V_CART ? D.n_cart : D.n_cutp;
+        off[0] = 0;
+        std::vector<int> hostlists;
+        for (int c = 0; c < 4; ++c) {
+          k_vertex_flags<<<ceil_div(nv, 256), 256, 0, st>>>(n, D.vkind, (uint8_t)kind, c, fl);
+          CF_LAUNCHED();
+          cnt[c] = select(fl, nv, tmpi);
+          std::vector<int> h(cnt[c]);
+          if (cnt[c]) CF_CUDA(cudaMemcpyAsync(h.data(), tmpi, sizeof(int) * cnt[c], cudaMemcpyDeviceToHost, st));
+          sync();
+          hostlists.insert(hostlists.end(), h.begin(), h.end());
+          off[c + 1] = off[c] + cnt[c];
+        }
+        int* dl = alloc<int>(hostlists.size());
+        if (!hostlists.empty())
+          CF_CUDA(cudaMemcpyAsync(dl, hostlists.data(), sizeof(int) * hostlists.size(), cudaMemcpyHostToDevice, st));
+        (kind == V_CART ? D.cart_list : D.cutp_list) = dl;
+      }
+      // Cartesian tiles
+      int TP = 0;
+      CF_DISPATCH(p, TP = cart_tp<P>());
+      std::vector<int> tiles;
+      D.cart_tile_off[0] = 0;
+      for (int c = 0; c < 4; ++c) {
+        int cxo = c & 1, cyo = c >> 1;
+        int npx = (n - cxo) / 2 + 1, npy = (n - cyo) / 2 + 1;
+        int tx = ceil_div(npx, TP), ty = ceil_div(npy, TP);
+        uint8_t* tf = alloc<uint8_t>((int64_t)tx * ty);
+        int* ts = alloc<int>((int64_t)tx * ty);
+        k_tile_flags<<<ceil_div((int64_t)tx * ty, 128), 128, 0, st>>>(n, D.vkind, c, TP, tx, ty, tf);
+        CF_LAUNCHED();
+        int ns = select(tf, tx * ty, ts);
+        if (ns) {
+          k_pack_tiles<<<ceil_div(ns, 128), 128, 0, st>>>(ts, ns, tx, ts);
+          CF_LAUNCHED();
+        }
+        std::vector<int> h(ns);
+        if (ns) CF_CUDA(cudaMemcpyAsync(h.data(), ts, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+        sync();
+        tiles.insert(tiles.end(), h.begin(), h.end());
+        D.n_cart_tiles[c] = ns;
+        D.cart_tile_off[c + 1] = D.cart_tile_off[c] + ns;
+      }
+      D.cart_tiles = alloc<int>(tiles.size());
+      if (!tiles.empty())
+        CF_CUDA(cudaMemcpyAsync(D.cart_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, st));
+      // cut patch interior sets (R3)
+      const int ncp = D.cutp_off[4];
+      int* mcount = alloc<int>(ncp);
+      D.cutp_ent = alloc<int64_t>(ncp + 1);
+      if (ncp) {
+        k_cut_interior<false><<<ceil_div(ncp, 128), 128, 0, st>>>(L, D.ctype, D.cutp_list, ncp, mcount, nullptr,
+                                                                   nullptr, nullptr, nullptr);
+        CF_LAUNCHED();
+      }
+      D.n_ent = scan64(mcount, ncp, D.cutp_ent);
+      for (int c = 0; c <= 4; ++c) {
+        D.ent_col_off[c] = 0;
+        if (ncp) CF_CUDA(cudaMemcpyAsync(&D.ent_col_off[c], D.cutp_ent + D.cutp_off[c], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      }
+      sync();
+      D.ent_node = alloc<int32_t>(D.n_ent);
+      D.ent_loc = alloc<uint8_t>(D.n_ent);
+      D.ent_patch = alloc<int32_t>(D.n_ent);
+      D.zbuf = alloc<double>(D.n_ent);
+      if (ncp) {
+        k_cut_interior<true><<<ceil_div(ncp, 128), 128, 0, st>>>(L, D.ctype, D.cutp_list, ncp, nullptr, D.cutp_ent,
+                                                                  D.ent_node, D.ent_loc, D.ent_patch);
+        CF_LAUNCHED();
+      }
+      // local matrices and their inverses (P l.193, R10)
+      int* msq = alloc<int>(ncp);
+      D.cutp_inv = alloc<int64_t>(ncp + 1);
+      int mmax = 0;
+      if (ncp) {
+        k_square<<<ceil_div(ncp, 128), 128, 0, st>>>(mcount, ncp, msq);
+        CF_LAUNCHED();
+        std::vector<int> hm(ncp);
+        CF_CUDA(cudaMemcpyAsync(hm.data(), mcount, sizeof(int) * ncp, cudaMemcpyDeviceToHost, st));
+        sync();
+        for (int v : hm) mmax = std::max(mmax, v);
+      }
+      D.n_inv = scan64(msq, ncp, D.cutp_inv);
+      D.inv = alloc<double>(D.n_inv);
+      if (D.n_ent) {
+        CF_DISPATCH(p, (k_local_matrix<P, CUT_WPB><<<ceil_div(D.n_ent, CUT_WPB), 32 * CUT_WPB, 0, st>>>(
+                           L, D.cutp_list, D.cutp_ent, D.ent_loc, D.ent_patch, D.n_ent, D.cutp_inv, D.inv)));
+        CF_LAUNCHED();
+        size_t smb = (size_t)(mmax * mmax + 2 * mmax) * sizeof(double);
+        CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smb, 48 * 1024)));
+        k_batched_inverse<<<ncp, 128, smb, st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp);
+        CF_LAUNCHED();
+      }
+      sync();
+    }
+    build_coarse();
+    // CG workspace on the finest level
+    const LevelArgs& F = lv.back().a;
+    const int64_t nvf = (int64_t)F.nl * F.ld;
+    cg_x = alloc<double>(nvf);
+    cg_r = alloc<double>(nvf);
+    cg_z = alloc<double>(nvf);
+    cg_p = alloc<double>(nvf);
+    cg_q = alloc<double>(nvf);
+    part = alloc<double>(DOT_BLOCKS);
+    sc = alloc<double>(8);
+    if (!sc_host) CF_CUDA(cudaMallocHost(&sc_host, 8 * sizeof(double)));
+    for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
+    sync();
+    built = true;
+  }
+
+  void build_coarse() {
+    LevelData& D = lv[0];
+    const LevelArgs& L = D.a;
+    const int64_t nv = (int64_t)L.nl * L.ld;
+    int* nodes = alloc<int>(nv);
+    n0 = select(D.mask, (int)nv, nodes);
+    require(n0 <= 160, ERR_SIZE, "coarse level has more than 160 DoFs; use a coarser level 0");
+    c_nodes = nodes;
+    c_inv = alloc<double>((int64_t)n0 * n0);
+    double* e = alloc<double>(nv);
+    double* y = alloc<double>(nv);
+    std::vector<int> hn(n0);
+    CF_CUDA(cudaMemcpyAsync(hn.data(), nodes, sizeof(int) * n0, cudaMemcpyDeviceToHost, st));
+    sync();
+    for (int i = 0; i < n0; ++i) {
+      CF_CUDA(cudaMemsetAsync(e, 0, nv * 8, st));
+      k_set_entry<<<1, 1, 0, st>>>(e, hn[i], 1.0);
+      CF_LAUNCHED();
+      apply(0, e, y, nullptr);
+      k_gather_column<<<ceil_div(n0, 128), 128, 0, st>>>(y, nodes, n0, c_inv + (int64_t)i * n0);
+      CF_LAUNCHED();
+    }
+    int64_t* offs = alloc<int64_t>(2);
+    int64_t ho[2] = {0, n0}, hz[2] = {0, 0};
+    CF_CUDA(cudaMemcpyAsync(offs, ho, sizeof(ho), cudaMemcpyHostToDevice, st));
+    int64_t* ioff = alloc<int64_t>(2);
+    CF_CUDA(cudaMemcpyAsync(ioff, hz, sizeof(hz), cudaMemcpyHostToDevice, st));
+    size_t smb = (size_t)(n0 * n0 + 2 * n0) * sizeof(double);
+    CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smb, 48 * 1024)));
+    k_batched_inverse<<<1, 256, smb, st>>>(offs, ioff, c_inv, 1);
+    CF_LAUNCHED();
+    sync();
+  }
+
+  // ------------------------------------------------------------- hot path
+  void apply(int l, const double* x, double* y, const double* b) {
+    const LevelArgs& L = lv[l].a;
+    const int p = prm.p;
+    const int warps = L.n_cut + ceil_div(L.n_ghost, 32);
+    if (warps) {
+      CF_DISPATCH(p, (k_band<P><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+      CF_LAUNCHED();
+    }
+    CF_DISPATCH(p, (k_node_apply<P><<<dim3(ceil_div(L.ld, 32), ceil_div(L.nl, 8)), dim3(32, 8), 0, st>>>(L, x, b, y)));
+    CF_LAUNCHED();
+  }
+
+  void cart_step(int l, int c, double* x, const double* b) {
+    LevelData& D = lv[l];
+    if (!D.n_cart_tiles[c]) return;
+    CF_DISPATCH(prm.p, {
+      constexpr int TP = cart_tp<P>();
+      constexpr int W = 2 * P * TP + 1;
+      const size_t smb = 2 * W * W * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        CF_CUDA(cudaFuncSetAttribute(k_cart_colour<P, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+        attr = true;
+      }
+      k_cart_colour<P, TP><<<D.n_cart_tiles[c], TP * TP, smb, st>>>(D.a, D.cart_tiles + D.cart_tile_off[c], c,
+                                                                     D.vkind, x, b);
+    });
+    CF_LAUNCHED();
+  }
+
+  void cut_step(int l, int c, double* x, const double* b) {
+    LevelData& D = lv[l];
+    const int np = D.n_cutp[c];
+    if (!np) return;
+    const int base = D.cutp_off[c];
+    CF_DISPATCH(prm.p, (k_cut_colour_p1<P, CUT_WPB><<<ceil_div(np, CUT_WPB), 32 * CUT_WPB, 0, st>>>(
+                           D.a, D.cutp_list + base, np, base, D.cutp_ent, D.ent_loc, D.ent_node, D.cutp_inv, D.inv,
+                           x, b, D.zbuf)));
+    CF_LAUNCHED();
+    const int64_t e0 = D.ent_col_off[c], e1 = D.ent_col_off[c + 1];
+    if (e1 <= e0) return;
+    k_cut_colour_p2<<<ceil_div(e1 - e0, 256), 256, 0, st>>>(D.ent_node, D.zbuf, e0, e1, x);
+    CF_LAUNCHED();
+  }
+
+  // x <- S(x, b) (P eq. smoother-split, l.196-210; reverse = adjoint order, R9)
+  void smooth(int l, double* x, const double* b, int reverse) {
+    std::vector<std::pair<int, int>> seq;
+    for (int c = 0; c < 4; ++c) seq.push_back({0, c});
+    for (int rep = 0; rep < prm.n_c; ++rep)
+      for (int c = 0; c < 4; ++c) seq.push_back({1, c});
+    if (reverse) std::reverse(seq.begin(), seq.end());
+    for (auto& s : seq) {
+      if (s.first == 0) cart_step(l, s.second, x, b);
+      else cut_step(l, s.second, x, b);
+    }
+  }
+
+  void restrict_(int l, const double* rf, double* bc) {
+    const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
+    CF_DISPATCH(prm.p, (k_restrict<P><<<dim3(ceil_div(Lc.ld, 32), ceil_div(Lc.nl, 8)), dim3(32, 8), 0, st>>>(Lf, Lc, rf, bc)));
+    CF_LAUNCHED();
+  }
+  void prolongate_add(int l, const double* xc, double* xf) {
+    const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
+    CF_DISPATCH(prm.p, (k_prolongate_add<P><<<dim3(ceil_div(Lf.nl, 32), ceil_div(Lf.nl, 8)), dim3(32, 8), 0, st>>>(Lf, Lc, xc, xf)));
+    CF_LAUNCHED();
+  }
+  void coarse_solve(const double* b, double* x) {
+    k_coarse_solve<<<1, 256, n0 * sizeof(double), st>>>(c_inv, c_nodes, n0, b, x);
+    CF_LAUNCHED();
+  }
+
+  // V-cycle on level l with initial guess x (P l.124, l.217)
+  void vcycle(int l, double* x, const double* b) {
+    if (l == 0) {
+      coarse_solve(b, x);
+      return;
+    }
+    LevelData& D = lv[l];
+    LevelData& C = lv[l - 1];
+    smooth(l, x, b, 0);
+    apply(l, x, D.r, b);
+    restrict_(l, D.r, C.b);
+    CF_CUDA(cudaMemsetAsync(C.x, 0, (size_t)C.a.nl * C.a.ld * 8, st));
+    vcycle(l - 1, C.x, C.b);
+    prolongate_add(l, C.x, x);
+    smooth(l, x, b, prm.symmetric ? 1 : 0);
+  }
+
+  // run `body` through a cached CUDA graph keyed by (tag, ptrs)
+  template <class F>
+  void graphed(int tag, const void* p1, const void* p2, int extra, F&& body) {
+    auto key = std::make_tuple(tag, p1, p2, extra);
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+      // capture on a private stream (the legacy default stream cannot be
+      // captured); the instantiated graph is launched on the caller's stream
+      if (!cap_st) CF_CUDA(cudaStreamCreateWithFlags(&cap_st, cudaStreamNonBlocking));
+      cudaStream_t user = st;
+      st = cap_st;
+      int64_t before = g_launches;
+      cudaGraph_t g;
+      CF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        st = user;
+        throw;
+      }
+      st = user;
+      CF_CUDA(cudaStreamEndCapture(cap_st, &g));
+      GraphRec rec;
+      CF_CUDA(cudaGraphInstantiate(&rec.exec, g, 0));
+      cudaGraphDestroy(g);
+      rec.launches = g_launches - before;
+      g_launches = before;
+      it = graphs.emplace(key, rec).first;
+    }
+    CF_CUDA(cudaGraphLaunch(it->second.exec, st));
+    g_launches += it->second.launches;
+  }
+
+  void dot(const double* a, const double* b, int mode, int slot) {
+    const LevelArgs& F = lv.back().a;
+    k_dot_partial<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(a, b, (int64_t)F.nl * F.ld, part);
+    CF_LAUNCHED();
+    k_dot_final<<<1, DOT_THREADS, 0, st>>>(part, sc, mode, slot);
+    CF_LAUNCHED();
+  }
+
+  // CG preconditioned by one V-cycle (zero initial guess); x_0 = 0
+  void solve_cg(double* x, const double* b, double tol, int max_it, int* iters, double* rel) {
+    const int Lf = prm.n_levels - 1;
+    LevelData& F = lv[Lf];
+    const int64_t nv = (int64_t)F.a.nl * F.a.ld;
+    const int grid = 4 * 148;
+    k_masked_copy<<<grid, 256, 0, st>>>(cg_r, b, F.mask, nv);
+    CF_LAUNCHED();
+    CF_CUDA(cudaMemsetAsync(cg_x, 0, nv * 8, st));
+    dot(cg_r, cg_r, 0, 3);
+    CF_CUDA(cudaMemcpyAsync(sc_host, sc, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    sync();
+    const double r0 = std::sqrt(sc_host[3]);
+    int it = 0;
+    double rn = r0;
+    if (r0 > 0.0) {
+      auto precond = [&]() {
+        CF_CUDA(cudaMemsetAsync(cg_z, 0, nv * 8, st));
+        vcycle(Lf, cg_z, cg_r);
+      };
+      graphed(100, cg_z, cg_r, 0, [&]() {
+        precond();
+        dot(cg_r, cg_z, 0, 0);
+        CF_CUDA(cudaMemcpyAsync(cg_p, cg_z, nv * 8, cudaMemcpyDeviceToDevice, st));
+      });
+      while (it < max_it) {
+        graphed(101, cg_p, cg_q, 0, [&]() {
+          apply(Lf, cg_p, cg_q, nullptr);
+          dot(cg_p, cg_q, 1, 0);
+          k_cg_update<<<grid, 256, 0, st>>>(cg_x, cg_r, cg_p, cg_q, sc, nv);
+          CF_LAUNCHED();
+          dot(cg_r, cg_r, 0, 3);
+          CF_CUDA(cudaMemcpyAsync(sc_host, sc, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        });
+        sync();
+        ++it;
+        rn = std::sqrt(sc_host[3]);
+        if (!(rn > tol * r0)) break;
+        graphed(102, cg_z, cg_r, 0, [&]() {
+          precond();
+          dot(cg_r, cg_z, 2, 0);
+          k_cg_direction<<<grid, 256, 0, st>>>(cg_p, cg_z, sc, nv);
+          CF_LAUNCHED();
+        });
+      }
+    }
+    CF_CUDA(cudaMemcpyAsync(x, cg_x, nv * 8, cudaMemcpyDeviceToDevice, st));
+    sync();
+    if (iters) *iters = it;
+    if (rel) *rel = r0 > 0.0 ? rn / r0 : 0.0;
+  }
+};
+
+}  // namespace cf
