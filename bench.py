@@ -1,0 +1,283 @@
+"""Benchmark of the hot path: one smoothing step of the coloured vertex-patch
+smoother (PAPER.md eq. smoother-split) on the finest level of BASELINE.json
+configs[1] (2D circle, Q2, 512x512 background mesh, fp64), plus V-cycle and
+CG+MG time-to-solution.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `value` = active DoFs x steps x ranks / max
+over ranks of the device time of the timed steps (CUDA events on the
+launching stream, L2 flushed between timed steps).  N > 1 runs independent
+replicas (one problem per GPU, no data-path collective; DESIGN.md
+"Multi-GPU").  `--impl reference` times the CPU oracle (as it stands) on a
+bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "smoother DoF/s (one multiplicative vertex-patch smoothing step, finest level)"
+UNIT = "DoF/s"
+WORKLOAD = workloads.CONFIG1
+ORACLE_SAMPLE_LEVEL = 6           # 128 x 128 cells of the same hierarchy (bounded CPU sample)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def clock_sampler_start(path):
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    try:
+        return subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                                stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except Exception:
+        return None
+
+
+def clock_sampler_stop(proc, path, gpu_index):
+    if proc is None:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    proc.terminate()
+    proc.wait()
+    sm, smax, reasons = [], None, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 9 or f[0] != str(gpu_index):
+            continue
+        try:
+            sm.append(float(f[1]))
+            smax = float(f[2])
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[5:9]):
+            if v.lower().startswith("active"):
+                reasons.add(nm)
+    load = [s for s in sm if smax and s > 0.5 * smax] or sm
+    return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_sample(steps):
+    """Time the oracle smoothing step on a bounded sample of the workload."""
+    from oracle.solver import from_workload
+    w = workloads.Workload(WORKLOAD.name + f"-level{ORACLE_SAMPLE_LEVEL}", WORKLOAD.x0, WORKLOAD.y0, WORKLOAD.length,
+                           WORKLOAD.n_coarse, ORACLE_SAMPLE_LEVEL + 1, WORKLOAD.cx, WORKLOAD.cy, WORKLOAD.r,
+                           WORKLOAD.p, WORKLOAD.n_c)
+    h = from_workload(w)
+    ld = h.fine
+    lv = ld.lv
+    b = workloads.lattice_vector(w, 2)[lv.dof_nodes]
+    x = workloads.lattice_vector(w, 1)[lv.dof_nodes]
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        ld.smooth(x, b, w.n_c)
+        times.append(time.perf_counter() - t0)
+    sec = float(np.mean(times))
+    return {"value": lv.n_dofs / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle smoothing step on level {ORACLE_SAMPLE_LEVEL} ({lv.n}x{lv.n} cells, {lv.n_dofs} DoFs) "
+                      f"of the {WORKLOAD.name} hierarchy, mean of {len(times)} steps, numpy/scipy single process"}, sec
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 5))
+    for _ in range(min(args.warmup, 1)):
+        pass
+    cb, sec = oracle_sample(steps)
+    out = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": WORKLOAD.name, "sample_level": ORACLE_SAMPLE_LEVEL},
+           "cpu_baseline": cb,
+           "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    args.warmup = max(3, args.warmup)
+
+    import torch
+    from paper_2508_11608_b200 import cutfem
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+
+    w = WORKLOAD
+    g = cutfem.Problem.from_workload(w)
+    L = w.n_levels - 1
+    info = g.level_info(L)
+    nl, ld = info.nl, info.ld
+    n_dofs = info.n_dofs
+    x0 = g.to_device(workloads.lattice_vector(w, 1))
+    b = g.to_device(workloads.lattice_vector(w, 2))
+    x = x0.clone()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 512 MB > 126 MB L2
+
+    def timed(fn, steps, warmup, per_step_flush=True):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for s, e in ev:
+            if per_step_flush:
+                flush.fill_(1.0)
+            s.record(stream)
+            fn()
+            e.record(stream)
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in ev]
+
+    # ---- headline: one smoothing step (device-resident inputs)
+    smooth = lambda: g.smooth(L, x, b)
+    for _ in range(args.warmup):
+        smooth()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk_path = tempfile.mktemp(suffix=".csv")
+    clk = clock_sampler_start(clk_path) if rank == 0 else None
+    time.sleep(0.3 if clk else 0)
+    l0 = cutfem.launch_count()
+    ms = timed(smooth, args.steps, 0)
+    launches = cutfem.launch_count() - l0
+    torch.cuda.synchronize()
+    clocks = clock_sampler_stop(clk, clk_path, local) if rank == 0 else None
+    total_ms = float(sum(ms))
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    value = n_dofs * args.steps * world / (total_ms * 1e-3)
+
+    # ---- dominant kernel: Cartesian colour step, timed alone (live, CUDA events)
+    kms = []
+    n_cart = list(info.n_cart)
+    for c in range(4):
+        kms.append(timed(lambda: g.colour_step(L, 0, c, x, b), 50, 3))
+    cart_ms = float(np.mean([np.mean(k) for k in kms]))
+    p = w.p
+    bytes_per_patch = 8 * ((2 * p) ** 2 + 2 * (2 * p - 1) ** 2)
+    cart_bytes = bytes_per_patch * float(np.mean(n_cart))
+    peak, peak_src = measured_peak_hbm()
+    achieved = cart_bytes / (cart_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "cart_colour_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("bytes_per_launch")
+
+    # ---- V-cycle and CG+MG time to solution
+    z = g.zeros()
+    vms = timed(lambda: (z.zero_(), g.vcycle(z, b)), 20, 3)
+    v_ms = float(np.median(vms))
+    xs = g.zeros()
+    torch.cuda.synchronize()
+    it, rel = g.solve_cg_mg(xs, b, tol=w.tol)  # warm (graph capture)
+    t_cg = []
+    for _ in range(3):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        it, rel = g.solve_cg_mg(xs, b, tol=w.tol)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        t_cg.append(t0.elapsed_time(t1))
+    cg_ms = float(np.median(t_cg))
+
+    # ---- e2e: the same smoothing step through the C ABI with pinned host buffers
+    xh = torch.empty(nl * ld, dtype=torch.float64).pin_memory()
+    bh = torch.empty(nl * ld, dtype=torch.float64).pin_memory()
+    xh.copy_(x0.cpu())
+    bh.copy_(b.cpu())
+    xn, bn = xh.numpy(), bh.numpy()
+    e2e_steps = max(5, min(args.steps, 100))
+    for _ in range(3):
+        g.smooth_host(L, xn, bn)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        g.smooth_host(L, xn, bn)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e = {"value": n_dofs * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * nl * ld * 8,
+           "d2h_bytes_per_step": nl * ld * 8}
+
+    if rank == 0:
+        cb = None
+        if not args.no_cpu_baseline:
+            cb, _ = oracle_sample(2)
+            cb["cores"] = 1
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded N(0,1) x0 and b on the lattice; analytic circle level set)",
+            "config": {"workload": w.name, "box": [w.x0, w.x0 + w.length], "circle_r": w.r, "degree": w.p,
+                       "cells_per_side": info.n, "levels": w.n_levels, "n_dofs": int(n_dofs), "n_c": w.n_c,
+                       "l2": "flushed (512 MB write) before every timed step",
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "roofline": {"bound": "hbm", "kernel": f"k_cart_colour<P={p}> (Cartesian colour step)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": cart_bytes, "avg_launch_ms": cart_ms},
+            "vcycle": {"ms": v_ms, "dofs_per_s": n_dofs / (v_ms * 1e-3)},
+            "cg_mg": {"time_to_solution_ms": cg_ms, "iterations": it, "rel_residual": rel, "tol": w.tol,
+                      "dofs_per_s": n_dofs / (cg_ms * 1e-3)},
+            "e2e": e2e,
+            "cpu_baseline": cb,
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
