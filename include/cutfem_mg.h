@@ -61,6 +61,8 @@ typedef struct {
   int n_q;              /* Gauss points per direction on cut cells; 0 selects p+1 (R6) */
   int n_c;              /* sweeps over cut patches per smoothing step (P l.203; >= 1) */
   int symmetric;        /* 1: post-smoother = reverse colour order (R9, needed by CG) */
+  int cut_mode;         /* cut-cell operator: 0 = element matrix of bulk + Nitsche terms precomputed
+                           from the cut quadrature at setup, 1 = quadrature on the fly */
 } cutfem_params;
 
 /* Per-level sizes and counts. */

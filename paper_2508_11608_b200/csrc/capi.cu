@@ -68,6 +68,8 @@ int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* ou
     P.n_q = prm->n_q > 0 ? prm->n_q : P.p + 1;
     P.n_c = prm->n_c;
     P.symmetric = prm->symmetric;
+    cf::require(prm->cut_mode == 0 || prm->cut_mode == 1, cf::ERR_ARG, "cut_mode must be 0 or 1");
+    P.cut_mode = prm->cut_mode;
     use_stream(pb, stream);
     try {
       pb->p.setup_mesh();

@@ -64,6 +64,7 @@ struct LevelArgs {
   int n_ghost;
   double* ycut;                      // n_cut * (p+1)^2 scratch (operator apply)
   double* jm;                        // n_ghost * p * (p+1) scratch (operator apply)
+  const double* ecut;                // n_cut * ((p+1)^2)^2 cut-cell matrices (bulk + Nitsche), cut_mode 0
 };
 
 // Per-level device data owned by the problem.
@@ -93,6 +94,8 @@ struct LevelData {
   int n_cart_tiles[4] = {0, 0, 0, 0};
   int* cart_tiles = nullptr;         // per colour concatenated, packed ti + 65536 tj
   int cart_tile_off[5] = {0, 0, 0, 0, 0};
+  int* fused_tiles = nullptr;        // TC x TC cell tiles for the fused Cartesian sweep
+  int n_fused_tiles = 0;
   int n_cutp[4] = {0, 0, 0, 0};
   int cutp_off[5] = {0, 0, 0, 0, 0};
   int* cutp_list = nullptr;          // packed I + (n+1) J
@@ -106,13 +109,15 @@ struct LevelData {
   double* inv = nullptr;             // local inverses, m_j^2 each, row-major (symmetric)
   int64_t n_inv = 0;
   double* zbuf = nullptr;            // n_ent corrections (two-phase cut colour step)
+  double* ecut = nullptr;            // cut-cell element matrices
+  void* desc = nullptr;              // CutDesc per cut patch (smoother2.cuh)
   // workspace lattice vectors for the V-cycle
   double *x = nullptr, *b = nullptr, *r = nullptr;
 };
 
 struct Params {
   double x0, y0, length, cx, cy, r, gamma_D, gamma_k[CF_MAXP];
-  int n_coarse, n_levels, p, sigma, n_q, n_c, symmetric;
+  int n_coarse, n_levels, p, sigma, n_q, n_c, symmetric, cut_mode;
 };
 
 // launch accounting for the bench's gpu_launches claim

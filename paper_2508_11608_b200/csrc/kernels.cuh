@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(TP* TP) k_cart_colour(LevelArgs L, const int* 
 // ---------------------------------------------------------------------------
 // Operator A x, pass 1: cut cells (warp each, quadrature) and ghost faces
 // (thread each, jump moments) into the level's scratch buffers.
-template <int P>
+template <int P, bool QUAD>
 __global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x) {
   constexpr int NB = (P + 1) * (P + 1);
   __shared__ double sX[4][NB];
@@ -474,11 +474,19 @@ __global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x) {
     for (int t = lane; t < NB; t += 32)
       sX[w][t] = x[(size_t)(j * P + t / (P + 1)) * L.ld + i * P + t % (P + 1)];
     __syncwarp();
-    double acc[NB];
-    cut_cell_warp<P>(L, gw, sX[w], P + 1, acc);
+    if (QUAD) {
+      double acc[NB];
+      cut_cell_warp<P>(L, gw, sX[w], P + 1, acc);
 #pragma unroll
-    for (int t = 0; t < NB; ++t)
-      if (lane == t) L.ycut[(size_t)gw * NB + t] = acc[t];
+      for (int t = 0; t < NB; ++t)
+        if (lane == t) L.ycut[(size_t)gw * NB + t] = acc[t];
+    } else if (lane < NB) {
+      const double* Er = L.ecut + ((size_t)gw * NB + lane) * NB;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < NB; ++l) s = fma(Er[l], sX[w][l], s);
+      L.ycut[(size_t)gw * NB + lane] = s;
+    }
     return;
   }
   const int g = (gw - L.n_cut) * 32 + lane;

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -16,6 +17,7 @@
 
 #include "internal.cuh"
 #include "kernels.cuh"
+#include "smoother2.cuh"
 #include "tables.cuh"
 
 namespace cf {
@@ -31,8 +33,9 @@ int64_t g_launches = 0;
     default: throw Error(ERR_ARG, "degree must be 1..4"); \
   }
 
-template <int P> constexpr int cart_tp() { return P <= 2 ? 16 : 8; }
+template <int P> constexpr int cart_tp() { return P == 1 ? 16 : (P == 2 ? 8 : (P == 3 ? 7 : 6)); }
 constexpr int CUT_WPB = 4;
+template <int P> constexpr int fused_tc() { return P == 1 ? 32 : (P <= 3 ? 16 : 8); }
 
 struct GraphRec {
   cudaGraphExec_t exec = nullptr;
@@ -45,6 +48,8 @@ struct Problem {
   cudaStream_t st = nullptr;
   cudaStream_t cap_st = nullptr;
   bool built = false;
+  bool persistent = false;  // one cooperative launch per smoothing step (env CUTFEM_PERSISTENT=1)
+  bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -127,9 +132,31 @@ struct Problem {
     return tot;
   }
 
+  // launch with programmatic dependent launch (PDL) when enabled: the kernel
+  // may start while its predecessor drains; it calls griddepcontrol.wait
+  // before touching data the predecessor writes
+  bool pdl = true;
+  template <typename... KArgs, typename... Args>
+  void launch(void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CF_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
+  }
+
   // ---------------------------------------------------------------- setup
   void setup_mesh() {
     host::upload_tables();
+    if (const char* e = std::getenv("CUTFEM_PERSISTENT")) persistent = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_FUSED")) fused = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_PDL")) pdl = std::atoi(e) != 0;
     d_count = alloc<int>(1);
     const int p = prm.p;
     lv.resize(prm.n_levels);
@@ -239,6 +266,15 @@ struct Problem {
                                                            D.sbuf + 3 * D.n_sq, D.sbuf + 4 * D.n_sq);
         CF_LAUNCHED();
       }
+      {
+        const int NB = (p + 1) * (p + 1);
+        D.ecut = alloc<double>((int64_t)L.n_cut * NB * NB);
+        L.ecut = D.ecut;
+        if (L.n_cut) {
+          CF_DISPATCH(p, (k_cut_elem<P><<<ceil_div((int64_t)L.n_cut * NB, 4), 128, 0, st>>>(L, D.ecut)));
+          CF_LAUNCHED();
+        }
+      }
       D.ycut = alloc<double>((int64_t)L.n_cut * (p + 1) * (p + 1));
       D.jm = alloc<double>((int64_t)L.n_ghost * p * (p + 1));
       L.ycut = D.ycut;
@@ -315,6 +351,21 @@ struct Problem {
         D.n_cart_tiles[c] = ns;
         D.cart_tile_off[c + 1] = D.cart_tile_off[c] + ns;
       }
+      {
+        int TC = 0;
+        CF_DISPATCH(p, TC = fused_tc<P>());
+        const int tx = ceil_div(n, TC), nt = tx * tx;
+        uint8_t* tf = alloc<uint8_t>(nt);
+        int* ts = alloc<int>(nt);
+        k_fused_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(n, D.vkind, TC, tx, tf, nt);
+        CF_LAUNCHED();
+        D.n_fused_tiles = select(tf, nt, ts);
+        if (D.n_fused_tiles) {
+          k_pack_tiles<<<ceil_div(D.n_fused_tiles, 128), 128, 0, st>>>(ts, D.n_fused_tiles, tx, ts);
+          CF_LAUNCHED();
+        }
+        D.fused_tiles = ts;
+      }
       D.cart_tiles = alloc<int>(tiles.size());
       if (!tiles.empty())
         CF_CUDA(cudaMemcpyAsync(D.cart_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, st));
@@ -363,6 +414,12 @@ struct Problem {
         size_t smb = (size_t)(mmax * mmax + 2 * mmax) * sizeof(double);
         CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smb, 48 * 1024)));
         k_batched_inverse<<<ncp, 128, smb, st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp);
+        CF_LAUNCHED();
+      }
+      D.desc = alloc<CutDesc>(ncp);
+      if (ncp) {
+        CF_DISPATCH(p, (k_cut_desc<P><<<ceil_div(ncp, 128), 128, 0, st>>>(L, D.cutp_list, ncp, D.cutp_ent, D.ent_loc,
+                                                                          D.cutp_inv, (CutDesc*)D.desc)));
         CF_LAUNCHED();
       }
       sync();
@@ -424,7 +481,11 @@ struct Problem {
     const int p = prm.p;
     const int warps = L.n_cut + ceil_div(L.n_ghost, 32);
     if (warps) {
-      CF_DISPATCH(p, (k_band<P><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+      if (prm.cut_mode == 0) {
+        CF_DISPATCH(p, (k_band<P, false><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+      } else {
+        CF_DISPATCH(p, (k_band<P, true><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+      }
       CF_LAUNCHED();
     }
     CF_DISPATCH(p, (k_node_apply<P><<<dim3(ceil_div(L.ld, 32), ceil_div(L.nl, 8)), dim3(32, 8), 0, st>>>(L, x, b, y)));
@@ -436,15 +497,14 @@ struct Problem {
     if (!D.n_cart_tiles[c]) return;
     CF_DISPATCH(prm.p, {
       constexpr int TP = cart_tp<P>();
-      constexpr int W = 2 * P * TP + 1;
-      const size_t smb = 2 * W * W * sizeof(double);
+      const size_t smb = CartSmem<P, TP>::doubles * sizeof(double);
       static bool attr = false;
       if (!attr) {
-        CF_CUDA(cudaFuncSetAttribute(k_cart_colour<P, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+        CF_CUDA(cudaFuncSetAttribute(k_cart_colour_v2<P, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
         attr = true;
       }
-      k_cart_colour<P, TP><<<D.n_cart_tiles[c], TP * TP, smb, st>>>(D.a, D.cart_tiles + D.cart_tile_off[c], c,
-                                                                     D.vkind, x, b);
+      k_cart_colour_v2<P, TP><<<D.n_cart_tiles[c], TP * TP * (2 * P - 1), smb, st>>>(
+          D.a, D.cart_tiles + D.cart_tile_off[c], c, D.vkind, x, b);
     });
     CF_LAUNCHED();
   }
@@ -454,18 +514,116 @@ struct Problem {
     const int np = D.n_cutp[c];
     if (!np) return;
     const int base = D.cutp_off[c];
-    CF_DISPATCH(prm.p, (k_cut_colour_p1<P, CUT_WPB><<<ceil_div(np, CUT_WPB), 32 * CUT_WPB, 0, st>>>(
-                           D.a, D.cutp_list + base, np, base, D.cutp_ent, D.ent_loc, D.ent_node, D.cutp_inv, D.inv,
-                           x, b, D.zbuf)));
+    const CutDesc* desc = (const CutDesc*)D.desc + base;
+    CF_DISPATCH(prm.p, {
+      const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
+      const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
+      const size_t smb = wpb * pw;
+      static bool attr = false;
+      if (!attr) {
+        CF_CUDA(cudaFuncSetAttribute(k_cut_colour_v3<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CF_CUDA(cudaFuncSetAttribute(k_cut_colour_v3<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+      }
+      if (prm.cut_mode == 0)
+        launch(k_cut_colour_v3<P, false>, dim3(ceil_div(np, wpb)), dim3(128), smb, D.a, desc, np, (const double*)D.ecut,
+               (const double*)D.inv, (const double*)x, b, D.zbuf, wpb);
+      else
+        launch(k_cut_colour_v3<P, true>, dim3(ceil_div(np, wpb)), dim3(128), smb, D.a, desc, np, (const double*)D.ecut,
+               (const double*)D.inv, (const double*)x, b, D.zbuf, wpb);
+    });
     CF_LAUNCHED();
     const int64_t e0 = D.ent_col_off[c], e1 = D.ent_col_off[c + 1];
     if (e1 <= e0) return;
-    k_cut_colour_p2<<<ceil_div(e1 - e0, 256), 256, 0, st>>>(D.ent_node, D.zbuf, e0, e1, x);
+    launch(k_cut_apply, dim3(ceil_div(e1 - e0, 256)), dim3(256), 0, (const int32_t*)D.ent_node, (const double*)D.zbuf,
+           e0, e1, x);
+    CF_LAUNCHED();
+  }
+
+  // one cooperative launch for the whole smoothing step
+  void smooth_persistent(int l, double* x, const double* b, int reverse) {
+    LevelData& D = lv[l];
+    SmoothArgs A;
+    A.L = D.a;
+    A.tiles = D.cart_tiles;
+    A.desc = (const CutDesc*)D.desc;
+    for (int c = 0; c < 5; ++c) {
+      A.tile_off[c] = D.cart_tile_off[c];
+      A.cut_off[c] = D.cutp_off[c];
+      A.ent_off_c[c] = D.ent_col_off[c];
+    }
+    A.ent_node = D.ent_node;
+    A.ecut = D.ecut;
+    A.inv = D.inv;
+    A.vk = D.vkind;
+    A.zbuf = D.zbuf;
+    A.x = x;
+    A.b = b;
+    A.n_c = prm.n_c;
+    A.reverse = reverse;
+    CF_DISPATCH(prm.p, {
+      constexpr int TP = cart_tp<P>();
+      const size_t pw = CutSmem<P>::per_warp * sizeof(double);
+      A.cut_wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (110 * 1024) / pw));
+      const size_t smb = std::max<size_t>(CartSmem<P, TP>::doubles * sizeof(double), A.cut_wpb * pw);
+      void* fn = prm.cut_mode == 0 ? (void*)k_smooth_persistent<P, TP, false> : (void*)k_smooth_persistent<P, TP, true>;
+      static int max_blocks = -1;
+      if (max_blocks < 0) {
+        int nsm = 0, dev = 0, per_sm = 1 << 30;
+        CF_CUDA(cudaGetDevice(&dev));
+        CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        for (void* f : {(void*)k_smooth_persistent<P, TP, false>, (void*)k_smooth_persistent<P, TP, true>}) {
+          CF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+          int b = 0;
+          CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, 256, smb));
+          per_sm = std::min(per_sm, b);
+        }
+        max_blocks = std::max(1, per_sm * nsm);
+      }
+      int need = 1;
+      for (int c = 0; c < 4; ++c) {
+        need = std::max(need, D.n_cart_tiles[c]);
+        need = std::max(need, ceil_div(D.n_cutp[c], A.cut_wpb));
+      }
+      const int grid = std::min(need, max_blocks);
+      void* args[] = {&A};
+      CF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, smb, st));
+    });
+    CF_LAUNCHED();
+  }
+
+  // all four Cartesian colours in one launch (temporal blocking)
+  void cart_fused(int l, double* x, const double* b, int reverse) {
+    LevelData& D = lv[l];
+    if (!D.n_fused_tiles) return;
+    CF_DISPATCH(prm.p, {
+      constexpr int TC = fused_tc<P>();
+      const size_t smb = CartFusedSmem<P, TC>::doubles * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        CF_CUDA(cudaFuncSetAttribute(k_cart_fused<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+        attr = true;
+      }
+      launch(k_cart_fused<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
+             (const uint8_t*)D.vkind, x, b, reverse);
+    });
     CF_LAUNCHED();
   }
 
   // x <- S(x, b) (P eq. smoother-split, l.196-210; reverse = adjoint order, R9)
   void smooth(int l, double* x, const double* b, int reverse) {
+    if (persistent) {
+      smooth_persistent(l, x, b, reverse);
+      return;
+    }
+    if (fused) {
+      if (!reverse) cart_fused(l, x, b, 0);
+      for (int rep = 0; rep < prm.n_c; ++rep)
+        for (int c = 0; c < 4; ++c) cut_step(l, reverse ? 3 - c : c, x, b);
+      if (reverse) cart_fused(l, x, b, 1);
+      return;
+    }
     std::vector<std::pair<int, int>> seq;
     for (int c = 0; c < 4; ++c) seq.push_back({0, c});
     for (int rep = 0; rep < prm.n_c; ++rep)

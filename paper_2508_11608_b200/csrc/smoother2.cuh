@@ -1,0 +1,804 @@
+// smoother2.cuh — latency-optimised smoother kernels (round 1, v2).
+//
+// Cut patches (P l.193): one warp per patch, one 64-byte descriptor per patch
+// (window cell kinds, cut-cell ids, interior-set bit mask, offsets) so that
+// after one broadcast load every other load of the patch (x window, b, the
+// cut-cell matrices, the local inverse) is issued at once with cp.async into
+// shared memory.  The cut-cell operator is either the element matrix of the
+// bulk + Nitsche terms precomputed from the cut quadrature at setup
+// (cut_mode 0) or the quadrature evaluated on the fly (cut_mode 1).
+//
+// Cartesian patches (P l.189, l.192): (2p-1) threads per patch (one per
+// interior row / column of the fast-diagonalisation passes) so a colour
+// keeps ~3x more warps in flight than one thread per patch.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+
+namespace cf {
+
+struct __align__(16) CutDesc {
+  int I, J;
+  uint32_t kinds;          // 2 bits per cell of the 4x4 window (I-2..I+1) x (J-2..J+1), index wy*4 + wx
+  int e0;                  // first entry (interior DoF) of the patch
+  int cid[4];              // cut-cell ids of the patch cells (dx + 2 dy), -1 if not cut
+  long long inv_off;       // offset of A_j^{-1}
+  unsigned long long mask[2];  // interior set as bits over the (2p+1)^2 block, row-major
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// PDL: wait until the preceding kernel in the stream has completed (no-op
+// when launched without the programmatic-serialization attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// PDL: allow the next kernel in the stream to be scheduled (its own wait
+// still orders it after this kernel's completion)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+__device__ __forceinline__ int desc_kind(const CutDesc& d, int wx, int wy) {
+  return (d.kinds >> (2 * (wy * 4 + wx))) & 3;
+}
+
+// ---- setup: cut-cell element matrices E_c = bulk + Nitsche (P eq. cutfem_nitsche)
+// from the cut quadrature (R6); one warp per (cut cell, column).
+template <int P>
+__global__ void __launch_bounds__(128) k_cut_elem(LevelArgs L, double* E) {
+  constexpr int NB = (P + 1) * (P + 1);
+  __shared__ double sX[4][NB];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t g = blockIdx.x * 4LL + w;
+  if (g >= (int64_t)L.n_cut * NB) return;
+  const int cid = (int)(g / NB), col = (int)(g % NB);
+  for (int t = lane; t < NB; t += 32) sX[w][t] = t == col ? 1.0 : 0.0;
+  __syncwarp();
+  double acc[NB];
+  cut_cell_warp<P>(L, cid, sX[w], P + 1, acc);
+#pragma unroll
+  for (int t = 0; t < NB; ++t)
+    if (lane == t) E[((int64_t)cid * NB + t) * NB + col] = acc[t];
+}
+
+// ---- setup: descriptors of the cut patches (all colours, list order)
+template <int P>
+__global__ void k_cut_desc(LevelArgs L, const int* plist, int np, const int64_t* ent_off, const uint8_t* ent_loc,
+                           const int64_t* inv_off, CutDesc* desc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  const int n = L.n;
+  CutDesc d;
+  d.I = plist[k] % (n + 1);
+  d.J = plist[k] / (n + 1);
+  d.kinds = 0;
+  for (int wy = 0; wy < 4; ++wy)
+    for (int wx = 0; wx < 4; ++wx)
+      d.kinds |= (uint32_t)cell_kind(L, L.ctype, d.I - 2 + wx, d.J - 2 + wy) << (2 * (wy * 4 + wx));
+  for (int q = 0; q < 4; ++q) {
+    int ci = d.I - 1 + (q & 1), cj = d.J - 1 + (q >> 1);
+    d.cid[q] = cell_kind(L, L.ctype, ci, cj) == CUT ? L.cut_id[cj * n + ci] : -1;
+  }
+  d.e0 = (int)ent_off[k];
+  d.inv_off = inv_off[k];
+  d.mask[0] = d.mask[1] = 0ull;
+  for (int64_t e = ent_off[k]; e < ent_off[k + 1]; ++e) {
+    int loc = ent_loc[e];
+    d.mask[loc >> 6] |= 1ull << (loc & 63);
+  }
+  desc[k] = d;
+}
+
+__device__ __forceinline__ int mask_count(const CutDesc& d) { return __popcll(d.mask[0]) + __popcll(d.mask[1]); }
+
+// i-th set bit of the 128-bit interior mask (block-local index)
+__device__ __forceinline__ int mask_select(const CutDesc& d, int i) {
+  int c0 = __popcll(d.mask[0]);
+  unsigned long long m = i < c0 ? d.mask[0] : d.mask[1];
+  int base = i < c0 ? 0 : 64;
+  int r = i < c0 ? i : i - c0;
+  for (int t = 0; t < r; ++t) m &= m - 1;
+  return base + __ffsll((long long)m) - 1;
+}
+
+template <int P>
+struct CutSmem {
+  static constexpr int NB = (P + 1) * (P + 1), BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS;
+  static constexpr int per_warp = WS * WS + MM + MM + P * (P + 1) + MM * MM + 4 * NB * NB;
+};
+
+// Cut-patch colour step, phase 1 (v2): z_j = A_j^{-1} (b - A x)|_{I_j}.
+// One warp: z = A_j^{-1} (b - A x)|_{I_j} for the patch of descriptor d,
+// written to zbuf[d.e0 ...]; Wp = this warp's CutSmem<P>::per_warp doubles.
+template <int P, bool QUAD>
+__device__ void cut_patch_z(const LevelArgs& L, const CutDesc& d, const double* ecut, const double* inv,
+                            const double* x, const double* b, double* zbuf, const SmTab& T, double* Wp) {
+  constexpr int NB = (P + 1) * (P + 1), BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS;
+  const int lane = threadIdx.x & 31;
+  double* Yb = Wp + WS * WS;
+  double* Rr = Yb + MM;
+  double* Js = Rr + MM;
+  double* Ai = Js + P * (P + 1);
+  double* Ec = Ai + MM * MM;
+  const int m = mask_count(d);
+  // ---- issue every load of the patch
+  for (int e = lane; e < WS * WS; e += 32) {
+    int a = P * (d.I - 2) + e % WS, bb = P * (d.J - 2) + e / WS;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, x + (size_t)bb * L.ld + a);
+    else Wp[e] = 0.0;
+  }
+  const double* Ag = inv + d.inv_off;
+  for (int e = lane; e < m * m; e += 32) cp_async8(Ai + e, Ag + e);
+  if (!QUAD) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (d.cid[q] >= 0)
+        for (int e = lane; e < NB * NB; e += 32) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
+  }
+  double bi[(MM + 31) / 32];
+#pragma unroll
+  for (int t = 0; t < (MM + 31) / 32; ++t) {
+    int i = lane + 32 * t;
+    bi[t] = 0.0;
+    if (i < m) {
+      int loc = mask_select(d, i);
+      bi[t] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
+    }
+  }
+  for (int e = lane; e < MM; e += 32) Yb[e] = 0.0;
+  cp_async_wait_all();
+  __syncwarp();
+  // ---- (A x) on the block rows: patch cells, then ghost faces
+  const int kx = lane % (P + 1), ky = lane / (P + 1);
+  for (int q = 0; q < 4; ++q) {
+    const int dx = q & 1, dy = q >> 1;
+    const int kind = desc_kind(d, dx + 1, dy + 1);
+    if (kind == OUTSIDE) continue;
+    const double* X = Wp + (P * (dy + 1)) * WS + P * (dx + 1);
+    if (kind == INSIDE) {
+      if (lane < NB) Yb[(P * dy + ky) * BS + P * dx + kx] += inside_row<P>(T, X, WS, kx, ky);
+    } else if (QUAD) {
+      double acc[NB];
+      cut_cell_warp<P>(L, d.cid[q], X, WS, acc);
+#pragma unroll
+      for (int t = 0; t < NB; ++t)
+        if (lane == t) Yb[(P * dy + ky) * BS + P * dx + kx] += acc[t];
+    } else if (lane < NB) {
+      const double* Er = Ec + q * NB * NB + lane * NB;
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < NB; ++l) s = fma(Er[l], X[(l / (P + 1)) * WS + l % (P + 1)], s);
+      Yb[(P * dy + ky) * BS + P * dx + kx] += s;
+    }
+    __syncwarp();
+  }
+  const int I = d.I, J = d.J;
+  for (int axis = 0; axis < 2; ++axis)
+    for (int s = 0; s < 3; ++s)
+      for (int t = 0; t < 2; ++t) {
+        int i1, j1, i2, j2;
+        if (axis == 0) {
+          i1 = I - 2 + s; j1 = J - 1 + t; i2 = i1 + 1; j2 = j1;
+        } else {
+          i1 = I - 1 + t; j1 = J - 2 + s; i2 = i1; j2 = j1 + 1;
+        }
+        const int k1 = desc_kind(d, i1 - (I - 2), j1 - (J - 2)), k2 = desc_kind(d, i2 - (I - 2), j2 - (J - 2));
+        if (k1 == OUTSIDE || k2 == OUTSIDE || (k1 != CUT && k2 != CUT)) continue;
+        const double* X1 = Wp + ((j1 - (J - 2)) * P) * WS + (i1 - (I - 2)) * P;
+        const double* X2 = Wp + ((j2 - (J - 2)) * P) * WS + (i2 - (I - 2)) * P;
+        double Jm[P + 1][P + 1];
+        face_moments<P>(axis, X1, X2, WS, Jm);
+        if (lane == 0) {
+#pragma unroll
+          for (int kk = 1; kk <= P; ++kk)
+#pragma unroll
+            for (int qq = 0; qq <= P; ++qq) Js[(kk - 1) * (P + 1) + qq] = Jm[kk][qq];
+        }
+        __syncwarp();
+        const bool in1 = i1 >= I - 1 && i1 <= I && j1 >= J - 1 && j1 <= J;
+        const bool in2 = i2 >= I - 1 && i2 <= I && j2 >= J - 1 && j2 <= J;
+        if (lane < NB) {
+          if (in1) Yb[((j1 - (J - 1)) * P + ky) * BS + (i1 - (I - 1)) * P + kx] += face_test<P>(L, T, axis, 1, kx, ky, Js);
+          if (in2) Yb[((j2 - (J - 1)) * P + ky) * BS + (i2 - (I - 1)) * P + kx] += face_test<P>(L, T, axis, 2, kx, ky, Js);
+        }
+        __syncwarp();
+      }
+  // ---- r = b - A x on the interior set, z = A_j^{-1} r
+#pragma unroll
+  for (int t = 0; t < (MM + 31) / 32; ++t) {
+    int i = lane + 32 * t;
+    if (i < m) Rr[i] = bi[t] - Yb[mask_select(d, i)];
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) {
+    double z = 0.0;
+    for (int q = 0; q < m; ++q) z = fma(Ai[q * m + i], Rr[q], z);
+    zbuf[d.e0 + i] = z;
+  }
+  __syncwarp();
+}
+
+template <int P, bool QUAD>
+__global__ void __launch_bounds__(128) k_cut_colour_v2(LevelArgs L, const CutDesc* desc, int np, const double* ecut,
+                                                       const double* inv, const double* x, const double* b,
+                                                       double* zbuf, int wpb) {
+  __shared__ SmTab T;
+  extern __shared__ double dsm[];
+  load_smtab<P>(T);
+  __syncthreads();
+  const int w = threadIdx.x >> 5;
+  if (w >= wpb) return;
+  const int k = blockIdx.x * wpb + w;
+  if (k >= np) return;
+  const CutDesc d = desc[k];
+  cut_patch_z<P, QUAD>(L, d, ecut, inv, x, b, zbuf, T, dsm + (size_t)w * CutSmem<P>::per_warp);
+}
+
+// ---- Cartesian colour step (v2): (2p-1) threads per patch -------------------
+template <int P, int TP>
+struct CartSmem {
+  static constexpr int NE = 2 * P + 1, NI = 2 * P - 1, W = 2 * P * TP + 1;
+  static constexpr int doubles = 2 * W * W + TP * TP * NE * NI * 2 + TP * TP * NI * NI + 2 * NE * NE + NI * NI + NI;
+};
+
+// One tile of TP x TP same-colour Cartesian patches, processed by the first
+// NT = TP^2 (2p-1) threads of the block (all threads reach the barriers).
+template <int P, int TP>
+__device__ void cart_tile(const LevelArgs& L, int tile, int colour, const uint8_t* vk, double* x, const double* b,
+                          double* sm) {
+  constexpr int NE = 2 * P + 1, NI = 2 * P - 1, W = 2 * P * TP + 1, NT = TP * TP * NI;
+  double* Xs = sm;
+  double* Bs = Xs + W * W;
+  double* T1 = Bs + W * W;                 // [TP*TP][NE][NI]
+  double* T2 = T1 + TP * TP * NE * NI;
+  double* Ex = T2 + TP * TP * NE * NI;     // [TP*TP][NI][NI]
+  double* sK = Ex + TP * TP * NI * NI;     // two-cell matrices, S, lam
+  double* sM = sK + NE * NE;
+  double* sS = sM + NE * NE;
+  double* sL = sS + NI * NI;
+  const Tab& Tc = c_tab[P];
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  for (int e = tid; e < NE * NE; e += nthr) {
+    sK[e] = Tc.Kp[e / NE][e % NE];
+    sM[e] = Tc.Mp[e / NE][e % NE];
+  }
+  for (int e = tid; e < NI * NI; e += nthr) sS[e] = Tc.S[e / NI][e % NI];
+  if (tid < NI) sL[tid] = Tc.lam[tid];
+  const int ti = tile & 0xffff, tj = tile >> 16;
+  const int I0 = (colour & 1) + 2 * ti * TP, J0 = (colour >> 1) + 2 * tj * TP;
+  const int a0 = P * (I0 - 1), b0 = P * (J0 - 1);
+  for (int e = tid; e < W * W; e += nthr) {
+    int a = a0 + e % W, bb = b0 + e / W;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) {
+      cp_async8(Xs + e, x + (size_t)bb * L.ld + a);
+      cp_async8(Bs + e, b + (size_t)bb * L.ld + a);
+    } else {
+      Xs[e] = 0.0;
+      Bs[e] = 0.0;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int q = tid / NI, t = tid % NI;
+  const int u = q % TP, v = q / TP;
+  const int I = I0 + 2 * u, J = J0 + 2 * v, n = L.n;
+  const bool cart = tid < NT && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART;
+  const double* X = Xs + (2 * P * v) * W + 2 * P * u;
+  double* t1 = T1 + q * NE * NI;
+  double* t2 = T2 + q * NE * NI;
+  double* ex = Ex + q * NI * NI;
+  // 1. T1 = X K̄^T, T2 = X M̄^T on the interior columns (rows b' = t, t+NI)
+  if (cart) {
+    for (int bp = t; bp < NE; bp += NI) {
+#pragma unroll
+      for (int ia = 0; ia < NI; ++ia) {
+        const int a = ia + 1, alo = a <= P ? 0 : P, ahi = a >= P ? 2 * P : P;
+        double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int ap = alo; ap <= ahi; ++ap) {
+          double xv = X[bp * W + ap];
+          s1 = fma(Tc.Kp[a][ap], xv, s1);
+          s2 = fma(Tc.Mp[a][ap], xv, s2);
+        }
+        t1[bp * NI + ia] = s1;
+        t2[bp * NI + ia] = s2;
+      }
+    }
+  }
+  __syncthreads();
+  // 2. residual row ib = t, V = R S
+  double R[NI];
+  if (cart) {
+    const int bq = t + 1;
+    const double* B = Bs + (2 * P * v) * W + 2 * P * u;
+#pragma unroll
+    for (int ia = 0; ia < NI; ++ia) R[ia] = B[bq * W + ia + 1];
+    for (int bp = 0; bp < NE; ++bp) {
+      const double mb = sM[bq * NE + bp], kb = sK[bq * NE + bp];
+#pragma unroll
+      for (int ia = 0; ia < NI; ++ia) R[ia] = fma(-mb, t1[bp * NI + ia], fma(-kb, t2[bp * NI + ia], R[ia]));
+    }
+#pragma unroll
+    for (int be = 0; be < NI; ++be) {
+      double s = 0.0;
+#pragma unroll
+      for (int ia = 0; ia < NI; ++ia) s = fma(R[ia], Tc.S[ia][be], s);
+      ex[t * NI + be] = s;
+    }
+  }
+  __syncthreads();
+  // 3. row alpha = t: U = (S^T V) ./ (lam_alpha + lam_beta), Y = U S^T
+  double Y[NI];
+  if (cart) {
+    double U[NI];
+#pragma unroll
+    for (int be = 0; be < NI; ++be) {
+      double s = 0.0;
+#pragma unroll
+      for (int ib = 0; ib < NI; ++ib) s = fma(sS[ib * NI + t], ex[ib * NI + be], s);
+      U[be] = s / (sL[t] + Tc.lam[be]);
+    }
+#pragma unroll
+    for (int ia = 0; ia < NI; ++ia) {
+      double s = 0.0;
+#pragma unroll
+      for (int be = 0; be < NI; ++be) s = fma(U[be], Tc.S[ia][be], s);
+      Y[ia] = s;
+    }
+  }
+  __syncthreads();
+  if (cart) {
+#pragma unroll
+    for (int ia = 0; ia < NI; ++ia) ex[t * NI + ia] = Y[ia];
+  }
+  __syncthreads();
+  // 4. row ib = t of Z = S Y, added to the patch interior
+  if (cart) {
+    double* Xw = Xs + (2 * P * v + t + 1) * W + 2 * P * u + 1;
+#pragma unroll
+    for (int ia = 0; ia < NI; ++ia) {
+      double s = 0.0;
+#pragma unroll
+      for (int al = 0; al < NI; ++al) s = fma(sS[t * NI + al], ex[al * NI + ia], s);
+      Xw[ia] += s;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < W * W; e += nthr) {
+    int c = e % W, r = e / W;
+    int lc = c % (2 * P), lr = r % (2 * P);
+    if (lc == 0 || lr == 0) continue;
+    int uu = c / (2 * P), vv = r / (2 * P);
+    int II = I0 + 2 * uu, JJ = J0 + 2 * vv;
+    if (II > n || JJ > n || vk[JJ * (n + 1) + II] != V_CART) continue;
+    x[(size_t)(b0 + r) * L.ld + a0 + c] = Xs[e];
+  }
+  __syncthreads();
+}
+
+template <int P, int TP>
+__global__ void __launch_bounds__(TP* TP*(2 * P - 1)) k_cart_colour_v2(LevelArgs L, const int* tiles, int colour,
+                                                                      const uint8_t* vk, double* x, const double* b) {
+  extern __shared__ double sm[];
+  cart_tile<P, TP>(L, tiles[blockIdx.x], colour, vk, x, b, sm);
+}
+
+// ---- persistent smoothing step ---------------------------------------------
+// All colour steps of one application of S (P eq. smoother-split) in one
+// cooperative launch: Cartesian colours (CTA per tile), then n_c sweeps of
+// cut colours (warp per patch, corrections to zbuf, grid barrier, scatter,
+// grid barrier).  A grid barrier separates dependent colour steps; the
+// order is reversed for the adjoint (post-)smoother (R9).
+struct SmoothArgs {
+  LevelArgs L;
+  const int* tiles;
+  int tile_off[5];
+  const CutDesc* desc;
+  int cut_off[5];
+  int64_t ent_off_c[5];
+  const int32_t* ent_node;
+  const double* ecut;
+  const double* inv;
+  const uint8_t* vk;
+  double* zbuf;
+  double* x;
+  const double* b;
+  int n_c, reverse, cut_wpb;
+};
+
+template <int P, int TP, bool QUAD>
+__global__ void __launch_bounds__(256) k_smooth_persistent(SmoothArgs A) {
+  extern __shared__ double sm[];
+  __shared__ SmTab T;
+  load_smtab<P>(T);
+  __syncthreads();
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int nphase = 4 + 4 * A.n_c;
+  const int w = threadIdx.x >> 5;
+  for (int s = 0; s < nphase; ++s) {
+    const int ph = A.reverse ? nphase - 1 - s : s;
+    if (ph < 4) {
+      const int c = ph, nt = A.tile_off[c + 1] - A.tile_off[c];
+      for (int t = blockIdx.x; t < nt; t += gridDim.x) cart_tile<P, TP>(A.L, A.tiles[A.tile_off[c] + t], c, A.vk, A.x, A.b, sm);
+      grid.sync();
+    } else {
+      const int c = (ph - 4) & 3, np = A.cut_off[c + 1] - A.cut_off[c];
+      if (w < A.cut_wpb) {
+        for (int k = blockIdx.x * A.cut_wpb + w; k < np; k += gridDim.x * A.cut_wpb) {
+          const CutDesc d = A.desc[A.cut_off[c] + k];
+          cut_patch_z<P, QUAD>(A.L, d, A.ecut, A.inv, A.x, A.b, A.zbuf, T, sm + (size_t)w * CutSmem<P>::per_warp);
+        }
+      }
+      grid.sync();
+      const int64_t e1 = A.ent_off_c[c + 1];
+      for (int64_t e = A.ent_off_c[c] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
+           e += (int64_t)gridDim.x * blockDim.x)
+        A.x[A.ent_node[e]] += A.zbuf[e];
+      if (s + 1 < nphase) grid.sync();
+    }
+  }
+}
+
+}  // namespace cf
+
+namespace cf {
+
+// ---- Cartesian sweep, all four colours in one kernel (temporal blocking) ---
+// A CTA owns TC x TC cells.  Colour step s (of 4) updates the Cartesian
+// patches within 3 - s vertices of the owned vertex range: a colour-c patch
+// reads its closed 2x2-cell block, which overlaps the interiors of patches of
+// the other colours only within one vertex, so the halo shrinks by one
+// vertex per step.  x and b are read once (region of TC + 8 cells), every
+// colour is applied in shared memory, the owned nodes are written once.
+template <int P, int TC>
+struct CartFusedSmem {
+  static constexpr int NE = 2 * P + 1, NI = 2 * P - 1, H = 4, RC = TC + 2 * H, RW = RC * P + 1;
+  static constexpr int NPR = 256 / NI;
+  static constexpr int doubles = 2 * RW * RW + NPR * NE * NI * 2 + NPR * NI * NI + 2 * NE * NE + NI * NI + NI;
+};
+
+template <int P, int TC>
+__global__ void __launch_bounds__(256) k_cart_fused(LevelArgs L, const int* tiles, const uint8_t* vk, double* x,
+                                                    const double* b, int reverse) {
+  using S = CartFusedSmem<P, TC>;
+  constexpr int NE = S::NE, NI = S::NI, H = S::H, RW = S::RW, NPR = S::NPR;
+  extern __shared__ double sm[];
+  double* Xs = sm;
+  double* Bs = Xs + RW * RW;
+  double* T1 = Bs + RW * RW;
+  double* T2 = T1 + NPR * NE * NI;
+  double* Ex = T2 + NPR * NE * NI;
+  double* sK = Ex + NPR * NI * NI;
+  double* sM = sK + NE * NE;
+  double* sS = sM + NE * NE;
+  double* sL = sS + NI * NI;
+  const Tab& Tc = c_tab[P];
+  const int tid = threadIdx.x, n = L.n;
+  for (int e = tid; e < NE * NE; e += 256) {
+    sK[e] = Tc.Kp[e / NE][e % NE];
+    sM[e] = Tc.Mp[e / NE][e % NE];
+  }
+  for (int e = tid; e < NI * NI; e += 256) sS[e] = Tc.S[e / NI][e % NI];
+  if (tid < NI) sL[tid] = Tc.lam[tid];
+  pdl_trigger();
+  const int tile = tiles[blockIdx.x];
+  const int ci0 = (tile & 0xffff) * TC, cj0 = (tile >> 16) * TC;
+  const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
+  pdl_wait();
+  for (int e = tid; e < RW * RW; e += 256) {
+    int a = a0 + e % RW, bb = b0 + e / RW;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) {
+      cp_async8(Xs + e, x + (size_t)bb * L.ld + a);
+      cp_async8(Bs + e, b + (size_t)bb * L.ld + a);
+    } else {
+      Xs[e] = 0.0;
+      Bs[e] = 0.0;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int s = 0; s < 4; ++s) {
+    const int c = reverse ? 3 - s : s, rad = 3 - s;
+    // colour-c vertices in [ci0 - rad, ci0 + TC + rad]
+    const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
+    const int nvx = (ci0 + TC + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
+    const int np = nvx * nvy;
+    for (int base = 0; base < np; base += NPR) {
+      const int q = tid / NI, t = tid % NI, pq = base + q;
+      const int I = ilo + 2 * (pq % nvx), J = jlo + 2 * (pq / nvx);
+      const bool cart = q < NPR && pq < np && I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART;
+      // patch block origin in the region (cells I-1, J-1)
+      const int ox = P * (I - 1 - (ci0 - H)), oy = P * (J - 1 - (cj0 - H));
+      const double* X = Xs + oy * RW + ox;
+      double* t1 = T1 + q * NE * NI;
+      double* t2 = T2 + q * NE * NI;
+      double* ex = Ex + q * NI * NI;
+      if (cart) {
+        for (int bp = t; bp < NE; bp += NI) {
+#pragma unroll
+          for (int ia = 0; ia < NI; ++ia) {
+            const int a = ia + 1, alo = a <= P ? 0 : P, ahi = a >= P ? 2 * P : P;
+            double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+            for (int ap = alo; ap <= ahi; ++ap) {
+              double xv = X[bp * RW + ap];
+              s1 = fma(Tc.Kp[a][ap], xv, s1);
+              s2 = fma(Tc.Mp[a][ap], xv, s2);
+            }
+            t1[bp * NI + ia] = s1;
+            t2[bp * NI + ia] = s2;
+          }
+        }
+      }
+      __syncthreads();
+      if (cart) {
+        const int bq = t + 1;
+        const double* B = Bs + oy * RW + ox;
+        double R[NI];
+#pragma unroll
+        for (int ia = 0; ia < NI; ++ia) R[ia] = B[bq * RW + ia + 1];
+        for (int bp = 0; bp < NE; ++bp) {
+          const double mb = sM[bq * NE + bp], kb = sK[bq * NE + bp];
+#pragma unroll
+          for (int ia = 0; ia < NI; ++ia) R[ia] = fma(-mb, t1[bp * NI + ia], fma(-kb, t2[bp * NI + ia], R[ia]));
+        }
+#pragma unroll
+        for (int be = 0; be < NI; ++be) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int ia = 0; ia < NI; ++ia) sacc = fma(R[ia], Tc.S[ia][be], sacc);
+          ex[t * NI + be] = sacc;
+        }
+      }
+      __syncthreads();
+      double Y[NI];
+      if (cart) {
+        double U[NI];
+#pragma unroll
+        for (int be = 0; be < NI; ++be) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int ib = 0; ib < NI; ++ib) sacc = fma(sS[ib * NI + t], ex[ib * NI + be], sacc);
+          U[be] = sacc / (sL[t] + Tc.lam[be]);
+        }
+#pragma unroll
+        for (int ia = 0; ia < NI; ++ia) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int be = 0; be < NI; ++be) sacc = fma(U[be], Tc.S[ia][be], sacc);
+          Y[ia] = sacc;
+        }
+      }
+      __syncthreads();
+      if (cart) {
+#pragma unroll
+        for (int ia = 0; ia < NI; ++ia) ex[t * NI + ia] = Y[ia];
+      }
+      __syncthreads();
+      if (cart) {
+        double* Xw = Xs + (oy + t + 1) * RW + ox + 1;
+#pragma unroll
+        for (int ia = 0; ia < NI; ++ia) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int al = 0; al < NI; ++al) sacc = fma(sS[t * NI + al], ex[al * NI + ia], sacc);
+          Xw[ia] += sacc;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // owned nodes: [P ci0, P (ci0 + TC)) (+ the last lattice line on the mesh boundary)
+  const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
+  const int aw = ahi - P * ci0, bw = bhi - P * cj0;
+  for (int e = tid; e < aw * bw; e += 256) {
+    const int a = P * ci0 + e % aw, bb = P * cj0 + e / aw;
+    x[(size_t)bb * L.ld + a] = Xs[(bb - b0) * RW + (a - a0)];
+  }
+}
+
+// tiles of TC x TC cells whose owned vertex range holds a Cartesian patch
+__global__ void k_fused_tile_flags(int n, const uint8_t* vk, int TC, int tx, uint8_t* flag, int ntiles) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int ci0 = (t % tx) * TC, cj0 = (t / tx) * TC;
+  uint8_t f = 0;
+  for (int J = cj0; J <= min(cj0 + TC, n) && !f; ++J)
+    for (int I = ci0; I <= min(ci0 + TC, n); ++I)
+      if (vk[J * (n + 1) + I] == V_CART) {
+        f = 1;
+        break;
+      }
+  flag[t] = f;
+}
+
+}  // namespace cf
+
+namespace cf {
+
+template <int P>
+struct CutSmem3 {
+  static constexpr int NB = (P + 1) * (P + 1), BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, NJ = 12 * P * (P + 1);
+  static constexpr int per_warp = WS * WS + 2 * NJ + MM + MM * MM + 4 * NB * NB;
+};
+
+// face f of the 12 faces touching the patch cells: axis 0 (x-faces) f = 2 s + t
+// between cells (I-2+s, J-1+t) | (I-1+s, J-1+t); axis 1 f = 6 + 2 s + t between
+// (I-1+t, J-2+s) | (I-1+t, J-1+s).  Window cell coordinates of both sides:
+__device__ __forceinline__ void face_cells(int f, int& axis, int& w1x, int& w1y, int& w2x, int& w2y) {
+  axis = f >= 6;
+  const int g = f - 6 * axis, s = g >> 1, t = g & 1;
+  if (!axis) {
+    w1x = s; w1y = 1 + t; w2x = s + 1; w2y = 1 + t;
+  } else {
+    w1x = 1 + t; w1y = s; w2x = 1 + t; w2y = s + 1;
+  }
+}
+
+// v3 cut-patch colour step: lanes work on ghost-face jump moments in
+// parallel, then one lane per row of the (2p+1)^2 block gathers the cell and
+// face contributions (no serial loop over cells and faces).
+template <int P, bool QUAD>
+__device__ void cut_patch_z3(const LevelArgs& L, const CutDesc& d, const double* ecut, const double* inv,
+                             const double* x, const double* b, double* zbuf, const SmTab& T, double* Wp) {
+  using S = CutSmem3<P>;
+  constexpr int NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, NJ = S::NJ, PP = P * (P + 1);
+  constexpr int RPL = (MM + 31) / 32;  // block rows per lane
+  const int lane = threadIdx.x & 31;
+  double* Jt = Wp + WS * WS;   // [12][P][P+1] jumps, then Ycut for QUAD
+  double* Jm = Jt + NJ;        // [12][P][P+1] moments
+  double* Rr = Jm + NJ;
+  double* Ai = Rr + MM;
+  double* Ec = Ai + MM * MM;
+  const int m = mask_count(d);
+  // ---- loads independent of the previous kernel
+  const double* Ag = inv + d.inv_off;
+  for (int e = lane; e < m * m; e += 32) cp_async8(Ai + e, Ag + e);
+  if (!QUAD) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (d.cid[q] >= 0)
+        for (int e = lane; e < NB * NB; e += 32) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
+  }
+  pdl_wait();
+  // ---- x window and b on the interior rows
+  for (int e = lane; e < WS * WS; e += 32) {
+    const int r = e / WS, c = e - r * WS;
+    const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, x + (size_t)bb * L.ld + a);
+    else Wp[e] = 0.0;
+  }
+  double bv[RPL];
+  bool inm[RPL];
+  int iidx[RPL];
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    const int loc = lane + 32 * t;
+    const unsigned long long word = d.mask[loc >> 6];
+    inm[t] = loc < MM && ((word >> (loc & 63)) & 1ull);
+    iidx[t] = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    bv[t] = inm[t] ? b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS] : 0.0;
+  }
+  cp_async_wait_all();
+  __syncwarp();
+  // ---- ghost faces: jumps J[f][k][l] (lane-parallel), then moments M J
+  const Tab& Tc = c_tab[P];
+  for (int job = lane; job < NJ; job += 32) {
+    const int f = job / PP, rem = job - f * PP, k = rem / (P + 1) + 1, l = rem % (P + 1);
+    int axis, w1x, w1y, w2x, w2y;
+    face_cells(f, axis, w1x, w1y, w2x, w2y);
+    const int k1 = desc_kind(d, w1x, w1y), k2 = desc_kind(d, w2x, w2y);
+    double s = 0.0;
+    if (k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT)) {
+      const double* X1 = Wp + (P * w1y) * WS + P * w1x;
+      const double* X2 = Wp + (P * w2y) * WS + P * w2x;
+#pragma unroll
+      for (int nn = 0; nn <= P; ++nn) {
+        const double v1 = axis == 0 ? X1[l * WS + nn] : X1[nn * WS + l];
+        const double v2 = axis == 0 ? X2[l * WS + nn] : X2[nn * WS + l];
+        s = fma(T.d1[k][nn], v1, fma(-T.d0[k][nn], v2, s));
+      }
+    }
+    Jt[job] = s;
+  }
+  __syncwarp();
+  for (int job = lane; job < NJ; job += 32) {
+    const int base = job - job % (P + 1), q = job % (P + 1);
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l <= P; ++l) s = fma(T.M[q][l], Jt[base + l], s);
+    Jm[job] = s;
+  }
+  __syncwarp();
+  // ---- cut cells by quadrature (warp-cooperative) into Jt (reused as Ycut)
+  if (QUAD) {
+    for (int q = 0; q < 4; ++q) {
+      if (d.cid[q] < 0) continue;
+      const int dx = q & 1, dy = q >> 1;
+      double acc[NB];
+      cut_cell_warp<P>(L, d.cid[q], Wp + (P * (dy + 1)) * WS + P * (dx + 1), WS, acc);
+#pragma unroll
+      for (int t = 0; t < NB; ++t)
+        if (lane == t) Jt[q * NB + t] = acc[t];
+    }
+    __syncwarp();
+  }
+  // ---- one lane per block row: (A x) on the row, residual
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    const int loc = lane + 32 * t;
+    if (!inm[t]) continue;
+    const int ra = loc % BS, rb = loc / BS;
+    double y = 0.0;
+    for (int dy = 0; dy < 2; ++dy) {
+      const int ky = rb - P * dy;
+      if (ky < 0 || ky > P) continue;
+      for (int dx = 0; dx < 2; ++dx) {
+        const int kx = ra - P * dx;
+        if (kx < 0 || kx > P) continue;
+        const int kind = desc_kind(d, dx + 1, dy + 1);
+        if (kind == OUTSIDE) continue;
+        const int q = dx + 2 * dy;
+        const double* X = Wp + (P * (dy + 1)) * WS + P * (dx + 1);
+        if (kind == INSIDE) {
+          y += inside_row<P>(T, X, WS, kx, ky);
+        } else if (QUAD) {
+          y += Jt[q * NB + ky * (P + 1) + kx];
+        } else {
+          const double* Er = Ec + q * NB * NB + (ky * (P + 1) + kx) * NB;
+#pragma unroll
+          for (int l = 0; l < NB; ++l) y = fma(Er[l], X[(l / (P + 1)) * WS + l % (P + 1)], y);
+        }
+        // ghost faces of this cell: left (side 2), right (side 1), bottom (side 2), top (side 1)
+        const int fl = 2 * dx + dy, fr = 2 * (dx + 1) + dy, fb = 6 + 2 * dy + dx, ft = 6 + 2 * (dy + 1) + dx;
+#pragma unroll
+        for (int kk = 1; kk <= P; ++kk) {
+          const double g = L.gs[kk];
+          y = fma(-g * T.d0[kk][kx], Jm[fl * PP + (kk - 1) * (P + 1) + ky], y);
+          y = fma(g * T.d1[kk][kx], Jm[fr * PP + (kk - 1) * (P + 1) + ky], y);
+          y = fma(-g * T.d0[kk][ky], Jm[fb * PP + (kk - 1) * (P + 1) + kx], y);
+          y = fma(g * T.d1[kk][ky], Jm[ft * PP + (kk - 1) * (P + 1) + kx], y);
+        }
+      }
+    }
+    Rr[iidx[t]] = bv[t] - y;
+  }
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) {
+    double z = 0.0;
+    for (int q = 0; q < m; ++q) z = fma(Ai[q * m + i], Rr[q], z);
+    zbuf[d.e0 + i] = z;
+  }
+  __syncwarp();
+  (void)Tc;
+}
+
+template <int P, bool QUAD>
+__global__ void __launch_bounds__(128) k_cut_colour_v3(LevelArgs L, const CutDesc* desc, int np, const double* ecut,
+                                                       const double* inv, const double* x, const double* b,
+                                                       double* zbuf, int wpb) {
+  __shared__ SmTab T;
+  extern __shared__ double dsm[];
+  pdl_trigger();
+  load_smtab<P>(T);
+  __syncthreads();
+  const int w = threadIdx.x >> 5;
+  if (w >= wpb) return;
+  const int k = blockIdx.x * wpb + w;
+  if (k >= np) return;
+  const CutDesc d = desc[k];
+  cut_patch_z3<P, QUAD>(L, d, ecut, inv, x, b, zbuf, T, dsm + (size_t)w * CutSmem3<P>::per_warp);
+}
+
+__global__ void k_cut_apply(const int32_t* ent_node, const double* zbuf, int64_t e0, int64_t e1, double* x) {
+  pdl_trigger();
+  const int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int32_t node = e < e1 ? ent_node[e] : 0;
+  pdl_wait();
+  if (e < e1) x[node] += zbuf[e];
+}
+
+}  // namespace cf

@@ -34,7 +34,8 @@ class Params(ctypes.Structure):
                 ("n_coarse", ctypes.c_int), ("n_levels", ctypes.c_int), ("degree", ctypes.c_int),
                 ("cx", ctypes.c_double), ("cy", ctypes.c_double), ("r", ctypes.c_double),
                 ("gamma_D", ctypes.c_double), ("gamma_k", ctypes.c_double * 4), ("sigma", ctypes.c_int),
-                ("n_q", ctypes.c_int), ("n_c", ctypes.c_int), ("symmetric", ctypes.c_int)]
+                ("n_q", ctypes.c_int), ("n_c", ctypes.c_int), ("symmetric", ctypes.c_int),
+                ("cut_mode", ctypes.c_int)]
 
 
 class LevelInfo(ctypes.Structure):
@@ -103,9 +104,10 @@ def launch_count():
 
 
 def make_params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D=0.0, gamma_k=(-1, -1, -1, -1),
-                sigma=-1, n_q=0, n_c=2, symmetric=1):
+                sigma=-1, n_q=0, n_c=2, symmetric=1, cut_mode=0):
     g = (ctypes.c_double * 4)(*[float(v) for v in (list(gamma_k) + [-1] * 4)[:4]])
-    return Params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D, g, sigma, n_q, n_c, symmetric)
+    return Params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D, g, sigma, n_q, n_c, symmetric,
+                  cut_mode)
 
 
 class Problem:

@@ -169,3 +169,22 @@ def test_host_pointer_entry_points(torch_cuda):
     ref = compact(lf, x0).copy()
     o.fine.smooth(ref, compact(lf, bl), w.n_c)
     assert rel_err(compact(lf, xs[:, :nl].ravel()), ref) < TOL
+
+
+@pytest.mark.parametrize("w", [CASES[0], CASES[2], CASES[4]], ids=[IDS[0], IDS[2], IDS[4]])
+def test_runtime_quadrature_mode_parity(w, torch_cuda):
+    # cut_mode 1: the cut-cell bulk + Nitsche terms are evaluated by quadrature
+    # on the fly (warp reductions) instead of precomputed element matrices
+    o = oracle(w)
+    g = gpu(w, cut_mode=1)
+    l = len(o.levels) - 1
+    ld = o.levels[l]
+    xl, bl = lattice_random(w, 12, l), lattice_random(w, 13, l)
+    y = g.zeros(l)
+    g.apply_operator(l, g.to_device(xl, l), y)
+    assert rel_err(compact(ld.lv, g.to_host(y, l)), ld.A @ compact(ld.lv, xl)) < TOL
+    x = g.to_device(xl, l)
+    g.smooth(l, x, g.to_device(bl, l))
+    xo = compact(ld.lv, xl).copy()
+    ld.smooth(xo, compact(ld.lv, bl), w.n_c)
+    assert rel_err(compact(ld.lv, g.to_host(x, l)), xo) < TOL
