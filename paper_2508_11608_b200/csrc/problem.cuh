@@ -50,6 +50,7 @@ struct Problem {
   bool built = false;
   bool persistent = false;  // one cooperative launch per smoothing step (env CUTFEM_PERSISTENT=1)
   bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
+  bool use_mma = true;      // Cartesian patch map on fp64 tensor cores (env CUTFEM_MMA=0 disables)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -157,6 +158,8 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_PERSISTENT")) persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_FUSED")) fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_PDL")) pdl = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_MMA")) use_mma = std::atoi(e) != 0;
+    host::cart_map(prm.p);  // dense Cartesian patch map (p <= 3), built outside any graph capture
     d_count = alloc<int>(1);
     const int p = prm.p;
     lv.resize(prm.n_levels);
@@ -593,17 +596,33 @@ struct Problem {
     CF_LAUNCHED();
   }
 
-  // all four Cartesian colours in one launch (temporal blocking)
+  // all four Cartesian colours in one launch (temporal blocking); p <= 3 on
+  // the fp64 tensor cores (dense patch map), p = 4 by fast diagonalisation
   void cart_fused(int l, double* x, const double* b, int reverse) {
     LevelData& D = lv[l];
     if (!D.n_fused_tiles) return;
     CF_DISPATCH(prm.p, {
       constexpr int TC = fused_tc<P>();
+      if constexpr (P <= 3) {
+        if (use_mma) {
+          const double* G = host::cart_map(P);
+          const size_t smb = CartMMASmem<P, TC>::doubles * sizeof(double) + CartMMASmem<P, TC>::ints * sizeof(int);
+          static bool attr = false;
+          if (!attr) {
+            CF_CUDA(cudaFuncSetAttribute(k_cart_fused_mma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+            attr = true;
+          }
+          launch(k_cart_fused_mma<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
+                 (const uint8_t*)D.vkind, G, x, b, reverse);
+          CF_LAUNCHED();
+          return;
+        }
+      }
       const size_t smb = CartFusedSmem<P, TC>::doubles * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
+      static bool attr2 = false;
+      if (!attr2) {
         CF_CUDA(cudaFuncSetAttribute(k_cart_fused<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-        attr = true;
+        attr2 = true;
       }
       launch(k_cart_fused<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
              (const uint8_t*)D.vkind, x, b, reverse);

@@ -802,3 +802,118 @@ __global__ void k_cut_apply(const int32_t* ent_node, const double* zbuf, int64_t
 }
 
 }  // namespace cf
+
+namespace cf {
+
+// fp64 tensor-core MMA: D(8x8) = A(8x4, row) B(4x8, col) + C.  Fragments per
+// lane: A[lane>>2][lane&3], B[lane&3][lane>>2], C/D[lane>>2][2(lane&3)+{0,1}].
+__device__ __forceinline__ void dmma(double a, double b, double& c0, double& c1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int P>
+struct CartMMA {
+  static constexpr int NE = 2 * P + 1, NI = 2 * P - 1, NINT = NI * NI, NEXT = NE * NE, K = NINT + NEXT;
+  static constexpr int KS = (K + 3) / 4, MT = (NINT + 7) / 8, COLS = 4 * KS, ROWS = 8 * MT;
+};
+
+template <int P, int TC>
+struct CartMMASmem {
+  static constexpr int H = 4, RC = TC + 2 * H, RW = RC * P + 1;
+  static constexpr int doubles = 2 * RW * RW;
+  static constexpr int ints = CartMMA<P>::COLS + CartMMA<P>::ROWS;
+};
+
+// All four Cartesian colours of one smoothing step (temporal blocking as in
+// k_cart_fused); every colour pass is the batched dense contraction
+// x_int_new = G [b_int; x_ext] over groups of 8 patches per warp on the fp64
+// tensor cores (mma.sync m8n8k4 .f64), G from host::cart_affine_map.
+template <int P, int TC>
+__global__ void __launch_bounds__(256) k_cart_fused_mma(LevelArgs L, const int* tiles, const uint8_t* vk,
+                                                        const double* G, double* x, const double* b, int reverse) {
+  using C = CartMMA<P>;
+  using S = CartMMASmem<P, TC>;
+  constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS, MT = C::MT, H = S::H, RW = S::RW;
+  extern __shared__ double sm[];
+  double* Xs = sm;
+  double* Bs = Xs + RW * RW;
+  int* koff = (int*)(Bs + RW * RW);   // operand k: offset in the region (+ (1 << 30) for b)
+  int* roff = koff + C::COLS;          // interior row r: offset in the region
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = L.n;
+  pdl_trigger();
+  for (int k = tid; k < C::COLS; k += 256) {
+    int v = -1;
+    if (k < NINT) v = (1 << 30) + (k / NI + 1) * RW + k % NI + 1;
+    else if (k < K) v = ((k - NINT) / NE) * RW + (k - NINT) % NE;
+    koff[k] = v;
+  }
+  for (int r = tid; r < C::ROWS; r += 256) roff[r] = r < NINT ? (r / NI + 1) * RW + r % NI + 1 : -1;
+  double af[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int s = 0; s < KS; ++s) af[mt][s] = G[(8 * mt + (lane >> 2)) * C::COLS + 4 * s + (lane & 3)];
+  const int tile = tiles[blockIdx.x];
+  const int ci0 = (tile & 0xffff) * TC, cj0 = (tile >> 16) * TC;
+  const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
+  pdl_wait();
+  for (int e = tid; e < RW * RW; e += 256) {
+    const int r = e / RW, c = e - r * RW;
+    const int a = a0 + c, bb = b0 + r;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) {
+      cp_async8(Xs + e, x + (size_t)bb * L.ld + a);
+      cp_async8(Bs + e, b + (size_t)bb * L.ld + a);
+    } else {
+      Xs[e] = 0.0;
+      Bs[e] = 0.0;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int s = 0; s < 4; ++s) {
+    const int c = reverse ? 3 - s : s, rad = 3 - s;
+    const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
+    const int nvx = (ci0 + TC + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
+    const int np = nvx * nvy, ng = (np + 7) / 8;
+    for (int g = warp; g < ng; g += 8) {
+      // this lane's patch in the B fragment: n = lane >> 2
+      const int pq = 8 * g + (lane >> 2);
+      const int I = ilo + 2 * (pq % nvx), J = jlo + 2 * (pq / nvx);
+      const bool cart = pq < np && I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART;
+      const int base = cart ? P * (J - 1 - (cj0 - H)) * RW + P * (I - 1 - (ci0 - H)) : -1;
+      double acc[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int ko = koff[4 * ks + (lane & 3)];
+        double v = 0.0;
+        if (base >= 0 && ko >= 0) v = ko >= (1 << 30) ? Bs[base + ko - (1 << 30)] : Xs[base + ko];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(af[mt][ks], v, acc[mt][0], acc[mt][1]);
+      }
+      // D[r][n'] with r = 8 mt + (lane >> 2), n' = 2 (lane & 3) + i
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int bo = __shfl_sync(0xffffffffu, base, 4 * (2 * (lane & 3) + i));
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + (lane >> 2);
+          if (bo >= 0 && r < NINT) Xs[bo + roff[r]] = acc[mt][i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
+  const int aw = ahi - P * ci0, bw = bhi - P * cj0;
+  for (int e = tid; e < aw * bw; e += 256) {
+    const int rr = e / aw, cc = e - rr * aw;
+    const int a = P * ci0 + cc, bb = P * cj0 + rr;
+    x[(size_t)bb * L.ld + a] = Xs[(bb - b0) * RW + (a - a0)];
+  }
+}
+
+}  // namespace cf

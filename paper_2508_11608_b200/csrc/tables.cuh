@@ -230,3 +230,92 @@ inline void upload_tables() {
 
 }  // namespace host
 }  // namespace cf
+
+namespace cf {
+namespace host {
+
+// Dense affine map of one Cartesian patch solve (P l.192 fast diagonalisation,
+// written out): x_int_new = A_int^{-1} b_int + (E - A_int^{-1} Ā) x_ext with
+// A = K̄⊗M̄ + M̄⊗K̄ on the two-cell patch (h-free in 2D), rows = interior
+// nodes (ib*NI + ia), columns = [b_int (NI^2) | x_ext (NE^2)], padded to
+// (8*MT) x (4*KS) for the fp64 tensor-core (DMMA m8n8k4) fragments.
+inline std::vector<double> cart_affine_map(int p, const Tab& t, int& rows_pad, int& cols_pad) {
+  const int NE = 2 * p + 1, NI = 2 * p - 1, NINT = NI * NI, NEXT = NE * NE, K = NINT + NEXT;
+  rows_pad = 8 * ((NINT + 7) / 8);
+  cols_pad = 4 * ((K + 3) / 4);
+  std::vector<double> Aext(NINT * NEXT), Ai(NINT * NINT);
+  for (int ib = 0; ib < NI; ++ib)
+    for (int ia = 0; ia < NI; ++ia)
+      for (int bb = 0; bb < NE; ++bb)
+        for (int aa = 0; aa < NE; ++aa) {
+          const int r = ib * NI + ia, c = bb * NE + aa, a = ia + 1, b = ib + 1;
+          Aext[r * NEXT + c] = t.Kp[a][aa] * t.Mp[b][bb] + t.Mp[a][aa] * t.Kp[b][bb];
+        }
+  for (int r = 0; r < NINT; ++r)
+    for (int q = 0; q < NINT; ++q) {
+      const int ib = q / NI, ia = q % NI;
+      Ai[r * NINT + q] = Aext[r * NEXT + (ib + 1) * NE + ia + 1];
+    }
+  // Gauss-Jordan inverse with partial pivoting
+  std::vector<double> inv(NINT * NINT, 0.0);
+  for (int i = 0; i < NINT; ++i) inv[i * NINT + i] = 1.0;
+  for (int c = 0; c < NINT; ++c) {
+    int pr = c;
+    for (int r = c + 1; r < NINT; ++r)
+      if (std::fabs(Ai[r * NINT + c]) > std::fabs(Ai[pr * NINT + c])) pr = r;
+    for (int q = 0; q < NINT; ++q) {
+      std::swap(Ai[c * NINT + q], Ai[pr * NINT + q]);
+      std::swap(inv[c * NINT + q], inv[pr * NINT + q]);
+    }
+    const double piv = Ai[c * NINT + c];
+    for (int q = 0; q < NINT; ++q) {
+      Ai[c * NINT + q] /= piv;
+      inv[c * NINT + q] /= piv;
+    }
+    for (int r = 0; r < NINT; ++r) {
+      if (r == c) continue;
+      const double f = Ai[r * NINT + c];
+      if (f == 0.0) continue;
+      for (int q = 0; q < NINT; ++q) {
+        Ai[r * NINT + q] -= f * Ai[c * NINT + q];
+        inv[r * NINT + q] -= f * inv[c * NINT + q];
+      }
+    }
+  }
+  std::vector<double> G((size_t)rows_pad * cols_pad, 0.0);
+  for (int r = 0; r < NINT; ++r) {
+    for (int q = 0; q < NINT; ++q) G[r * cols_pad + q] = inv[r * NINT + q];
+    for (int c = 0; c < NEXT; ++c) {
+      double s = 0.0;
+      for (int q = 0; q < NINT; ++q) s += inv[r * NINT + q] * Aext[q * NEXT + c];
+      const int ib = r / NI, ia = r % NI;
+      const double e = (c == (ib + 1) * NE + ia + 1) ? 1.0 : 0.0;
+      G[r * cols_pad + NINT + c] = e - s;
+    }
+  }
+  return G;
+}
+
+}  // namespace host
+}  // namespace cf
+
+namespace cf {
+namespace host {
+// per-degree dense patch maps in global memory (p = 1..3), built once per process
+inline const double* cart_map(int p) {
+  static const double* maps[CF_MAXP + 1] = {nullptr};
+  if (p < 1 || p > 3) return nullptr;
+  if (!maps[p]) {
+    Tab t;
+    build_tab(p, t);
+    int rp = 0, cp = 0;
+    std::vector<double> G = cart_affine_map(p, t, rp, cp);
+    void* d = nullptr;
+    CF_CUDA(cudaMalloc(&d, G.size() * sizeof(double)));
+    CF_CUDA(cudaMemcpy(d, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice));
+    maps[p] = (const double*)d;
+  }
+  return maps[p];
+}
+}  // namespace host
+}  // namespace cf

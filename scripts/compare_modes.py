@@ -9,10 +9,11 @@ import workloads  # noqa: E402
 from paper_2508_11608_b200 import cutfem  # noqa: E402
 
 w = getattr(workloads, sys.argv[1] if len(sys.argv) > 1 else "CONFIG1")
-MODES = {"fused+pdl": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1"), "fused": dict(CUTFEM_FUSED="1", CUTFEM_PDL="0"),
-         "separate+pdl": dict(CUTFEM_FUSED="0", CUTFEM_PDL="1")}
+MODES = {"fused+pdl+mma": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="1"),
+         "fused+pdl (FD)": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="0"),
+         "separate+pdl": dict(CUTFEM_FUSED="0", CUTFEM_PDL="1", CUTFEM_MMA="1")}
 for mode, env in MODES.items():
-    for cut_mode in (0, 1):
+    for cut_mode in (0,):
         os.environ.update(env)
         g = cutfem.Problem.from_workload(w, cut_mode=cut_mode)
         L = w.n_levels - 1
