@@ -196,21 +196,39 @@ def main():
         dist.barrier()
     value = n_dofs * args.steps * world / (total_ms * 1e-3)
 
-    # ---- dominant kernel: Cartesian colour step, timed alone (live, CUDA events)
-    kms = []
-    n_cart = list(info.n_cart)
-    for c in range(4):
-        kms.append(timed(lambda: g.colour_step(L, 0, c, x, b), 50, 3))
-    cart_ms = float(np.mean([np.mean(k) for k in kms]))
+    # ---- kernels of the step, timed alone (live, CUDA events, L2 flushed)
     p = w.p
-    bytes_per_patch = 8 * ((2 * p) ** 2 + 2 * (2 * p - 1) ** 2)
-    cart_bytes = bytes_per_patch * float(np.mean(n_cart))
     peak, peak_src = measured_peak_hbm()
-    achieved = cart_bytes / (cart_ms * 1e-3) / 1e9
+    cart_ms = float(np.mean(timed(lambda: g.colour_step(L, 2, 0, x, b), 50, 3)))
+    cart_bytes = 24.0 * p * p * info.n_inside
+    cut_ms, cut_bytes = [], []
+    off, _ = g.cut_interior(L)
+    m_all = np.diff(off)
+    nb = (p + 1) ** 2
+    for c in range(4):
+        cut_ms.append(float(np.mean(timed(lambda: g.colour_step(L, 1, c, x, b), 50, 3))))
+        lo = int(sum(info.n_cutp[:c]))
+        m = m_all[lo:lo + info.n_cutp[c]].astype(np.float64)
+        cut_bytes.append(float(np.sum(8 * m * m + 8 * (2 * p + 1) ** 2 + 32 * m)) + 8.0 * nb * nb * info.n_cut / 4)
+    per_step = {"cart_sweep": cart_ms, "cut_colours": w.n_c * float(np.sum(cut_ms))}
+    kernels = {
+        "k_cart_fused_mma (4 Cartesian colours)": {
+            "launches_per_step": 1, "avg_launch_ms": cart_ms, "bytes_per_launch": cart_bytes,
+            "achieved_gbs": cart_bytes / (cart_ms * 1e-3) / 1e9},
+        "k_cut_colour_v3 + k_cut_apply (one cut colour)": {
+            "launches_per_step": 8 * w.n_c, "avg_launch_ms": float(np.mean(cut_ms)),
+            "bytes_per_launch": float(np.mean(cut_bytes)),
+            "achieved_gbs": float(np.mean(cut_bytes)) / (float(np.mean(cut_ms)) * 1e-3) / 1e9}}
+    if per_step["cart_sweep"] >= per_step["cut_colours"]:
+        dom, d_bytes, d_ms = "k_cart_fused_mma<P=%d> (fused Cartesian sweep)" % p, cart_bytes, cart_ms
+    else:
+        dom, d_bytes, d_ms = ("k_cut_colour_v3<P=%d> + k_cut_apply (cut colour step)" % p,
+                              float(np.mean(cut_bytes)), float(np.mean(cut_ms)))
+    achieved = d_bytes / (d_ms * 1e-3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "cart_colour_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("bytes_per_launch")
+        traffic = json.load(open(tp)).get(dom.split("<")[0])
 
     # ---- V-cycle and CG+MG time to solution
     z = g.zeros()
@@ -263,10 +281,11 @@ def main():
                        "parallelism": "replicas" if world > 1 else "single GPU"},
             "gpu_launches": int(launches),
             "clocks": clocks,
-            "roofline": {"bound": "hbm", "kernel": f"k_cart_colour<P={p}> (Cartesian colour step)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": cart_bytes, "avg_launch_ms": cart_ms},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": d_bytes, "avg_launch_ms": d_ms,
+                         "step_share_ms": per_step},
+            "kernels": kernels,
             "vcycle": {"ms": v_ms, "dofs_per_s": n_dofs / (v_ms * 1e-3)},
             "cg_mg": {"time_to_solution_ms": cg_ms, "iterations": it, "rel_residual": rel, "tol": w.tol,
                       "dofs_per_s": n_dofs / (cg_ms * 1e-3)},

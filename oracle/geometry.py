@@ -128,6 +128,38 @@ class Patch:
 CARTESIAN, CUTPATCH = 0, 1
 
 
+def vertex_patch(lv, I, J, vertices="active"):
+    """The patch of vertex (I, J) or None (see build_patches)."""
+    p = lv.p
+    block = [(i, j) for j in (J - 1, J) for i in (I - 1, I)]
+    cells = [c for c in block if lv.active(*c)]
+    if not cells:
+        return None
+    if vertices == "inside":
+        X = lv.x0 + I * lv.h - lv.circle.cx
+        Y = lv.y0 + J * lv.h - lv.circle.cy
+        if not X * X + Y * Y < lv.circle.r * lv.circle.r:
+            return None
+    pt = Patch()
+    pt.I, pt.J, pt.cells = I, J, cells
+    cellset = set(cells)
+    interior = []
+    for b in range(max(0, p * (J - 1)), min(lv.nl - 1, p * (J + 1)) + 1):
+        for a in range(max(0, p * (I - 1)), min(lv.nl - 1, p * (I + 1)) + 1):
+            if not lv.dof_mask[b, a]:
+                continue
+            if set(lv.node_support(a, b)) <= cellset:
+                interior.append(int(lv.dof_index[b * lv.nl + a]))
+    pt.interior = np.array(interior, dtype=np.int64)
+    all_inside = len(cells) == 4 and all(lv.ctype(*c) == INSIDE for c in cells)
+    nbrs = [(I - 2, J - 1), (I - 2, J), (I + 1, J - 1), (I + 1, J),
+            (I - 1, J - 2), (I, J - 2), (I - 1, J + 1), (I, J + 1)]
+    touches_ghost = any(lv.ctype(*c) == CUT for c in nbrs)
+    pt.kind = CARTESIAN if (all_inside and not touches_ghost) else CUTPATCH
+    pt.colour = (I % 2) + 2 * (J % 2)
+    return pt
+
+
 def build_patches(lv, vertices="active"):
     """Vertex patches with interior DoF sets, kind and colour.
 
@@ -144,37 +176,12 @@ def build_patches(lv, vertices="active"):
     cut patches (l.193).
     Colouring (l.179): colour = (I mod 2) + 2 (J mod 2); Cartesian and cut
     patches are listed separately (l.195-212).  Order: J-major, I-minor."""
-    p, n = lv.p, lv.n
     patches = []
-    for J in range(n + 1):
-        for I in range(n + 1):
-            block = [(i, j) for j in (J - 1, J) for i in (I - 1, I)]
-            cells = [c for c in block if lv.active(*c)]
-            if not cells:
-                continue
-            if vertices == "inside":
-                X = lv.x0 + I * lv.h - lv.circle.cx
-                Y = lv.y0 + J * lv.h - lv.circle.cy
-                if not X * X + Y * Y < lv.circle.r * lv.circle.r:
-                    continue
-            pt = Patch()
-            pt.I, pt.J, pt.cells = I, J, cells
-            cellset = set(cells)
-            interior = []
-            for b in range(max(0, p * (J - 1)), min(lv.nl - 1, p * (J + 1)) + 1):
-                for a in range(max(0, p * (I - 1)), min(lv.nl - 1, p * (I + 1)) + 1):
-                    if not lv.dof_mask[b, a]:
-                        continue
-                    if set(lv.node_support(a, b)) <= cellset:
-                        interior.append(int(lv.dof_index[b * lv.nl + a]))
-            pt.interior = np.array(interior, dtype=np.int64)
-            all_inside = len(cells) == 4 and all(lv.ctype(*c) == INSIDE for c in cells)
-            nbrs = [(I - 2, J - 1), (I - 2, J), (I + 1, J - 1), (I + 1, J),
-                    (I - 1, J - 2), (I, J - 2), (I - 1, J + 1), (I, J + 1)]
-            touches_ghost = any(lv.ctype(*c) == CUT for c in nbrs)
-            pt.kind = CARTESIAN if (all_inside and not touches_ghost) else CUTPATCH
-            pt.colour = (I % 2) + 2 * (J % 2)
-            patches.append(pt)
+    for J in range(lv.n + 1):
+        for I in range(lv.n + 1):
+            pt = vertex_patch(lv, I, J, vertices)
+            if pt is not None:
+                patches.append(pt)
     return patches
 
 

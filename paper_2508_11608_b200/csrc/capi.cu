@@ -139,11 +139,12 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
   return guarded([&]() {
     check_built(pb);
     check_level(pb, level);
-    cf::require((kind == 0 || kind == 1) && colour >= 0 && colour < 4, cf::ERR_ARG, "bad kind/colour");
+    cf::require(kind >= 0 && kind <= 2 && colour >= 0 && colour < 4, cf::ERR_ARG, "bad kind/colour");
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
     if (kind == 0) pb->p.cart_step(level, colour, x, b);
-    else pb->p.cut_step(level, colour, x, b);
+    else if (kind == 1) pb->p.cut_step(level, colour, x, b);
+    else pb->p.cart_fused(level, x, b, colour & 1);
   });
 }
 
