@@ -143,7 +143,11 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
     if (kind == 0) pb->p.cart_step(level, colour, x, b);
-    else if (kind == 1) pb->p.cut_step(level, colour, x, b);
+    else if (kind == 1 && pb->p.pingpong) {
+      cf::LevelData& D = pb->p.lv[level];
+      CF_CUDA(cudaMemcpyAsync(D.xs, x, (size_t)D.a.nl * D.a.ld * sizeof(double), cudaMemcpyDeviceToDevice, pb->p.st));
+      pb->p.cut_pp_step(level, colour, -1, D.xs, x, b);
+    } else if (kind == 1) pb->p.cut_step(level, colour, x, b);
     else pb->p.cart_fused(level, x, b, colour & 1);
   });
 }

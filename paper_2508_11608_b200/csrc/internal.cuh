@@ -111,6 +111,10 @@ struct LevelData {
   double* zbuf = nullptr;            // n_ent corrections (two-phase cut colour step)
   double* ecut = nullptr;            // cut-cell element matrices
   void* desc = nullptr;              // CutDesc per cut patch (smoother2.cuh)
+  double* xs = nullptr;              // shadow lattice vector for the ping-pong cut steps
+  int32_t* copy_lists = nullptr;     // node lists: [prev][cur] = N_prev \ N_cur (prev = 4: read band)
+  int copy_off[5][4] = {};           // offsets into copy_lists
+  int copy_n[5][4] = {};
   // workspace lattice vectors for the V-cycle
   double *x = nullptr, *b = nullptr, *r = nullptr;
 };

@@ -51,6 +51,7 @@ struct Problem {
   bool persistent = false;  // one cooperative launch per smoothing step (env CUTFEM_PERSISTENT=1)
   bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
   bool use_mma = true;      // Cartesian patch map on fp64 tensor cores (env CUTFEM_MMA=0 disables)
+  bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -159,6 +160,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_FUSED")) fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_PDL")) pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_MMA")) use_mma = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_PINGPONG")) pingpong = std::atoi(e) != 0;
     host::cart_map(prm.p);  // dense Cartesian patch map (p <= 3), built outside any graph capture
     d_count = alloc<int>(1);
     const int p = prm.p;
@@ -425,6 +427,7 @@ struct Problem {
                                                                           D.cutp_inv, (CutDesc*)D.desc)));
         CF_LAUNCHED();
       }
+      build_copy_lists(D);
       sync();
     }
     build_coarse();
@@ -442,6 +445,49 @@ struct Problem {
     for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
     sync();
     built = true;
+  }
+
+  // ping-pong copy lists (see k_cut_step): [prev][cur] = N_prev \ N_cur for
+  // prev, cur colours, and [4][cur] = band \ N_cur for the first step
+  void build_copy_lists(LevelData& D) {
+    const LevelArgs& L = D.a;
+    const int64_t nv = (int64_t)L.nl * L.ld;
+    D.xs = alloc<double>(nv);
+    CF_CUDA(cudaMemsetAsync(D.xs, 0, nv * 8, st));
+    uint8_t* marks = alloc<uint8_t>(5 * nv);
+    CF_CUDA(cudaMemsetAsync(marks, 0, 5 * nv, st));
+    for (int c = 0; c < 4; ++c)
+      if (D.ent_col_off[c + 1] > D.ent_col_off[c]) {
+        k_mark_entries<<<ceil_div(D.ent_col_off[c + 1] - D.ent_col_off[c], 256), 256, 0, st>>>(
+            D.ent_node, D.ent_col_off[c], D.ent_col_off[c + 1], marks + c * nv);
+        CF_LAUNCHED();
+      }
+    const int ncp = D.cutp_off[4];
+    if (ncp) {
+      k_mark_band<<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, ncp, L, marks + 4 * nv);
+      CF_LAUNCHED();
+    }
+    uint8_t* fl = alloc<uint8_t>(nv);
+    int* tmp = alloc<int>(nv);
+    std::vector<int> all;
+    for (int pv = 0; pv < 5; ++pv)
+      for (int c = 0; c < 4; ++c) {
+        D.copy_off[pv][c] = (int)all.size();
+        D.copy_n[pv][c] = 0;
+        if (pv == c) continue;
+        k_andnot_flags<<<ceil_div(nv, 256), 256, 0, st>>>(marks + pv * nv, marks + c * nv, nv, fl);
+        CF_LAUNCHED();
+        const int cnt = select(fl, (int)nv, tmp);
+        std::vector<int> h(cnt);
+        if (cnt) CF_CUDA(cudaMemcpyAsync(h.data(), tmp, sizeof(int) * cnt, cudaMemcpyDeviceToHost, st));
+        sync();
+        all.insert(all.end(), h.begin(), h.end());
+        D.copy_n[pv][c] = cnt;
+      }
+    D.copy_lists = alloc<int32_t>(all.size());
+    if (!all.empty())
+      CF_CUDA(cudaMemcpyAsync(D.copy_lists, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
+    sync();
   }
 
   void build_coarse() {
@@ -630,8 +676,57 @@ struct Problem {
     CF_LAUNCHED();
   }
 
+  // one ping-pong cut step: read R, write W (k_cut_step); prev = colour of the
+  // previous step (4 = first step of the sweep: copy the read band)
+  void cut_pp_step(int l, int c, int prev, const double* R, double* W, const double* b) {
+    LevelData& D = lv[l];
+    const int np = D.n_cutp[c];
+    const int ncopy = prev < 0 ? 0 : D.copy_n[prev][c];
+    const int32_t* cl = D.copy_lists + (prev < 0 ? 0 : D.copy_off[prev][c]);
+    if (!np && !ncopy) return;
+    const CutDesc* desc = (const CutDesc*)D.desc + D.cutp_off[c];
+    CF_DISPATCH(prm.p, {
+      const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
+      const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
+      const size_t smb = wpb * pw;
+      static bool attr = false;
+      if (!attr) {
+        CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+      }
+      const int pb = ceil_div(np, wpb), cb = ceil_div(ncopy, 128);
+      if (prm.cut_mode == 0)
+        launch(k_cut_step<P, false>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
+               (const double*)D.inv, R, W, b, cl, ncopy);
+      else
+        launch(k_cut_step<P, true>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
+               (const double*)D.inv, R, W, b, cl, ncopy);
+    });
+    CF_LAUNCHED();
+  }
+
+  // the n_c sweeps over the cut colours with ping-pong buffers (x, xs); an
+  // even number of steps (4 n_c) leaves the result in x
+  void cut_sweeps(int l, double* x, const double* b, int reverse) {
+    double* bufs[2] = {x, lv[l].xs};
+    int prev = 4, s = 0;
+    for (int rep = 0; rep < prm.n_c; ++rep)
+      for (int cc = 0; cc < 4; ++cc, ++s) {
+        const int c = reverse ? 3 - cc : cc;
+        cut_pp_step(l, c, prev, bufs[s & 1], bufs[(s + 1) & 1], b);
+        prev = c;
+      }
+  }
+
   // x <- S(x, b) (P eq. smoother-split, l.196-210; reverse = adjoint order, R9)
   void smooth(int l, double* x, const double* b, int reverse) {
+    if (pingpong && fused) {
+      if (!reverse) cart_fused(l, x, b, 0);
+      cut_sweeps(l, x, b, reverse);
+      if (reverse) cart_fused(l, x, b, 1);
+      return;
+    }
     if (persistent) {
       smooth_persistent(l, x, b, reverse);
       return;

@@ -622,7 +622,7 @@ namespace cf {
 template <int P>
 struct CutSmem3 {
   static constexpr int NB = (P + 1) * (P + 1), BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, NJ = 12 * P * (P + 1);
-  static constexpr int per_warp = WS * WS + 2 * NJ + MM + MM * MM + 4 * NB * NB;
+  static constexpr int per_warp = WS * WS + 2 * NJ + MM + MM * MM + 4 * NB * NB + MM;
 };
 
 // face f of the 12 faces touching the patch cells: axis 0 (x-faces) f = 2 s + t
@@ -914,6 +914,83 @@ __global__ void __launch_bounds__(256) k_cart_fused_mma(LevelArgs L, const int* 
     const int a = P * ci0 + cc, bb = P * cj0 + rr;
     x[(size_t)bb * L.ld + a] = Xs[(bb - b0) * RW + (a - a0)];
   }
+}
+
+}  // namespace cf
+
+namespace cf {
+
+// ---- cut colour step without a separate scatter (ping-pong buffers) --------
+// Step s reads R (the current state) and writes W, which before the step holds
+// the state two steps back, i.e. differs from R exactly on N_{s-1} (the
+// interior nodes of the previous step).  The kernel writes
+//   W[node] = R[node] + z   for node in N_s (this colour's interior sets)
+//   W[node] = R[node]       for node in N_{s-1} \ N_s   (copy list)
+// so that afterwards W holds the state after step s and R differs from it
+// exactly on N_s; R and W then swap.  No node is read and written in the same
+// launch, so the colour-start snapshot semantics (R9) hold without a second
+// kernel.  The first cut step of a sweep copies the whole read band instead.
+template <int P, bool QUAD>
+__global__ void __launch_bounds__(128) k_cut_step(LevelArgs L, const CutDesc* desc, int np, int wpb, int patch_blocks,
+                                                  const double* ecut, const double* inv, const double* R, double* W,
+                                                  const double* b, const int32_t* copy, int ncopy) {
+  using S = CutSmem3<P>;
+  constexpr int BS = S::BS, WS = S::WS, MM = S::MM, RPL = (MM + 31) / 32;
+  __shared__ SmTab T;
+  extern __shared__ double dsm[];
+  pdl_trigger();
+  if ((int)blockIdx.x >= patch_blocks) {
+    const int e = (blockIdx.x - patch_blocks) * blockDim.x + threadIdx.x;
+    const int32_t node = e < ncopy ? copy[e] : 0;
+    pdl_wait();
+    if (e < ncopy) W[node] = R[node];
+    return;
+  }
+  load_smtab<P>(T);
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w >= wpb) return;
+  const int k = blockIdx.x * wpb + w;
+  if (k >= np) return;
+  const CutDesc d = desc[k];
+  double* Wp = dsm + (size_t)w * S::per_warp;
+  double* zs = Wp + WS * WS + 2 * S::NJ + MM + MM * MM + 4 * S::NB * S::NB;  // per-warp tail: MM doubles
+  CutDesc dl = d;
+  dl.e0 = 0;
+  cut_patch_z3<P, QUAD>(L, dl, ecut, inv, R, b, zs, T, Wp);   // z_i -> zs[i]
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    const int loc = lane + 32 * t;
+    if (loc >= MM) continue;
+    const unsigned long long word = d.mask[loc >> 6];
+    if (!((word >> (loc & 63)) & 1ull)) continue;
+    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    const int ra = loc % BS, rb = loc / BS;
+    const double xr = Wp[(P + rb) * WS + P + ra];   // R at the node (window origin p(I-2), p(J-2))
+    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = xr + zs[i];
+  }
+}
+
+// marks of the interior nodes of one colour's cut patches / of the read band
+__global__ void k_mark_entries(const int32_t* ent_node, int64_t e0, int64_t e1, uint8_t* mark) {
+  const int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < e1) mark[ent_node[e]] = 1;
+}
+__global__ void k_mark_band(const CutDesc* desc, int np, LevelArgs L, uint8_t* mark) {
+  constexpr int MAXW = 4 * CF_MAXP + 1;
+  const int k = blockIdx.x;
+  if (k >= np) return;
+  const CutDesc d = desc[k];
+  const int WS = 4 * L.p + 1;
+  for (int e = threadIdx.x; e < WS * WS; e += blockDim.x) {
+    const int a = L.p * (d.I - 2) + e % WS, bb = L.p * (d.J - 2) + e / WS;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) mark[(size_t)bb * L.ld + a] = 1;
+  }
+  (void)MAXW;
+}
+__global__ void k_andnot_flags(const uint8_t* a, const uint8_t* b, int64_t n, uint8_t* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] && !b[i];
 }
 
 }  // namespace cf

@@ -9,9 +9,9 @@ import workloads  # noqa: E402
 from paper_2508_11608_b200 import cutfem  # noqa: E402
 
 w = getattr(workloads, sys.argv[1] if len(sys.argv) > 1 else "CONFIG1")
-MODES = {"fused+pdl+mma": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="1"),
-         "fused+pdl (FD)": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="0"),
-         "separate+pdl": dict(CUTFEM_FUSED="0", CUTFEM_PDL="1", CUTFEM_MMA="1")}
+MODES = {"default (fused+pdl+mma+pingpong)": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="1", CUTFEM_PINGPONG="1"),
+         "no pingpong": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="1", CUTFEM_PINGPONG="0"),
+         "no pdl": dict(CUTFEM_FUSED="1", CUTFEM_PDL="0", CUTFEM_MMA="1", CUTFEM_PINGPONG="1")}
 for mode, env in MODES.items():
     for cut_mode in (0,):
         os.environ.update(env)
