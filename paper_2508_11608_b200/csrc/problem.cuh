@@ -52,6 +52,7 @@ struct Problem {
   bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
   bool use_mma = true;      // Cartesian patch map on fp64 tensor cores (env CUTFEM_MMA=0 disables)
   bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
+  bool use_tma = true;      // TMA tile loads in the fused Cartesian sweep (env CUTFEM_TMA=0 disables)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -161,6 +162,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_PDL")) pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_MMA")) use_mma = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_PINGPONG")) pingpong = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_TMA")) use_tma = std::atoi(e) != 0;
     host::cart_map(prm.p);  // dense Cartesian patch map (p <= 3), built outside any graph capture
     d_count = alloc<int>(1);
     const int p = prm.p;
@@ -650,6 +652,21 @@ struct Problem {
     CF_DISPATCH(prm.p, {
       constexpr int TC = fused_tc<P>();
       if constexpr (P <= 3) {
+        if (use_mma && use_tma) {
+          const double* G = host::cart_map(P);
+          using S = CartTmaSmem<P, TC>;
+          const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
+          const CUtensorMap tmb = host::lattice_tmap(b, D.a.nl, D.a.ld, S::RWP, S::RW);
+          static bool attr3 = false;
+          if (!attr3) {
+            CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+            attr3 = true;
+          }
+          launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tmx, tmb, D.a,
+                 (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse);
+          CF_LAUNCHED();
+          return;
+        }
         if (use_mma) {
           const double* G = host::cart_map(P);
           const size_t smb = CartMMASmem<P, TC>::doubles * sizeof(double) + CartMMASmem<P, TC>::ints * sizeof(int);

@@ -994,3 +994,99 @@ __global__ void k_andnot_flags(const uint8_t* a, const uint8_t* b, int64_t n, ui
 }
 
 }  // namespace cf
+
+#include "tma.cuh"
+
+namespace cf {
+
+// ---- fused Cartesian sweep, v2: TMA tile loads, hoisted operand offsets ----
+template <int P, int TC>
+struct CartTmaSmem {
+  static constexpr int H = 4, RC = TC + 2 * H, RW = RC * P + 1, RWP = (RW + 1) & ~1;
+  static constexpr int tile_doubles = (RW * RWP + 15) & ~15;   // 128-byte aligned tiles (TMA destination)
+  static constexpr size_t bytes = 128 + 2 * tile_doubles * sizeof(double);
+};
+
+template <int P, int TC>
+__global__ void __launch_bounds__(256) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
+                                                        const __grid_constant__ CUtensorMap tmb, LevelArgs L,
+                                                        const int* tiles, const uint8_t* vk, const double* G,
+                                                        double* x, int reverse) {
+  using C = CartMMA<P>;
+  using S = CartTmaSmem<P, TC>;
+  constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS, MT = C::MT;
+  constexpr int H = S::H, RW = S::RW, RWP = S::RWP, TD = S::tile_doubles;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  uint64_t* bar = (uint64_t*)smraw;
+  double* Xs = (double*)(smraw + 128);   // x tile [RW][RWP]; the b tile follows at Xs + TD
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = L.n;
+  pdl_trigger();
+  // operand offsets of this lane's k slots (x block / b interior), interior row offsets
+  int ko[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int k = 4 * ks + (lane & 3);
+    int v = -1;
+    if (k < NINT) v = TD + (k / NI + 1) * RWP + k % NI + 1;
+    else if (k < K) v = ((k - NINT) / NE) * RWP + (k - NINT) % NE;
+    ko[ks] = v;
+  }
+  double af[MT][KS];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int s = 0; s < KS; ++s) af[mt][s] = G[(8 * mt + (lane >> 2)) * C::COLS + 4 * s + (lane & 3)];
+  const int tile = tiles[blockIdx.x];
+  const int ci0 = (tile & 0xffff) * TC, cj0 = (tile >> 16) * TC;
+  const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  pdl_wait();
+  if (tid == 0) {
+    mbar_expect_tx(bar, 2u * RW * RWP * sizeof(double));
+    tma_load_2d(Xs, &tmx, a0, b0, bar);
+    tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
+  }
+  mbar_wait(bar, 0);
+  for (int s = 0; s < 4; ++s) {
+    const int c = reverse ? 3 - s : s, rad = 3 - s;
+    const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
+    const int nvx = (ci0 + TC + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
+    const int np = nvx * nvy, ng = (np + 7) / 8;
+    for (int g = warp; g < ng; g += 8) {
+      const int pq = 8 * g + (lane >> 2);
+      const int pj = pq / nvx, pi = pq - pj * nvx;
+      const int I = ilo + 2 * pi, J = jlo + 2 * pj;
+      const bool cart = pq < np && I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART;
+      const int base = cart ? P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H)) : -1;
+      double acc[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const double v = (base >= 0 && ko[ks] >= 0) ? Xs[base + ko[ks]] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma(af[mt][ks], v, acc[mt][0], acc[mt][1]);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int bo = __shfl_sync(0xffffffffu, base, 4 * (2 * (lane & 3) + i));
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int r = 8 * mt + (lane >> 2);
+          if (bo >= 0 && r < NINT) Xs[bo + (r / NI + 1) * RWP + r % NI + 1] = acc[mt][i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
+  const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
+  for (int bb = P * cj0 + warp; bb < bhi; bb += 8) {
+    const double* src = Xs + (bb - b0) * RWP - a0;
+    double* dst = x + (size_t)bb * L.ld;
+    for (int a = P * ci0 + lane; a < ahi; a += 32) dst[a] = src[a];
+  }
+}
+
+}  // namespace cf
