@@ -1004,7 +1004,9 @@ template <int P, int TC>
 struct CartTmaSmem {
   static constexpr int H = 4, RC = TC + 2 * H, RW = RC * P + 1, RWP = (RW + 1) & ~1;
   static constexpr int tile_doubles = (RW * RWP + 15) & ~15;   // 128-byte aligned tiles (TMA destination)
-  static constexpr size_t bytes = 128 + 2 * tile_doubles * sizeof(double);
+  static constexpr int maxp = ((TC + 7) / 2 + 1) * ((TC + 7) / 2 + 1);
+  static constexpr int head = ((16 + 4 * maxp) + 127) & ~127;     // mbarrier, count, patch list
+  static constexpr size_t bytes = head + 2 * tile_doubles * sizeof(double);
 };
 
 template <int P, int TC>
@@ -1014,14 +1016,18 @@ __global__ void __launch_bounds__(256) k_cart_fused_tma(const __grid_constant__ 
                                                         double* x, int reverse) {
   using C = CartMMA<P>;
   using S = CartTmaSmem<P, TC>;
-  constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS, MT = C::MT;
+  constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
+  constexpr int MF = NINT / 8;                 // full 8-row tiles on the tensor cores
+  constexpr int RR = NINT - 8 * MF;            // remainder rows on the FMA pipe (p = 1: 1, p = 2: 1, p = 3: 1)
   constexpr int H = S::H, RW = S::RW, RWP = S::RWP, TD = S::tile_doubles;
+  constexpr int MAXP = ((TC + 7) / 2 + 1) * ((TC + 7) / 2 + 1);   // candidate patches of the widest pass
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* bar = (uint64_t*)smraw;
-  double* Xs = (double*)(smraw + 128);   // x tile [RW][RWP]; the b tile follows at Xs + TD
+  int* plist = (int*)(smraw + 16);             // compacted Cartesian patches of a pass (block origins)
+  int* pcount = (int*)(smraw + 8);
+  double* Xs = (double*)(smraw + S::head);     // x tile [RW][RWP]; the b tile follows at Xs + TD
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = L.n;
   pdl_trigger();
-  // operand offsets of this lane's k slots (x block / b interior), interior row offsets
   int ko[KS];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
@@ -1031,11 +1037,16 @@ __global__ void __launch_bounds__(256) k_cart_fused_tma(const __grid_constant__ 
     else if (k < K) v = ((k - NINT) / NE) * RWP + (k - NINT) % NE;
     ko[ks] = v;
   }
-  double af[MT][KS];
+  double af[MF > 0 ? MF : 1][KS];
+  double gr[RR > 0 ? RR : 1][KS];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
+  for (int mt = 0; mt < MF; ++mt)
 #pragma unroll
     for (int s = 0; s < KS; ++s) af[mt][s] = G[(8 * mt + (lane >> 2)) * C::COLS + 4 * s + (lane & 3)];
+#pragma unroll
+  for (int rr = 0; rr < RR; ++rr)
+#pragma unroll
+    for (int s = 0; s < KS; ++s) gr[rr][s] = G[(8 * MF + rr) * C::COLS + 4 * s + (lane & 3)];
   const int tile = tiles[blockIdx.x];
   const int ci0 = (tile & 0xffff) * TC, cj0 = (tile >> 16) * TC;
   const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
@@ -1047,34 +1058,53 @@ __global__ void __launch_bounds__(256) k_cart_fused_tma(const __grid_constant__ 
     tma_load_2d(Xs, &tmx, a0, b0, bar);
     tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
   }
-  mbar_wait(bar, 0);
   for (int s = 0; s < 4; ++s) {
     const int c = reverse ? 3 - s : s, rad = 3 - s;
     const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
     const int nvx = (ci0 + TC + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
-    const int np = nvx * nvy, ng = (np + 7) / 8;
+    // compact the Cartesian patches of this pass
+    if (tid == 0) *pcount = 0;
+    __syncthreads();
+    for (int q = tid; q < nvx * nvy; q += 256) {
+      const int pj = q / nvx, pi = q - pj * nvx;
+      const int I = ilo + 2 * pi, J = jlo + 2 * pj;
+      if (I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART)
+        plist[atomicAdd(pcount, 1)] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
+    }
+    if (s == 0) mbar_wait(bar, 0);
+    __syncthreads();
+    const int np = *pcount, ng = (np + 7) / 8;
     for (int g = warp; g < ng; g += 8) {
       const int pq = 8 * g + (lane >> 2);
-      const int pj = pq / nvx, pi = pq - pj * nvx;
-      const int I = ilo + 2 * pi, J = jlo + 2 * pj;
-      const bool cart = pq < np && I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART;
-      const int base = cart ? P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H)) : -1;
-      double acc[MT][2];
+      const int base = pq < np ? plist[pq] : -1;
+      double acc[MF > 0 ? MF : 1][2][2];
+      double rs[RR > 0 ? RR : 1];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+      for (int mt = 0; mt < MF; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < RR; ++rr) rs[rr] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         const double v = (base >= 0 && ko[ks] >= 0) ? Xs[base + ko[ks]] : 0.0;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) dmma(af[mt][ks], v, acc[mt][0], acc[mt][1]);
+        for (int mt = 0; mt < MF; ++mt) dmma(af[mt][ks], v, acc[mt][ks & 1][0], acc[mt][ks & 1][1]);
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) rs[rr] = fma(gr[rr][ks], v, rs[rr]);
+      }
+#pragma unroll
+      for (int rr = 0; rr < RR; ++rr) {
+        rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], 1);
+        rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], 2);
+        const int r = 8 * MF + rr;
+        if ((lane & 3) == 0 && base >= 0) Xs[base + (r / NI + 1) * RWP + r % NI + 1] = rs[rr];
       }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int bo = __shfl_sync(0xffffffffu, base, 4 * (2 * (lane & 3) + i));
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
+        for (int mt = 0; mt < MF; ++mt) {
           const int r = 8 * mt + (lane >> 2);
-          if (bo >= 0 && r < NINT) Xs[bo + (r / NI + 1) * RWP + r % NI + 1] = acc[mt][i];
+          if (bo >= 0) Xs[bo + (r / NI + 1) * RWP + r % NI + 1] = acc[mt][0][i] + acc[mt][1][i];
         }
       }
     }
