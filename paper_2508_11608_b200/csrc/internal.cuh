@@ -39,6 +39,7 @@ struct Tab {
 
 // single translation unit (capi.cu): the tables are defined here
 __constant__ Tab c_tab[CF_MAXP + 1];
+__device__ Tab g_tab[CF_MAXP + 1];   // global-memory copy for lane-varying (coalesced) reads
 __constant__ double c_gx[CF_MAXNQ + 1][CF_MAXNQ];  // Gauss-Legendre points on [0,1], c_gx[n][i]
 __constant__ double c_gw[CF_MAXNQ + 1][CF_MAXNQ];
 

@@ -26,7 +26,7 @@ struct SmTab {
 
 template <int P>
 __device__ __forceinline__ void load_smtab(SmTab& s) {
-  const Tab& T = c_tab[P];
+  const Tab& T = g_tab[P];   // global copy: lane-varying indices would serialise constant-bank reads
   for (int e = threadIdx.x + blockDim.x * threadIdx.y; e < (CF_MAXP + 1) * (CF_MAXP + 1);
        e += blockDim.x * blockDim.y) {
     int i = e / (CF_MAXP + 1), j = e % (CF_MAXP + 1);

@@ -221,6 +221,7 @@ inline void upload_tables() {
   std::memset(&tabs[0], 0, sizeof(Tab));
   for (int p = 1; p <= CF_MAXP; ++p) build_tab(p, tabs[p]);
   CF_CUDA(cudaMemcpyToSymbol(c_tab, tabs, sizeof(tabs)));
+  CF_CUDA(cudaMemcpyToSymbol(g_tab, tabs, sizeof(tabs)));
   double gx[CF_MAXNQ + 1][CF_MAXNQ] = {}, gw[CF_MAXNQ + 1][CF_MAXNQ] = {};
   for (int n = 1; n <= CF_MAXNQ; ++n) gauss_legendre(n, gx[n], gw[n]);
   CF_CUDA(cudaMemcpyToSymbol(c_gx, gx, sizeof(gx)));
