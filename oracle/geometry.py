@@ -37,6 +37,8 @@ class Level:
         self.circle = circle
         self.h = self.length / self.n           # R1: h = L / n, fp64 division
         self.nl = self.n * self.p + 1           # lattice nodes per side
+        self.dim = 2
+        self.n_colours = 4
         self.cell_type = classify_cells(self)
         self.dof_mask = node_mask(self)
         self.dof_index = -np.ones(self.nl * self.nl, dtype=np.int64)
@@ -122,7 +124,7 @@ def ghost_faces(lv):
 
 
 class Patch:
-    __slots__ = ("I", "J", "cells", "kind", "colour", "interior")
+    __slots__ = ("I", "J", "K", "cells", "kind", "colour", "interior")
 
 
 CARTESIAN, CUTPATCH = 0, 1

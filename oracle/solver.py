@@ -26,9 +26,15 @@ from .transfer import prolongation_matrix
 class LevelData:
     def __init__(self, lv, prm, vertices="active"):
         self.lv = lv
-        self.A = assemble_matrix(lv, prm)
-        self.patches = build_patches(lv, vertices)
-        self.groups = {(k, c): [] for k in (CARTESIAN, CUTPATCH) for c in range(4)}
+        if getattr(lv, "dim", 2) == 3:
+            from .dim3 import assemble_matrix3, build_patches3
+            self.A = assemble_matrix3(lv, prm)
+            self.patches = build_patches3(lv)
+        else:
+            self.A = assemble_matrix(lv, prm)
+            self.patches = build_patches(lv, vertices)
+        self.nc = lv.n_colours
+        self.groups = {(k, c): [] for k in (CARTESIAN, CUTPATCH) for c in range(self.nc)}
         self.inv = []
         for idx, pt in enumerate(self.patches):
             self.groups[(pt.kind, pt.colour)].append(idx)
@@ -54,7 +60,7 @@ class LevelData:
         colours 0..3, then n_c sweeps over cut colours 0..3.  reverse=True
         applies the steps in the opposite order (the adjoint sweep, used as
         post-smoother; reading R9)."""
-        seq = [(CARTESIAN, c) for c in range(4)] + [(CUTPATCH, c) for _ in range(n_c) for c in range(4)]
+        seq = [(CARTESIAN, c) for c in range(self.nc)] + [(CUTPATCH, c) for _ in range(n_c) for c in range(self.nc)]
         if reverse:
             seq = seq[::-1]
         for kind, c in seq:
@@ -65,14 +71,20 @@ class LevelData:
 class Hierarchy:
     """Levels 0..L of PAPER.md l.65-69 with operators, patches and transfers."""
 
-    def __init__(self, x0, y0, length, n0, n_levels, circle, p, prm=None, n_c=2, symmetric=True, vertices="active"):
+    def __init__(self, x0, y0, length, n0, n_levels, circle, p, prm=None, n_c=2, symmetric=True, vertices="active",
+                 levels=None):
         self.prm = prm if prm is not None else Params()
         self.p = p
         self.n_c = n_c
         self.symmetric = symmetric
-        self.levels = [LevelData(lv, self.prm, vertices) for lv in hierarchy(x0, y0, length, n0, n_levels, circle, p)]
-        self.P = [None] + [prolongation_matrix(self.levels[l - 1].lv, self.levels[l].lv)
-                           for l in range(1, n_levels)]
+        if levels is None:
+            levels = hierarchy(x0, y0, length, n0, n_levels, circle, p)
+        self.levels = [LevelData(lv, self.prm, vertices) for lv in levels]
+        if getattr(levels[0], "dim", 2) == 3:
+            from .dim3 import prolongation_matrix3 as prolong
+        else:
+            prolong = prolongation_matrix
+        self.P = [None] + [prolong(self.levels[l - 1].lv, self.levels[l].lv) for l in range(1, len(levels))]
         A0 = self.levels[0].A.toarray()
         self.A0inv = np.linalg.inv(A0)
 
@@ -197,6 +209,11 @@ def fractional_iterations(n_it, r_final, r_0):
 
 
 def from_workload(w, prm=None, **kw):
-    """Hierarchy for a workloads.Workload description."""
+    """Hierarchy for a workloads.Workload description (2D circle or 3D sphere)."""
+    if getattr(w, "dim", 2) == 3:
+        from .dim3 import Level3, Sphere
+        sph = Sphere(w.cx, w.cy, w.cz, w.r)
+        levels = [Level3(w.x0, w.y0, w.z0, w.length, w.n_coarse * 2 ** l, sph, w.p) for l in range(w.n_levels)]
+        return Hierarchy(None, None, None, None, None, None, w.p, prm=prm, n_c=w.n_c, levels=levels, **kw)
     return Hierarchy(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, Circle(w.cx, w.cy, w.r), w.p,
                      prm=prm, n_c=w.n_c, **kw)

@@ -28,6 +28,9 @@ class Workload:
     p: int             # Q_p degree
     n_c: int = 2       # cut-patch sweeps per smoothing step
     tol: float = 1e-8  # CG relative residual tolerance
+    dim: int = 2       # 3: sphere (cx, cy, cz, r) in the cube [x0, x0+length]^3
+    z0: float = 0.0
+    cz: float = 0.0
 
     @property
     def n_fine(self):
@@ -42,6 +45,16 @@ CONFIG0 = Workload("config0-circle-r0.3-Q1-16x16", -0.5, -0.5, 1.0, 4, 3, 0.0, 0
 # fp64".  The circle is the paper's section-4 setup (unit circle, 2x2 coarse
 # mesh, box [-1.105,1.105]^2 -- reading R1 in DESIGN.md).
 CONFIG1 = Workload("config1-circle-Q2-512x512", -1.105, -1.105, 2.21, 2, 9, 0.0, 0.0, 1.0, 2)
+
+
+# BASELINE.json configs[2]: "3D sphere, Q2, 128^3 background mesh, 1 GPU,
+# fp64" -- the 3D analogue of the section-4 setup (unit sphere in
+# [-1.105,1.105]^3, 2^3 coarse cells, levels up to 128^3).
+CONFIG2 = Workload("config2-sphere-Q2-128^3", -1.105, -1.105, 2.21, 2, 7, 0.0, 0.0, 1.0, 2, dim=3, z0=-1.105, cz=0.0)
+
+
+def sphere(name, n_coarse, n_levels, p, x0=-1.105, length=2.21, c=(0.0, 0.0, 0.0), r=1.0):
+    return Workload(name, x0, x0, length, n_coarse, n_levels, c[0], c[1], r, p, dim=3, z0=x0, cz=c[2])
 
 
 def paper_level(p, L, n_c=2, tol=1e-9):
@@ -61,7 +74,7 @@ def lattice_nodes(w, level=None):
 def lattice_vector(w, seed, level=None):
     """Seeded N(0,1) values on every lattice node of a level (unmasked)."""
     nl = lattice_nodes(w, level)
-    return np.random.default_rng(seed).standard_normal(nl * nl)
+    return np.random.default_rng(seed).standard_normal(nl ** w.dim)
 
 
 def with_degree(w, p):
