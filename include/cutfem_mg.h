@@ -17,7 +17,8 @@
  *    stream).  Device work is queued on it asynchronously unless the call
  *    says otherwise.
  *  - Vectors are DEVICE pointers to fp64 "lattice vectors" of a level: NL rows
- *    of LD doubles (cutfem_level_info), entry [b*LD + a] is lattice node
+ *    (NL*NL rows in 3D, row c*NL + b) of LD doubles (cutfem_level_info),
+ *    entry [b*LD + a] (3D: [(c*NL + b)*LD + a]) is lattice node
  *    (a, b) = x-index a, y-index b, at position
  *    x0 + (a div p + xi_{a mod p}) h (xi = Gauss-Lobatto nodes on [0,1]).
  *    Entries of nodes that carry no DoF (P l.121: no DoFs on exterior cells)
@@ -63,18 +64,21 @@ typedef struct {
   int symmetric;        /* 1: post-smoother = reverse colour order (R9, needed by CG) */
   int cut_mode;         /* cut-cell operator: 0 = element matrix of bulk + Nitsche terms precomputed
                            from the cut quadrature at setup, 1 = quadrature on the fly */
+  int dim;              /* 2 (circle, default when 0) or 3 (sphere; degree 1..2) */
+  double z0, cz;        /* 3D: box corner z and sphere centre z (the box is a cube of side length) */
 } cutfem_params;
 
 /* Per-level sizes and counts. */
 typedef struct {
+  int dim;              /* 2 or 3 */
   int n;                /* cells per side */
   int nl;               /* lattice nodes per side = n p + 1 */
   int ld;               /* row stride of lattice vectors (doubles), even, >= nl */
   int64_t n_dofs;       /* active DoFs n_l (P l.120) */
   int n_inside, n_cut;  /* cells of M_{l,Omega} \ M_{l,Gamma} and of M_{l,Gamma} (P l.69) */
   int n_ghost_faces;    /* |F_G| (P l.97-101) */
-  int n_cart[4];        /* Cartesian patches per colour (R4) */
-  int n_cutp[4];        /* cut patches per colour */
+  int n_cart[8];        /* Cartesian patches per colour (R4); 4 colours in 2D, 8 in 3D */
+  int n_cutp[8];        /* cut patches per colour */
   int64_t n_vol_qp, n_surf_qp; /* cut-cell quadrature points (R6) */
   double h;
 } cutfem_level_info;

@@ -55,6 +55,12 @@ class Level3:
         h = self.h
         return np.array([self.x0 + i * h, self.y0 + j * h, self.z0 + k * h])
 
+    def hi(self, i, j, k):
+        """x0 + (i+1) h (reading R2: the same fp64 expression as the
+        classification, not lo + h)"""
+        h = self.h
+        return np.array([self.x0 + (i + 1.0) * h, self.y0 + (j + 1.0) * h, self.z0 + (k + 1.0) * h])
+
     def ctype(self, i, j, k):
         n = self.n
         if 0 <= i < n and 0 <= j < n and 0 <= k < n:
@@ -260,7 +266,7 @@ def eval_basis3(lv, i, j, k, pts):
 def cell_matrix3(lv, i, j, k, prm):
     ct = lv.cell_type[k, j, i]
     lo = lv.lo(i, j, k)
-    hi = lo + lv.h
+    hi = lv.hi(i, j, k)
     if ct == INSIDE:
         vp, vw = tensor_gauss3(lo, hi, prm.n_q)
         sp_ = np.zeros((0, 3)); sw = np.zeros(0); sn = np.zeros((0, 3))

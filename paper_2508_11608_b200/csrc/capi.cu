@@ -44,6 +44,8 @@ int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* ou
   return guarded([&]() {
     cf::require(prm != nullptr && out != nullptr, cf::ERR_ARG, "null argument");
     cf::require(prm->degree >= 1 && prm->degree <= CF_MAXP, cf::ERR_ARG, "degree must be 1..4");
+    cf::require(prm->dim == 0 || prm->dim == 2 || prm->dim == 3, cf::ERR_ARG, "dim must be 2 or 3");
+    cf::require(prm->dim != 3 || prm->degree <= 2, cf::ERR_ARG, "3D supports degree 1..2");
     cf::require(prm->n_coarse >= 1 && prm->n_levels >= 1 && prm->n_levels <= 16, cf::ERR_ARG, "bad level counts");
     cf::require(((int64_t)prm->n_coarse << (prm->n_levels - 1)) * prm->degree < 60000, cf::ERR_SIZE,
                 "finest lattice too large");
@@ -53,8 +55,11 @@ int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* ou
     *out = nullptr;
     auto* pb = new cutfem_problem_s();
     cf::Params& P = pb->p.prm;
+    P.dim = prm->dim == 3 ? 3 : 2;
     P.x0 = prm->x0;
     P.y0 = prm->y0;
+    P.z0 = prm->z0;
+    P.cz = prm->cz;
     P.length = prm->length;
     P.cx = prm->cx;
     P.cy = prm->cy;
@@ -106,7 +111,8 @@ int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out) 
     out->n_inside = D.n_inside;
     out->n_cut = D.a.n_cut;
     out->n_ghost_faces = D.a.n_ghost;
-    for (int c = 0; c < 4; ++c) {
+    out->dim = pb->p.prm.dim;
+    for (int c = 0; c < 8; ++c) {
       out->n_cart[c] = D.n_cart[c];
       out->n_cutp[c] = D.n_cutp[c];
     }
@@ -139,13 +145,18 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
   return guarded([&]() {
     check_built(pb);
     check_level(pb, level);
-    cf::require(kind >= 0 && kind <= 2 && colour >= 0 && colour < 4, cf::ERR_ARG, "bad kind/colour");
+    cf::require(kind >= 0 && kind <= 2 && colour >= 0 && colour < 8, cf::ERR_ARG, "bad kind/colour");
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
-    if (kind == 0) pb->p.cart_step(level, colour, x, b);
+    if (pb->p.prm.dim == 3) {
+      cf::require(kind <= 1 && colour < 8, cf::ERR_ARG, "3D colour step: kind 0/1, colour 0..7");
+      if (kind == 0) pb->p.cart_step3(level, colour, x, b);
+      else pb->p.cut_step3(level, colour, x, b);
+    } else if (kind == 0) pb->p.cart_step(level, colour, x, b);
     else if (kind == 1 && pb->p.pingpong) {
+      cf::require(colour < 4, cf::ERR_ARG, "2D colours are 0..3");
       cf::LevelData& D = pb->p.lv[level];
-      CF_CUDA(cudaMemcpyAsync(D.xs, x, (size_t)D.a.nl * D.a.ld * sizeof(double), cudaMemcpyDeviceToDevice, pb->p.st));
+      CF_CUDA(cudaMemcpyAsync(D.xs, x, (size_t)pb->p.vsize(level) * sizeof(double), cudaMemcpyDeviceToDevice, pb->p.st));
       pb->p.cut_pp_step(level, colour, -1, D.xs, x, b);
     } else if (kind == 1) pb->p.cut_step(level, colour, x, b);
     else pb->p.cart_fused(level, x, b, colour & 1);
@@ -175,9 +186,9 @@ int cutfem_solve_cg_mg(cutfem_problem pb, double* x, const double* b, double tol
 
 static void host_buffers(cutfem_problem pb) {
   if (!pb->p.hx) {
-    const cf::LevelArgs& F = pb->p.lv.back().a;
-    pb->p.hx = pb->p.alloc<double>((int64_t)F.nl * F.ld);
-    pb->p.hb = pb->p.alloc<double>((int64_t)F.nl * F.ld);
+    const int64_t nv = pb->p.vsize(pb->p.prm.n_levels - 1);
+    pb->p.hx = pb->p.alloc<double>(nv);
+    pb->p.hb = pb->p.alloc<double>(nv);
   }
 }
 
@@ -189,8 +200,7 @@ int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const doubl
     cf::require(x_host && b_host, cf::ERR_ARG, "null vector");
     use_stream(pb, stream);
     host_buffers(pb);
-    const cf::LevelArgs& L = pb->p.lv[level].a;
-    const size_t bytes = (size_t)L.nl * L.ld * sizeof(double);
+    const size_t bytes = (size_t)pb->p.vsize(level) * sizeof(double);
     CF_CUDA(cudaMemcpyAsync(pb->p.hx, x_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
     CF_CUDA(cudaMemcpyAsync(pb->p.hb, b_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
     double* dx = pb->p.hx;
@@ -208,8 +218,7 @@ int cutfem_solve_cg_mg_host(cutfem_problem pb, double* x_host, const double* b_h
     cf::require(x_host && b_host, cf::ERR_ARG, "null vector");
     use_stream(pb, stream);
     host_buffers(pb);
-    const cf::LevelArgs& F = pb->p.lv.back().a;
-    const size_t bytes = (size_t)F.nl * F.ld * sizeof(double);
+    const size_t bytes = (size_t)pb->p.vsize(pb->p.prm.n_levels - 1) * sizeof(double);
     CF_CUDA(cudaMemcpyAsync(pb->p.hb, b_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
     pb->p.solve_cg(pb->p.hx, pb->p.hb, tol, max_it, iters, rel_res);
     CF_CUDA(cudaMemcpyAsync(x_host, pb->p.hx, bytes, cudaMemcpyDeviceToHost, pb->p.st));
@@ -242,7 +251,8 @@ int cutfem_export_cell_types(cutfem_problem pb, int level, int8_t* host_out) {
     check_level(pb, level);
     cf::require(host_out != nullptr, cf::ERR_ARG, "null output");
     const cf::LevelData& D = pb->p.lv[level];
-    CF_CUDA(cudaMemcpy(host_out, D.ctype, (size_t)D.a.n * D.a.n, cudaMemcpyDeviceToHost));
+    const size_t nc = (size_t)D.a.n * D.a.n * (pb->p.prm.dim == 3 ? D.a.n : 1);
+    CF_CUDA(cudaMemcpy(host_out, D.ctype, nc, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -251,7 +261,8 @@ int cutfem_export_dof_mask(cutfem_problem pb, int level, uint8_t* host_out) {
     check_level(pb, level);
     cf::require(host_out != nullptr, cf::ERR_ARG, "null output");
     const cf::LevelArgs& L = pb->p.lv[level].a;
-    CF_CUDA(cudaMemcpy2D(host_out, L.nl, pb->p.lv[level].mask, L.ld, L.nl, L.nl, cudaMemcpyDeviceToHost));
+    const int rows = L.nl * (pb->p.prm.dim == 3 ? L.nl : 1);
+    CF_CUDA(cudaMemcpy2D(host_out, L.nl, pb->p.lv[level].mask, L.ld, L.nl, rows, cudaMemcpyDeviceToHost));
   });
 }
 
@@ -259,7 +270,8 @@ int cutfem_export_patches(cutfem_problem pb, int level, int kind, int colour, in
   return guarded([&]() {
     check_built(pb);
     check_level(pb, level);
-    cf::require((kind == 0 || kind == 1) && colour >= 0 && colour < 4 && count, cf::ERR_ARG, "bad kind/colour");
+    cf::require((kind == 0 || kind == 1) && colour >= 0 && colour < (pb->p.prm.dim == 3 ? 8 : 4) && count, cf::ERR_ARG,
+                "bad kind/colour");
     const cf::LevelData& D = pb->p.lv[level];
     const int* off = kind == 0 ? D.cart_off : D.cutp_off;
     const int* list = kind == 0 ? D.cart_list : D.cutp_list;
@@ -275,7 +287,7 @@ int cutfem_export_cut_interior(cutfem_problem pb, int level, int64_t* host_offse
     check_built(pb);
     check_level(pb, level);
     const cf::LevelData& D = pb->p.lv[level];
-    const int ncp = D.cutp_off[4];
+    const int ncp = D.cutp_off[pb->p.prm.dim == 3 ? 8 : 4];
     if (n_patches) *n_patches = ncp;
     if (n_entries) *n_entries = D.n_ent;
     if (host_offsets) CF_CUDA(cudaMemcpy(host_offsets, D.cutp_ent, sizeof(int64_t) * (ncp + 1), cudaMemcpyDeviceToHost));
@@ -283,7 +295,7 @@ int cutfem_export_cut_interior(cutfem_problem pb, int level, int64_t* host_offse
       std::vector<int32_t> tmp(D.n_ent);
       CF_CUDA(cudaMemcpy(tmp.data(), D.ent_node, sizeof(int32_t) * D.n_ent, cudaMemcpyDeviceToHost));
       for (int64_t e = 0; e < D.n_ent; ++e) {
-        int b = tmp[e] / D.a.ld, a = tmp[e] % D.a.ld;
+        int b = tmp[e] / D.a.ld, a = tmp[e] % D.a.ld;   // b = row (c nl + b in 3D)
         host_nodes[e] = b * D.a.nl + a;
       }
     }

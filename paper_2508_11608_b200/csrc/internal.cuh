@@ -46,8 +46,9 @@ __constant__ double c_gw[CF_MAXNQ + 1][CF_MAXNQ];
 // Per-level arguments passed by value to every kernel.
 struct LevelArgs {
   int n, p, nl, ld;
-  double h, x0, y0;
-  double cx, cy, r;
+  int dim;                           // 2 or 3
+  double h, x0, y0, z0;
+  double cx, cy, cz, r;
   double gDh;                        // gamma_D / h
   double gs[CF_MAXP + 1];            // ghost scale gamma_k h^(sigma+1) / (k!)^2 (index k = 1..p)
   const int8_t* ctype;               // n*n
@@ -56,11 +57,12 @@ struct LevelArgs {
   const int* cut_list;               // packed i + n*j
   int n_cut;
   const int* q_off;                  // n_cut+1, volume points
-  const double *qx, *qy, *qw;        // reference coordinates, physical weight
+  const double *qx, *qy, *qz, *qw;   // reference coordinates, physical weight
   const int* s_off;                  // n_cut+1, surface points
-  const double *sx, *sy, *sw, *snx, *sny;
+  const double *sx, *sy, *sz, *sw, *snx, *sny, *snz;
   const int* gx_id;                  // face (i,j)|(i+1,j) -> ghost id or -1, index j*n+i
   const int* gy_id;                  // face (i,j)|(i,j+1)
+  const int* gz_id;                  // 3D: face (i,j,k)|(i,j,k+1)
   const int* ghost_list;             // packed axis | i << 1 | j << 16... see setup
   int n_ghost;
   double* ycut;                      // n_cut * (p+1)^2 scratch (operator apply)
@@ -78,34 +80,35 @@ struct LevelData {
   int* cut_id = nullptr;
   int* cut_list = nullptr;
   int* q_off = nullptr;
-  double* qbuf = nullptr;            // qx|qy|qw
+  double* qbuf = nullptr;            // qx|qy|(qz)|qw
   int* s_off = nullptr;
-  double* sbuf = nullptr;            // sx|sy|sw|snx|sny
+  double* sbuf = nullptr;            // sx|sy|(sz)|sw|snx|sny|(snz)
   int64_t n_vq = 0, n_sq = 0;
   int* gx_id = nullptr;
   int* gy_id = nullptr;
+  int* gz_id = nullptr;
   int* ghost_list = nullptr;
   double* ycut = nullptr;
   double* jm = nullptr;
   // patches
-  uint8_t* vkind = nullptr;          // (n+1)^2
-  int n_cart[4] = {0, 0, 0, 0};
+  uint8_t* vkind = nullptr;          // (n+1)^dim
+  int n_cart[8] = {};
   int* cart_list = nullptr;          // all colours concatenated, packed I + (n+1) J
-  int cart_off[5] = {0, 0, 0, 0, 0};
+  int cart_off[9] = {};
   int n_cart_tiles[4] = {0, 0, 0, 0};
   int* cart_tiles = nullptr;         // per colour concatenated, packed ti + 65536 tj
   int cart_tile_off[5] = {0, 0, 0, 0, 0};
   int* fused_tiles = nullptr;        // TC x TC cell tiles for the fused Cartesian sweep
   int n_fused_tiles = 0;
-  int n_cutp[4] = {0, 0, 0, 0};
-  int cutp_off[5] = {0, 0, 0, 0, 0};
+  int n_cutp[8] = {};
+  int cutp_off[9] = {};
   int* cutp_list = nullptr;          // packed I + (n+1) J
   int64_t* cutp_ent = nullptr;       // n_cutp+1 offsets into entry arrays
   int32_t* ent_node = nullptr;       // lattice index of each interior DoF
-  uint8_t* ent_loc = nullptr;        // local index in the (2p+1)^2 block
+  uint16_t* ent_loc = nullptr;       // local index in the (2p+1)^dim block
   int32_t* ent_patch = nullptr;      // owning patch of each entry
   int64_t n_ent = 0;
-  int64_t ent_col_off[5] = {0, 0, 0, 0, 0};  // host copy of cutp_ent at the colour boundaries
+  int64_t ent_col_off[9] = {};       // host copy of cutp_ent at the colour boundaries
   int64_t* cutp_inv = nullptr;       // n_cutp+1 offsets into inverse storage
   double* inv = nullptr;             // local inverses, m_j^2 each, row-major (symmetric)
   int64_t n_inv = 0;
@@ -121,8 +124,8 @@ struct LevelData {
 };
 
 struct Params {
-  double x0, y0, length, cx, cy, r, gamma_D, gamma_k[CF_MAXP];
-  int n_coarse, n_levels, p, sigma, n_q, n_c, symmetric, cut_mode;
+  double x0, y0, z0, length, cx, cy, cz, r, gamma_D, gamma_k[CF_MAXP];
+  int dim, n_coarse, n_levels, p, sigma, n_q, n_c, symmetric, cut_mode;
 };
 
 // launch accounting for the bench's gpu_launches claim

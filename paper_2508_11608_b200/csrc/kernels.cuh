@@ -267,7 +267,7 @@ __device__ void local_block_apply(const LevelArgs& L, int I, int J, const double
 // (R9); the corrections go to zbuf and are applied by phase 2.
 template <int P, int WPB>
 __global__ void __launch_bounds__(32 * WPB) k_cut_colour_p1(LevelArgs L, const int* plist, int np, int pbase,
-                                                           const int64_t* ent_off, const uint8_t* ent_loc,
+                                                           const int64_t* ent_off, const uint16_t* ent_loc,
                                                            const int32_t* ent_node, const int64_t* inv_off,
                                                            const double* inv, const double* x, const double* b,
                                                            double* zbuf) {
@@ -315,7 +315,7 @@ __global__ void k_cut_colour_p2(const int32_t* ent_node, const double* zbuf, int
 // local matrix column k of cut patch j: A_j e_k (setup, P l.156/l.193)
 template <int P, int WPB>
 __global__ void __launch_bounds__(32 * WPB) k_local_matrix(LevelArgs L, const int* plist_all, const int64_t* ent_off,
-                                                          const uint8_t* ent_loc, const int32_t* ent_patch,
+                                                          const uint16_t* ent_loc, const int32_t* ent_patch,
                                                           int64_t n_ent, const int64_t* inv_off, double* inv) {
   constexpr int BS = 2 * P + 1, WS = 4 * P + 1;
   __shared__ SmTab T;

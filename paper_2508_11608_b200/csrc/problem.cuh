@@ -18,6 +18,7 @@
 #include "internal.cuh"
 #include "kernels.cuh"
 #include "smoother2.cuh"
+#include "dim3.cuh"
 #include "tables.cuh"
 
 namespace cf {
@@ -31,6 +32,13 @@ int64_t g_launches = 0;
     case 3: { constexpr int P = 3; __VA_ARGS__; } break;  \
     case 4: { constexpr int P = 4; __VA_ARGS__; } break;  \
     default: throw Error(ERR_ARG, "degree must be 1..4"); \
+  }
+
+#define CF_DISPATCH3(p, ...)                              \
+  switch (p) {                                            \
+    case 1: { constexpr int P = 1; __VA_ARGS__; } break;  \
+    case 2: { constexpr int P = 2; __VA_ARGS__; } break;  \
+    default: throw Error(ERR_ARG, "3D supports degree 1..2"); \
   }
 
 template <int P> constexpr int cart_tp() { return P == 1 ? 16 : (P == 2 ? 8 : (P == 3 ? 7 : 6)); }
@@ -156,6 +164,10 @@ struct Problem {
 
   // ---------------------------------------------------------------- setup
   void setup_mesh() {
+    if (prm.dim == 3) {
+      setup_mesh3();
+      return;
+    }
     host::upload_tables();
     if (const char* e = std::getenv("CUTFEM_PERSISTENT")) persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_FUSED")) fused = std::atoi(e) != 0;
@@ -302,6 +314,10 @@ struct Problem {
   }
 
   void build_patches() {
+    if (prm.dim == 3) {
+      build_patches3();
+      return;
+    }
     const int p = prm.p;
     for (int l = 0; l < prm.n_levels; ++l) {
       LevelData& D = lv[l];
@@ -392,7 +408,7 @@ struct Problem {
       }
       sync();
       D.ent_node = alloc<int32_t>(D.n_ent);
-      D.ent_loc = alloc<uint8_t>(D.n_ent);
+      D.ent_loc = alloc<uint16_t>(D.n_ent);
       D.ent_patch = alloc<int32_t>(D.n_ent);
       D.zbuf = alloc<double>(D.n_ent);
       if (ncp) {
@@ -434,8 +450,7 @@ struct Problem {
     }
     build_coarse();
     // CG workspace on the finest level
-    const LevelArgs& F = lv.back().a;
-    const int64_t nvf = (int64_t)F.nl * F.ld;
+    const int64_t nvf = vsize(prm.n_levels - 1);
     cg_x = alloc<double>(nvf);
     cg_r = alloc<double>(nvf);
     cg_z = alloc<double>(nvf);
@@ -494,8 +509,7 @@ struct Problem {
 
   void build_coarse() {
     LevelData& D = lv[0];
-    const LevelArgs& L = D.a;
-    const int64_t nv = (int64_t)L.nl * L.ld;
+    const int64_t nv = vsize(0);
     int* nodes = alloc<int>(nv);
     n0 = select(D.mask, (int)nv, nodes);
     require(n0 <= 160, ERR_SIZE, "coarse level has more than 160 DoFs; use a coarser level 0");
@@ -528,6 +542,10 @@ struct Problem {
 
   // ------------------------------------------------------------- hot path
   void apply(int l, const double* x, double* y, const double* b) {
+    if (prm.dim == 3) {
+      apply3(l, x, y, b);
+      return;
+    }
     const LevelArgs& L = lv[l].a;
     const int p = prm.p;
     const int warps = L.n_cut + ceil_div(L.n_ghost, 32);
@@ -738,6 +756,10 @@ struct Problem {
 
   // x <- S(x, b) (P eq. smoother-split, l.196-210; reverse = adjoint order, R9)
   void smooth(int l, double* x, const double* b, int reverse) {
+    if (prm.dim == 3) {
+      smooth3(l, x, b, reverse);
+      return;
+    }
     if (pingpong && fused) {
       if (!reverse) cart_fused(l, x, b, 0);
       cut_sweeps(l, x, b, reverse);
@@ -768,11 +790,23 @@ struct Problem {
 
   void restrict_(int l, const double* rf, double* bc) {
     const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
+    if (prm.dim == 3) {
+      const int64_t nv = (int64_t)Lc.nl * Lc.nl * Lc.ld;
+      CF_DISPATCH3(prm.p, (k_restrict3<P><<<ceil_div(nv, 128), 128, 0, st>>>(Lf, Lc, rf, bc)));
+      CF_LAUNCHED();
+      return;
+    }
     CF_DISPATCH(prm.p, (k_restrict<P><<<dim3(ceil_div(Lc.ld, 32), ceil_div(Lc.nl, 8)), dim3(32, 8), 0, st>>>(Lf, Lc, rf, bc)));
     CF_LAUNCHED();
   }
   void prolongate_add(int l, const double* xc, double* xf) {
     const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
+    if (prm.dim == 3) {
+      const int64_t nv = (int64_t)Lf.nl * Lf.nl * Lf.ld;
+      CF_DISPATCH3(prm.p, (k_prolongate_add3<P><<<ceil_div(nv, 128), 128, 0, st>>>(Lf, Lc, xc, xf)));
+      CF_LAUNCHED();
+      return;
+    }
     CF_DISPATCH(prm.p, (k_prolongate_add<P><<<dim3(ceil_div(Lf.nl, 32), ceil_div(Lf.nl, 8)), dim3(32, 8), 0, st>>>(Lf, Lc, xc, xf)));
     CF_LAUNCHED();
   }
@@ -792,7 +826,7 @@ struct Problem {
     smooth(l, x, b, 0);
     apply(l, x, D.r, b);
     restrict_(l, D.r, C.b);
-    CF_CUDA(cudaMemsetAsync(C.x, 0, (size_t)C.a.nl * C.a.ld * 8, st));
+    CF_CUDA(cudaMemsetAsync(C.x, 0, vsize(l - 1) * 8, st));
     vcycle(l - 1, C.x, C.b);
     prolongate_add(l, C.x, x);
     smooth(l, x, b, prm.symmetric ? 1 : 0);
@@ -832,19 +866,305 @@ struct Problem {
     g_launches += it->second.launches;
   }
 
+  // doubles in a lattice vector of level l
+  int64_t vsize(int l) const {
+    const LevelArgs& L = lv[l].a;
+    return (int64_t)L.nl * L.ld * (prm.dim == 3 ? L.nl : 1);
+  }
+
   void dot(const double* a, const double* b, int mode, int slot) {
-    const LevelArgs& F = lv.back().a;
-    k_dot_partial<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(a, b, (int64_t)F.nl * F.ld, part);
+    k_dot_partial<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(a, b, vsize(prm.n_levels - 1), part);
     CF_LAUNCHED();
     k_dot_final<<<1, DOT_THREADS, 0, st>>>(part, sc, mode, slot);
     CF_LAUNCHED();
+  }
+
+  // ================================================================ 3D
+  void setup_mesh3() {
+    host::upload_tables();
+    host::cart_map3(prm.p);
+    d_count = alloc<int>(1);
+    const int p = prm.p;
+    lv.resize(prm.n_levels);
+    for (int l = 0; l < prm.n_levels; ++l) {
+      LevelData& D = lv[l];
+      LevelArgs& L = D.a;
+      std::memset(&L, 0, sizeof(L));
+      L.dim = 3;
+      L.n = prm.n_coarse << l;
+      L.p = p;
+      L.nl = L.n * p + 1;
+      L.ld = (L.nl + 1) & ~1;
+      L.h = prm.length / L.n;
+      L.x0 = prm.x0;
+      L.y0 = prm.y0;
+      L.z0 = prm.z0;
+      L.cx = prm.cx;
+      L.cy = prm.cy;
+      L.cz = prm.cz;
+      L.r = prm.r;
+      L.gDh = prm.gamma_D / L.h;
+      for (int k = 1; k <= p; ++k) {
+        double f = 1.0;
+        for (int q = 2; q <= k; ++q) f *= q;
+        L.gs[k] = prm.gamma_k[k - 1] * std::pow(L.h, prm.sigma + 2) / (f * f);
+      }
+      const int n = L.n;
+      const int64_t n3 = (int64_t)n * n * n, nv = vsize(l);
+      D.ctype = alloc<int8_t>(n3);
+      k_classify3<<<ceil_div(n3, 256), 256, 0, st>>>(L, D.ctype);
+      CF_LAUNCHED();
+      L.ctype = D.ctype;
+      D.mask = alloc<uint8_t>(nv);
+      CF_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int), st));
+      k_mask3<<<ceil_div(nv, 256), 256, 0, st>>>(L, D.ctype, D.mask, d_count);
+      CF_LAUNCHED();
+      L.mask = D.mask;
+      D.n_dofs = read_count();
+      if (l > 0) {
+        CF_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int), st));
+        k_parent_check3<<<ceil_div(n3, 256), 256, 0, st>>>(L, lv[l - 1].a, d_count);
+        CF_LAUNCHED();
+        require(read_count() == 0, ERR_GEOMETRY, "a fine active cell has an inactive parent");
+      }
+      uint8_t* flags = alloc<uint8_t>(3 * n3);
+      int* tmpi = alloc<int>(3 * n3);
+      k_cell_flags<<<ceil_div(n3, 256), 256, 0, st>>>(n3, D.ctype, INSIDE, flags);
+      CF_LAUNCHED();
+      D.n_inside = select(flags, (int)n3, tmpi);
+      k_cell_flags<<<ceil_div(n3, 256), 256, 0, st>>>(n3, D.ctype, CUT, flags);
+      CF_LAUNCHED();
+      L.n_cut = select(flags, (int)n3, tmpi);
+      D.cut_list = alloc<int>(L.n_cut);
+      CF_CUDA(cudaMemcpyAsync(D.cut_list, tmpi, sizeof(int) * L.n_cut, cudaMemcpyDeviceToDevice, st));
+      L.cut_list = D.cut_list;
+      D.cut_id = alloc<int>(n3);
+      k_fill<<<ceil_div(n3, 256), 256, 0, st>>>(D.cut_id, n3, -1);
+      CF_LAUNCHED();
+      if (L.n_cut) {
+        k_scatter_id<<<ceil_div(L.n_cut, 256), 256, 0, st>>>(D.cut_list, L.n_cut, D.cut_id);
+        CF_LAUNCHED();
+      }
+      L.cut_id = D.cut_id;
+      k_ghost_flags3<<<ceil_div(3 * n3, 256), 256, 0, st>>>(L, flags);
+      CF_LAUNCHED();
+      L.n_ghost = select(flags, (int)(3 * n3), tmpi);
+      D.ghost_list = alloc<int>(L.n_ghost);
+      CF_CUDA(cudaMemcpyAsync(D.ghost_list, tmpi, sizeof(int) * L.n_ghost, cudaMemcpyDeviceToDevice, st));
+      L.ghost_list = D.ghost_list;
+      D.gx_id = alloc<int>(n3);
+      D.gy_id = alloc<int>(n3);
+      D.gz_id = alloc<int>(n3);
+      for (int* m : {D.gx_id, D.gy_id, D.gz_id}) {
+        k_fill<<<ceil_div(n3, 256), 256, 0, st>>>(m, n3, -1);
+        CF_LAUNCHED();
+      }
+      if (L.n_ghost) {
+        k_ghost_maps3<<<ceil_div(L.n_ghost, 256), 256, 0, st>>>(D.ghost_list, L.n_ghost, n, D.gx_id, D.gy_id, D.gz_id);
+        CF_LAUNCHED();
+      }
+      L.gx_id = D.gx_id;
+      L.gy_id = D.gy_id;
+      L.gz_id = D.gz_id;
+      D.q_off = alloc<int>(L.n_cut + 1);
+      D.s_off = alloc<int>(L.n_cut + 1);
+      int* vc = tmpi;
+      int* scn = tmpi + n3;
+      if (L.n_cut) {
+        k_cut_count3<<<ceil_div(L.n_cut, 64), 64, 0, st>>>(L, prm.n_q, vc, scn);
+        CF_LAUNCHED();
+      }
+      D.n_vq = scan32(vc, L.n_cut, D.q_off);
+      D.n_sq = scan32(scn, L.n_cut, D.s_off);
+      L.q_off = D.q_off;
+      L.s_off = D.s_off;
+      D.qbuf = alloc<double>(4 * D.n_vq);
+      D.sbuf = alloc<double>(7 * D.n_sq);
+      QPtrs3 QP;
+      for (int d = 0; d < 4; ++d) QP.q[d] = D.qbuf + d * D.n_vq;
+      for (int d = 0; d < 7; ++d) QP.s[d] = D.sbuf + d * D.n_sq;
+      L.qx = QP.q[0]; L.qy = QP.q[1]; L.qz = QP.q[2]; L.qw = QP.q[3];
+      L.sx = QP.s[0]; L.sy = QP.s[1]; L.sz = QP.s[2]; L.sw = QP.s[3];
+      L.snx = QP.s[4]; L.sny = QP.s[5]; L.snz = QP.s[6];
+      if (L.n_cut) {
+        k_cut_fill3<<<ceil_div(L.n_cut, 64), 64, 0, st>>>(L, prm.n_q, QP);
+        CF_LAUNCHED();
+      }
+      const int NB = (p + 1) * (p + 1) * (p + 1);
+      D.ecut = alloc<double>((int64_t)L.n_cut * NB * NB);
+      L.ecut = D.ecut;
+      if (L.n_cut) {
+        CF_DISPATCH3(p, (k_cut_elem3<P><<<ceil_div((int64_t)L.n_cut * NB, 4), 128, 0, st>>>(L, D.ecut)));
+        CF_LAUNCHED();
+      }
+      D.ycut = alloc<double>((int64_t)L.n_cut * NB);
+      D.jm = alloc<double>((int64_t)L.n_ghost * p * (p + 1) * (p + 1));
+      L.ycut = D.ycut;
+      L.jm = D.jm;
+      D.x = alloc<double>(nv);
+      D.b = alloc<double>(nv);
+      D.r = alloc<double>(nv);
+      for (double* v : {D.x, D.b, D.r}) CF_CUDA(cudaMemsetAsync(v, 0, nv * 8, st));
+      sync();
+      cudaFree(flags);
+      cudaFree(tmpi);
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), (void*)flags), allocs.end());
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), (void*)tmpi), allocs.end());
+    }
+  }
+
+  void build_patches3() {
+    const int p = prm.p;
+    for (int l = 0; l < prm.n_levels; ++l) {
+      LevelData& D = lv[l];
+      LevelArgs& L = D.a;
+      const int n = L.n;
+      const int64_t nvt = (int64_t)(n + 1) * (n + 1) * (n + 1);
+      D.vkind = alloc<uint8_t>(nvt);
+      k_vertex_kind3<<<ceil_div(nvt, 256), 256, 0, st>>>(L, D.vkind);
+      CF_LAUNCHED();
+      uint8_t* fl = alloc<uint8_t>(nvt);
+      int* tmpi = alloc<int>(nvt);
+      for (int kind = V_CART; kind <= V_CUT; ++kind) {
+        int* off = kind == V_CART ? D.cart_off : D.cutp_off;
+        int* cnt = kind == V_CART ? D.n_cart : D.n_cutp;
+        off[0] = 0;
+        std::vector<int> hostlists;
+        for (int c = 0; c < 8; ++c) {
+          k_vertex_flags3<<<ceil_div(nvt, 256), 256, 0, st>>>(n, D.vkind, (uint8_t)kind, c, fl);
+          CF_LAUNCHED();
+          cnt[c] = select(fl, (int)nvt, tmpi);
+          std::vector<int> h(cnt[c]);
+          if (cnt[c]) CF_CUDA(cudaMemcpyAsync(h.data(), tmpi, sizeof(int) * cnt[c], cudaMemcpyDeviceToHost, st));
+          sync();
+          hostlists.insert(hostlists.end(), h.begin(), h.end());
+          off[c + 1] = off[c] + cnt[c];
+        }
+        int* dl = alloc<int>(hostlists.size());
+        if (!hostlists.empty())
+          CF_CUDA(cudaMemcpyAsync(dl, hostlists.data(), sizeof(int) * hostlists.size(), cudaMemcpyHostToDevice, st));
+        (kind == V_CART ? D.cart_list : D.cutp_list) = dl;
+      }
+      const int ncp = D.cutp_off[8];
+      int* mcount = alloc<int>(ncp);
+      D.cutp_ent = alloc<int64_t>(ncp + 1);
+      if (ncp) {
+        k_cut_interior3<false><<<ceil_div(ncp, 64), 64, 0, st>>>(L, D.cutp_list, ncp, mcount, nullptr, nullptr,
+                                                                  nullptr, nullptr);
+        CF_LAUNCHED();
+      }
+      D.n_ent = scan64(mcount, ncp, D.cutp_ent);
+      for (int c = 0; c <= 8; ++c) {
+        D.ent_col_off[c] = 0;
+        if (ncp) CF_CUDA(cudaMemcpyAsync(&D.ent_col_off[c], D.cutp_ent + D.cutp_off[c], sizeof(int64_t),
+                                         cudaMemcpyDeviceToHost, st));
+      }
+      sync();
+      D.ent_node = alloc<int32_t>(D.n_ent);
+      D.ent_loc = alloc<uint16_t>(D.n_ent);
+      D.ent_patch = alloc<int32_t>(D.n_ent);
+      D.zbuf = alloc<double>(D.n_ent);
+      if (ncp) {
+        k_cut_interior3<true><<<ceil_div(ncp, 64), 64, 0, st>>>(L, D.cutp_list, ncp, nullptr, D.cutp_ent, D.ent_node,
+                                                                 D.ent_loc, D.ent_patch);
+        CF_LAUNCHED();
+      }
+      int* msq = alloc<int>(ncp);
+      D.cutp_inv = alloc<int64_t>(ncp + 1);
+      int mmax = 0;
+      if (ncp) {
+        k_square<<<ceil_div(ncp, 128), 128, 0, st>>>(mcount, ncp, msq);
+        CF_LAUNCHED();
+        std::vector<int> hm(ncp);
+        CF_CUDA(cudaMemcpyAsync(hm.data(), mcount, sizeof(int) * ncp, cudaMemcpyDeviceToHost, st));
+        sync();
+        for (int v : hm) mmax = std::max(mmax, v);
+      }
+      D.n_inv = scan64(msq, ncp, D.cutp_inv);
+      D.inv = alloc<double>(D.n_inv);
+      if (D.n_ent) {
+        CF_DISPATCH3(p, (k_local_matrix3<P><<<ceil_div(D.n_ent, 2), 64, 0, st>>>(
+                            L, D.cutp_list, D.cutp_ent, D.ent_loc, D.ent_patch, D.n_ent, D.cutp_inv, D.inv,
+                            prm.cut_mode)));
+        CF_LAUNCHED();
+        const size_t smb = (size_t)(mmax * mmax + 2 * mmax) * sizeof(double);
+        require(smb <= 200 * 1024, ERR_SIZE, "cut patch too large for the batched inverse");
+        CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smb, 48 * 1024)));
+        k_batched_inverse<<<ncp, 256, smb, st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp);
+        CF_LAUNCHED();
+      }
+      sync();
+    }
+    build_coarse();
+    const int64_t nvf = vsize(prm.n_levels - 1);
+    cg_x = alloc<double>(nvf);
+    cg_r = alloc<double>(nvf);
+    cg_z = alloc<double>(nvf);
+    cg_p = alloc<double>(nvf);
+    cg_q = alloc<double>(nvf);
+    part = alloc<double>(DOT_BLOCKS);
+    sc = alloc<double>(8);
+    if (!sc_host) CF_CUDA(cudaMallocHost(&sc_host, 8 * sizeof(double)));
+    for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
+    sync();
+    built = true;
+  }
+
+  void apply3(int l, const double* x, double* y, const double* b) {
+    const LevelArgs& L = lv[l].a;
+    const int warps = L.n_cut + ceil_div(L.n_ghost, 32);
+    if (warps) {
+      CF_DISPATCH3(prm.p, (k_band3<P><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+      CF_LAUNCHED();
+    }
+    CF_DISPATCH3(prm.p, (k_node_apply3<P><<<ceil_div(vsize(l), 256), 256, 0, st>>>(L, x, b, y)));
+    CF_LAUNCHED();
+  }
+
+  void cart_step3(int l, int c, double* x, const double* b) {
+    LevelData& D = lv[l];
+    const int np = D.n_cart[c];
+    if (!np) return;
+    CF_DISPATCH3(prm.p, (launch(k_cart_colour3<P>, dim3(ceil_div(ceil_div(np, 8), 4)), dim3(128), 0, D.a,
+                                (const int*)(D.cart_list + D.cart_off[c]), np, host::cart_map3(P), x, b)));
+    CF_LAUNCHED();
+  }
+
+  void cut_step3(int l, int c, double* x, const double* b) {
+    LevelData& D = lv[l];
+    const int np = D.n_cutp[c];
+    if (!np) return;
+    const int base = D.cutp_off[c];
+    CF_DISPATCH3(prm.p, (launch(k_cut_colour3<P>, dim3(ceil_div(np, 2)), dim3(64), 0, D.a,
+                                (const int*)(D.cutp_list + base), np, base, (const int64_t*)D.cutp_ent,
+                                (const uint16_t*)D.ent_loc, (const int32_t*)D.ent_node, (const int64_t*)D.cutp_inv,
+                                (const double*)D.inv, (const double*)x, b, D.zbuf, prm.cut_mode)));
+    CF_LAUNCHED();
+    const int64_t e0 = D.ent_col_off[c], e1 = D.ent_col_off[c + 1];
+    if (e1 <= e0) return;
+    launch(k_cut_apply, dim3(ceil_div(e1 - e0, 256)), dim3(256), 0, (const int32_t*)D.ent_node, (const double*)D.zbuf,
+           e0, e1, x);
+    CF_LAUNCHED();
+  }
+
+  void smooth3(int l, double* x, const double* b, int reverse) {
+    std::vector<std::pair<int, int>> seq;
+    for (int c = 0; c < 8; ++c) seq.push_back({0, c});
+    for (int rep = 0; rep < prm.n_c; ++rep)
+      for (int c = 0; c < 8; ++c) seq.push_back({1, c});
+    if (reverse) std::reverse(seq.begin(), seq.end());
+    for (auto& q : seq) {
+      if (q.first == 0) cart_step3(l, q.second, x, b);
+      else cut_step3(l, q.second, x, b);
+    }
   }
 
   // CG preconditioned by one V-cycle (zero initial guess); x_0 = 0
   void solve_cg(double* x, const double* b, double tol, int max_it, int* iters, double* rel) {
     const int Lf = prm.n_levels - 1;
     LevelData& F = lv[Lf];
-    const int64_t nv = (int64_t)F.a.nl * F.a.ld;
+    const int64_t nv = vsize(Lf);
     const int grid = 4 * 148;
     k_masked_copy<<<grid, 256, 0, st>>>(cg_r, b, F.mask, nv);
     CF_LAUNCHED();

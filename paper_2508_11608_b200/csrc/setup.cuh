@@ -271,7 +271,7 @@ __global__ void k_pack_tiles(const int* sel, int nsel, int tx, int* out) {
 // lies in the patch (P l.153, reading R3).  WRITE = false counts.
 template <bool WRITE>
 __global__ void k_cut_interior(LevelArgs L, const int8_t* ct, const int* plist, int np, int* count,
-                               const int64_t* off, int32_t* node, uint8_t* loc, int32_t* owner) {
+                               const int64_t* off, int32_t* node, uint16_t* loc, int32_t* owner) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= np) return;
   int n = L.n, p = L.p;
@@ -292,7 +292,7 @@ __global__ void k_cut_interior(LevelArgs L, const int8_t* ct, const int* plist, 
       if (!inside) continue;
       if (WRITE) {
         node[o + m] = b * L.ld + a;
-        loc[o + m] = (uint8_t)(db * (2 * p + 1) + da);
+        loc[o + m] = (uint16_t)(db * (2 * p + 1) + da);
         owner[o + m] = k;
       }
       ++m;

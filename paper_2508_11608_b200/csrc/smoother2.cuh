@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(128) k_cut_elem(LevelArgs L, double* E) {
 
 // ---- setup: descriptors of the cut patches (all colours, list order)
 template <int P>
-__global__ void k_cut_desc(LevelArgs L, const int* plist, int np, const int64_t* ent_off, const uint8_t* ent_loc,
+__global__ void k_cut_desc(LevelArgs L, const int* plist, int np, const int64_t* ent_off, const uint16_t* ent_loc,
                            const int64_t* inv_off, CutDesc* desc) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= np) return;

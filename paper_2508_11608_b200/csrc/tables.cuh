@@ -320,3 +320,82 @@ inline const double* cart_map(int p) {
 }
 }  // namespace host
 }  // namespace cf
+
+namespace cf {
+namespace host {
+// 3D dense patch map for h = 1 (A scales with h in 3D; the kernel divides
+// the b operands by h): rows = interior nodes (ic, ib, ia), columns =
+// [b_int | x_ext]
+inline std::vector<double> cart_affine_map3(int p, const Tab& t, int& cols_pad) {
+  const int NE = 2 * p + 1, NI = 2 * p - 1, NINT = NI * NI * NI, NEXT = NE * NE * NE, K = NINT + NEXT;
+  cols_pad = 4 * ((K + 3) / 4);
+  const int rows_pad = 8 * ((NINT + 7) / 8);
+  std::vector<double> Aext((size_t)NINT * NEXT), Ai((size_t)NINT * NINT);
+  for (int r = 0; r < NINT; ++r) {
+    const int a = r % NI + 1, b = (r / NI) % NI + 1, c = r / (NI * NI) + 1;
+    for (int q = 0; q < NEXT; ++q) {
+      const int aa = q % NE, bb = (q / NE) % NE, cc = q / (NE * NE);
+      Aext[(size_t)r * NEXT + q] = t.Kp[a][aa] * t.Mp[b][bb] * t.Mp[c][cc] + t.Mp[a][aa] * t.Kp[b][bb] * t.Mp[c][cc] +
+                                   t.Mp[a][aa] * t.Mp[b][bb] * t.Kp[c][cc];
+    }
+  }
+  for (int r = 0; r < NINT; ++r)
+    for (int q = 0; q < NINT; ++q) {
+      const int a = q % NI + 1, b = (q / NI) % NI + 1, c = q / (NI * NI) + 1;
+      Ai[(size_t)r * NINT + q] = Aext[(size_t)r * NEXT + (c * NE + b) * NE + a];
+    }
+  std::vector<double> inv((size_t)NINT * NINT, 0.0);
+  for (int i = 0; i < NINT; ++i) inv[(size_t)i * NINT + i] = 1.0;
+  for (int c = 0; c < NINT; ++c) {
+    int pr = c;
+    for (int r = c + 1; r < NINT; ++r)
+      if (std::fabs(Ai[(size_t)r * NINT + c]) > std::fabs(Ai[(size_t)pr * NINT + c])) pr = r;
+    for (int q = 0; q < NINT; ++q) {
+      std::swap(Ai[(size_t)c * NINT + q], Ai[(size_t)pr * NINT + q]);
+      std::swap(inv[(size_t)c * NINT + q], inv[(size_t)pr * NINT + q]);
+    }
+    const double piv = Ai[(size_t)c * NINT + c];
+    for (int q = 0; q < NINT; ++q) {
+      Ai[(size_t)c * NINT + q] /= piv;
+      inv[(size_t)c * NINT + q] /= piv;
+    }
+    for (int r = 0; r < NINT; ++r) {
+      if (r == c) continue;
+      const double f = Ai[(size_t)r * NINT + c];
+      if (f == 0.0) continue;
+      for (int q = 0; q < NINT; ++q) {
+        Ai[(size_t)r * NINT + q] -= f * Ai[(size_t)c * NINT + q];
+        inv[(size_t)r * NINT + q] -= f * inv[(size_t)c * NINT + q];
+      }
+    }
+  }
+  std::vector<double> G((size_t)rows_pad * cols_pad, 0.0);
+  for (int r = 0; r < NINT; ++r) {
+    for (int q = 0; q < NINT; ++q) G[(size_t)r * cols_pad + q] = inv[(size_t)r * NINT + q];
+    const int a = r % NI + 1, b = (r / NI) % NI + 1, c = r / (NI * NI) + 1;
+    for (int qe = 0; qe < NEXT; ++qe) {
+      double s = 0.0;
+      for (int q = 0; q < NINT; ++q) s += inv[(size_t)r * NINT + q] * Aext[(size_t)q * NEXT + qe];
+      G[(size_t)r * cols_pad + NINT + qe] = (qe == (c * NE + b) * NE + a ? 1.0 : 0.0) - s;
+    }
+  }
+  return G;
+}
+
+inline const double* cart_map3(int p) {
+  static const double* maps[3] = {nullptr};
+  if (p < 1 || p > 2) return nullptr;
+  if (!maps[p]) {
+    Tab t;
+    build_tab(p, t);
+    int cp = 0;
+    std::vector<double> G = cart_affine_map3(p, t, cp);
+    void* d = nullptr;
+    CF_CUDA(cudaMalloc(&d, G.size() * sizeof(double)));
+    CF_CUDA(cudaMemcpy(d, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice));
+    maps[p] = (const double*)d;
+  }
+  return maps[p];
+}
+}  // namespace host
+}  // namespace cf

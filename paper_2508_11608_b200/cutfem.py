@@ -35,13 +35,14 @@ class Params(ctypes.Structure):
                 ("cx", ctypes.c_double), ("cy", ctypes.c_double), ("r", ctypes.c_double),
                 ("gamma_D", ctypes.c_double), ("gamma_k", ctypes.c_double * 4), ("sigma", ctypes.c_int),
                 ("n_q", ctypes.c_int), ("n_c", ctypes.c_int), ("symmetric", ctypes.c_int),
-                ("cut_mode", ctypes.c_int)]
+                ("cut_mode", ctypes.c_int), ("dim", ctypes.c_int), ("z0", ctypes.c_double),
+                ("cz", ctypes.c_double)]
 
 
 class LevelInfo(ctypes.Structure):
-    _fields_ = [("n", ctypes.c_int), ("nl", ctypes.c_int), ("ld", ctypes.c_int), ("n_dofs", ctypes.c_int64),
+    _fields_ = [("dim", ctypes.c_int), ("n", ctypes.c_int), ("nl", ctypes.c_int), ("ld", ctypes.c_int), ("n_dofs", ctypes.c_int64),
                 ("n_inside", ctypes.c_int), ("n_cut", ctypes.c_int), ("n_ghost_faces", ctypes.c_int),
-                ("n_cart", ctypes.c_int * 4), ("n_cutp", ctypes.c_int * 4), ("n_vol_qp", ctypes.c_int64),
+                ("n_cart", ctypes.c_int * 8), ("n_cutp", ctypes.c_int * 8), ("n_vol_qp", ctypes.c_int64),
                 ("n_surf_qp", ctypes.c_int64), ("h", ctypes.c_double)]
 
 
@@ -104,10 +105,10 @@ def launch_count():
 
 
 def make_params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D=0.0, gamma_k=(-1, -1, -1, -1),
-                sigma=-1, n_q=0, n_c=2, symmetric=1, cut_mode=0):
+                sigma=-1, n_q=0, n_c=2, symmetric=1, cut_mode=0, dim=2, z0=0.0, cz=0.0):
     g = (ctypes.c_double * 4)(*[float(v) for v in (list(gamma_k) + [-1] * 4)[:4]])
     return Params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D, g, sigma, n_q, n_c, symmetric,
-                  cut_mode)
+                  cut_mode, dim, z0, cz)
 
 
 class Problem:
@@ -123,7 +124,8 @@ class Problem:
 
     @classmethod
     def from_workload(cls, w, stream=None, **kw):
-        prm = make_params(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, w.p, w.cx, w.cy, w.r, n_c=w.n_c, **kw)
+        prm = make_params(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, w.p, w.cx, w.cy, w.r, n_c=w.n_c,
+                          dim=getattr(w, "dim", 2), z0=getattr(w, "z0", 0.0), cz=getattr(w, "cz", 0.0), **kw)
         return cls(prm, stream)
 
     def build_patches(self, stream=None):
@@ -151,23 +153,27 @@ class Problem:
         i = self.level_info(level)
         return i.nl, i.ld
 
+    def _rows(self, level):
+        i = self.level_info(level)
+        return i.nl ** (i.dim - 1), i.nl, i.ld
+
     def zeros(self, level=-1):
         import torch
-        nl, ld = self.lattice_shape(level)
-        return torch.zeros(nl * ld, dtype=torch.float64, device="cuda")
+        rows, nl, ld = self._rows(level)
+        return torch.zeros(rows * ld, dtype=torch.float64, device="cuda")
 
     def to_device(self, lattice_np, level=-1):
-        """(NL*NL,) numpy lattice vector (b*NL + a) -> padded device vector."""
+        """(NL^dim,) numpy lattice vector (x fastest) -> padded device vector."""
         import torch
-        nl, ld = self.lattice_shape(level)
-        a = np.zeros((nl, ld))
-        a[:, :nl] = np.asarray(lattice_np, dtype=np.float64).reshape(nl, nl)
+        rows, nl, ld = self._rows(level)
+        a = np.zeros((rows, ld))
+        a[:, :nl] = np.asarray(lattice_np, dtype=np.float64).reshape(rows, nl)
         return torch.from_numpy(a.ravel()).cuda()
 
     def to_host(self, t, level=-1):
-        """padded device vector -> (NL*NL,) numpy lattice vector."""
-        nl, ld = self.lattice_shape(level)
-        return t.detach().cpu().numpy().reshape(nl, ld)[:, :nl].ravel().copy()
+        """padded device vector -> (NL^dim,) numpy lattice vector."""
+        rows, nl, ld = self._rows(level)
+        return t.detach().cpu().numpy().reshape(rows, ld)[:, :nl].ravel().copy()
 
     # --- hot path (names of the C ABI)
     def apply_operator(self, level, x, y, stream=None):
@@ -211,15 +217,15 @@ class Problem:
     # --- exports (host)
     def cell_types(self, level=-1):
         i = self.level_info(level)
-        out = np.zeros(i.n * i.n, dtype=np.int8)
+        out = np.zeros(i.n ** i.dim, dtype=np.int8)
         _check(_lib.cutfem_export_cell_types(self._h, level % self.n_levels, out.ctypes.data_as(_D)))
-        return out.reshape(i.n, i.n)
+        return out.reshape((i.n,) * i.dim)
 
     def dof_mask(self, level=-1):
         i = self.level_info(level)
-        out = np.zeros(i.nl * i.nl, dtype=np.uint8)
+        out = np.zeros(i.nl ** i.dim, dtype=np.uint8)
         _check(_lib.cutfem_export_dof_mask(self._h, level % self.n_levels, out.ctypes.data_as(_D)))
-        return out.reshape(i.nl, i.nl).astype(bool)
+        return out.reshape((i.nl,) * i.dim).astype(bool)
 
     def patches(self, level, kind, colour):
         level = level % self.n_levels

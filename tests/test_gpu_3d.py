@@ -1,0 +1,109 @@
+"""CUDA 3D (sphere) path vs the 3D oracle through the C ABI: structure
+bit-exact, operator / colour steps / smoothing steps / transfer to 1e-10,
+V-cycle to 1e-9, identical CG iteration counts."""
+import functools
+
+import numpy as np
+import pytest
+
+import workloads
+from gpu_util import KIND, rel_err
+from oracle.solver import from_workload
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+CASES = [
+    workloads.sphere("sphere-Q1-16", 2, 4, 1),
+    workloads.sphere("sphere-Q2-8", 2, 3, 2),
+    workloads.sphere("offc-Q2-8", 2, 3, 2, x0=-0.5, length=1.0, c=(0.0137, -0.0211, 0.0093), r=0.3071),
+]
+IDS = [w.name for w in CASES]
+
+
+@functools.lru_cache(maxsize=4)
+def oracle(w):
+    return from_workload(w)
+
+
+def gpu(w, **kw):
+    from paper_2508_11608_b200 import cutfem
+    return cutfem.Problem.from_workload(w, **kw)
+
+
+def rnd(w, seed, level):
+    return workloads.lattice_vector(w, seed, level)
+
+
+@pytest.mark.parametrize("w", CASES, ids=IDS)
+def test_structure_3d(w):
+    o, g = oracle(w), gpu(w)
+    for l, ld in enumerate(o.levels):
+        lv = ld.lv
+        assert np.array_equal(g.cell_types(l), lv.cell_type)
+        assert np.array_equal(g.dof_mask(l), lv.dof_mask)
+        n1 = lv.n + 1
+        for kind in (0, 1):
+            for c in range(8):
+                ref = [(pt.K * n1 + pt.J) * n1 + pt.I for pt in ld.patches if pt.kind == KIND[kind] and pt.colour == c]
+                assert np.array_equal(g.patches(l, kind, c), np.array(ref, dtype=np.int32)), (l, kind, c)
+        off, nodes = g.cut_interior(l)
+        ref = [lv.dof_nodes[pt.interior] for c in range(8) for pt in ld.patches if pt.kind == KIND[1] and pt.colour == c]
+        for k, r in enumerate(ref):
+            assert np.array_equal(nodes[off[k]:off[k + 1]], r)
+
+
+@pytest.mark.parametrize("w", CASES, ids=IDS)
+def test_operator_3d(w):
+    o, g = oracle(w), gpu(w)
+    for l, ld in enumerate(o.levels):
+        xl = rnd(w, 30 + l, l)
+        y = g.zeros(l)
+        g.apply_operator(l, g.to_device(xl, l), y)
+        assert rel_err(g.to_host(y, l)[ld.lv.dof_nodes], ld.A @ xl[ld.lv.dof_nodes]) < TOL, l
+
+
+@pytest.mark.parametrize("w", CASES, ids=IDS)
+def test_colour_steps_and_smoother_3d(w):
+    o, g = oracle(w), gpu(w)
+    l = len(o.levels) - 1
+    ld = o.levels[l]
+    dn = ld.lv.dof_nodes
+    xl, bl = rnd(w, 40, l), rnd(w, 41, l)
+    for kind in (0, 1):
+        for c in range(8):
+            x = g.to_device(xl, l)
+            g.colour_step(l, kind, c, x, g.to_device(bl, l))
+            xo = xl[dn].copy()
+            ld.colour_step(xo, bl[dn], KIND[kind], c)
+            assert rel_err(g.to_host(x, l)[dn], xo) < TOL, (kind, c)
+    for rev in (False, True):
+        x = g.to_device(xl, l)
+        g.smooth(l, x, g.to_device(bl, l), rev)
+        xo = xl[dn].copy()
+        ld.smooth(xo, bl[dn], w.n_c, reverse=rev)
+        assert rel_err(g.to_host(x, l)[dn], xo) < TOL
+
+
+@pytest.mark.parametrize("w", CASES, ids=IDS)
+def test_transfer_vcycle_cg_3d(w):
+    o, g = oracle(w), gpu(w)
+    for l in range(1, len(o.levels)):
+        c, f = o.levels[l - 1].lv, o.levels[l].lv
+        xc, xf = rnd(w, 50, l - 1), rnd(w, 51, l) * f.dof_mask.ravel()
+        d = g.to_device(xf, l)
+        g.prolongate_add(l, g.to_device(xc, l - 1), d)
+        assert rel_err(g.to_host(d, l)[f.dof_nodes], xf[f.dof_nodes] + o.P[l] @ xc[c.dof_nodes]) < TOL
+        bc = g.zeros(l - 1)
+        g.restrict(l, g.to_device(xf, l), bc)
+        assert rel_err(g.to_host(bc, l - 1)[c.dof_nodes], o.P[l].T @ xf[f.dof_nodes]) < TOL
+    lf = o.fine.lv
+    bl = rnd(w, 52, None)
+    x = g.zeros()
+    g.vcycle(x, g.to_device(bl))
+    assert rel_err(g.to_host(x)[lf.dof_nodes], o.precondition(bl[lf.dof_nodes])) < 10 * TOL
+    x = g.zeros()
+    it, rel = g.solve_cg_mg(x, g.to_device(bl), tol=1e-8, max_it=100)
+    xo, ito, _ = o.solve_cg(bl[lf.dof_nodes], 1e-8, 100)
+    assert it == ito and rel <= 1e-8
+    assert rel_err(g.to_host(x)[lf.dof_nodes], xo) < 1e-7

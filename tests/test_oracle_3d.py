@@ -52,7 +52,7 @@ def test_global_volume_and_area(n, tol):
     area = 0.0
     for k, j, i in zip(*np.nonzero(lv.cell_type == CUT)):
         lo = lv.lo(i, j, k)
-        vp, vw, sp, sw, sn = cut_cell_rules3(lo, lo + lv.h, S1, 3)
+        vp, vw, sp, sw, sn = cut_cell_rules3(lo, lv.hi(i, j, k), S1, 3)
         vol += vw.sum()
         area += sw.sum()
     assert abs(vol - 4 * math.pi / 3) < tol
@@ -139,7 +139,7 @@ def test_spd_symmetry_constant_and_ghost_consistency(p):
     area = 0.0
     for k, j, i in zip(*np.nonzero(lv.cell_type == CUT)):
         lo = lv.lo(i, j, k)
-        area += cut_cell_rules3(lo, lo + lv.h, S1, prm.n_q)[3].sum()
+        area += cut_cell_rules3(lo, lv.hi(i, j, k), S1, prm.n_q)[3].sum()
     y = A @ np.ones(lv.n_dofs)
     assert abs(y.sum() - prm.gamma_D / lv.h * area) < 1e-10 * abs(y.sum())
     G = assemble_matrix3(lv, prm, with_cells=False)
@@ -176,10 +176,10 @@ def test_manufactured_solution_rate_3d(p, ns):
                         continue
                     lo = lv.lo(i, j, k)
                     if ct == INSIDE:
-                        vp, vw = tensor_gauss3(lo, lo + lv.h, p + 1)
+                        vp, vw = tensor_gauss3(lo, lv.hi(i, j, k), p + 1)
                         sp_ = np.zeros((0, 3)); sw = np.zeros(0); sn = np.zeros((0, 3))
                     else:
-                        vp, vw, sp_, sw, sn = cut_cell_rules3(lo, lo + lv.h, S1, p + 1)
+                        vp, vw, sp_, sw, sn = cut_cell_rules3(lo, lv.hi(i, j, k), S1, p + 1)
                     d = cell_dofs3(lv, i, j, k)
                     if len(vw):
                         v, *_ = eval_basis3(lv, i, j, k, vp)
@@ -195,9 +195,9 @@ def test_manufactured_solution_rate_3d(p, ns):
         for i, j, k, ct in err_pts:
             lo = lv.lo(i, j, k)
             if ct == INSIDE:
-                vp, vw = tensor_gauss3(lo, lo + lv.h, p + 3)
+                vp, vw = tensor_gauss3(lo, lv.hi(i, j, k), p + 3)
             else:
-                vp, vw, *_ = cut_cell_rules3(lo, lo + lv.h, S1, p + 3)
+                vp, vw, *_ = cut_cell_rules3(lo, lv.hi(i, j, k), S1, p + 3)
             if len(vw):
                 v, *_ = eval_basis3(lv, i, j, k, vp)
                 e2 += float(np.sum(vw * (u[cell_dofs3(lv, i, j, k)] @ v - ex(*vp.T)) ** 2))
