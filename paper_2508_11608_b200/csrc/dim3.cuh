@@ -871,3 +871,186 @@ __global__ void k_restrict3(LevelArgs Lf, LevelArgs Lc, const double* rf, double
 }
 
 }  // namespace cf
+
+namespace cf {
+
+// ---- 3D cut patches, v2: descriptor + lane-parallel faces and cells --------
+struct __align__(16) CutDesc3 {
+  int I, J, K, e0;
+  unsigned long long kinds[2];   // 2 bits per cell of the 4x4x4 window, index (wz*4 + wy)*4 + wx
+  int cid[8];                    // cut ids of the patch cells q = dx + 2 dy + 4 dz (-1 if not cut)
+  long long inv_off;
+  unsigned long long mask[2];    // interior set over the (2p+1)^3 block (p <= 2: <= 125 bits)
+};
+
+__device__ __forceinline__ int dkind3(const CutDesc3& d, int wx, int wy, int wz) {
+  const int idx = (wz * 4 + wy) * 4 + wx;
+  return (int)((d.kinds[idx >> 5] >> (2 * (idx & 31))) & 3ull);
+}
+
+template <int P>
+__global__ void k_cut_desc3(LevelArgs L, const int* plist, int np, const int64_t* ent_off, const uint16_t* ent_loc,
+                            const int64_t* inv_off, CutDesc3* desc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  const int nv = L.n + 1;
+  CutDesc3 d;
+  d.I = plist[k] % nv;
+  d.J = (plist[k] / nv) % nv;
+  d.K = plist[k] / (nv * nv);
+  d.kinds[0] = d.kinds[1] = 0ull;
+  for (int wz = 0; wz < 4; ++wz)
+    for (int wy = 0; wy < 4; ++wy)
+      for (int wx = 0; wx < 4; ++wx) {
+        const int idx = (wz * 4 + wy) * 4 + wx;
+        d.kinds[idx >> 5] |= (unsigned long long)cell_kind3(L, d.I - 2 + wx, d.J - 2 + wy, d.K - 2 + wz) << (2 * (idx & 31));
+      }
+  for (int q = 0; q < 8; ++q) {
+    const int ci = d.I - 1 + (q & 1), cj = d.J - 1 + ((q >> 1) & 1), ck = d.K - 1 + (q >> 2);
+    d.cid[q] = cell_kind3(L, ci, cj, ck) == CUT ? L.cut_id[((size_t)ck * L.n + cj) * L.n + ci] : -1;
+  }
+  d.e0 = (int)ent_off[k];
+  d.inv_off = inv_off[k];
+  d.mask[0] = d.mask[1] = 0ull;
+  for (int64_t e = ent_off[k]; e < ent_off[k + 1]; ++e) d.mask[ent_loc[e] >> 6] |= 1ull << (ent_loc[e] & 63);
+  desc[k] = d;
+}
+
+template <int P>
+struct Cut3Smem {
+  static constexpr int N1 = P + 1, NB = N1 * N1 * N1, BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS * BS;
+  static constexpr int NJ = 36 * P * N1 * N1;
+  static constexpr int per_warp = WS * WS * WS + 2 * NJ + 8 * NB + 2 * MM;
+};
+
+// one CTA of NT threads per patch: z = A_j^{-1} (b - A x)|_{I_j} -> zbuf[d.e0 + i]
+template <int P, int NT>
+__device__ void cut_patch_z3d(const LevelArgs& L, const CutDesc3& d, const double* inv, const double* x,
+                              const double* b, double* zbuf, const SmTab& T, double* Wp) {
+  using S = Cut3Smem<P>;
+  constexpr int N1 = S::N1, NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, NJ = S::NJ, FJ = P * N1 * N1;
+  const int lane = threadIdx.x;   // thread index within the patch group of NT threads
+  double* Jt = Wp + WS * WS * WS;
+  double* Jm = Jt + NJ;
+  double* Yc = Jm + NJ;        // [8][NB] per-cell outputs
+  double* Rr = Yc + 8 * NB;    // [MM]
+  const int m = __popcll(d.mask[0]) + __popcll(d.mask[1]);
+  pdl_wait();
+  for (int e = lane; e < WS * WS * WS; e += NT) {
+    const int a = P * (d.I - 2) + e % WS, bb = P * (d.J - 2) + (e / WS) % WS, c = P * (d.K - 2) + e / (WS * WS);
+    if (a >= 0 && bb >= 0 && c >= 0 && a < L.nl && bb < L.nl && c < L.nl)
+      cp_async8(Wp + e, x + ((size_t)c * L.nl + bb) * L.ld + a);
+    else Wp[e] = 0.0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  // ghost faces: jumps (face f = (axis*3 + s)*4 + t), then (M⊗M) moments
+  for (int job = lane; job < NJ; job += NT) {
+    const int f = job / FJ, rem = job - f * FJ;
+    const int k = rem / (N1 * N1) + 1, l1 = (rem / N1) % N1, l2 = rem % N1;
+    const int axis = f / 12, s = (f / 4) % 3, t = f % 4;
+    const int t1 = axis == 0 ? 1 : 0, t2 = axis == 2 ? 1 : 2;
+    int w1[3];
+    w1[axis] = s;
+    w1[t1] = 1 + (t & 1);
+    w1[t2] = 1 + (t >> 1);
+    int w2[3] = {w1[0], w1[1], w1[2]};
+    w2[axis] += 1;
+    const int k1 = dkind3(d, w1[0], w1[1], w1[2]), k2 = dkind3(d, w2[0], w2[1], w2[2]);
+    double sacc = 0.0;
+    if (k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT)) {
+      const int st[3] = {1, WS, WS * WS};
+      const double* X1 = Wp + (P * w1[2] * WS + P * w1[1]) * WS + P * w1[0];
+      const double* X2 = Wp + (P * w2[2] * WS + P * w2[1]) * WS + P * w2[0];
+#pragma unroll
+      for (int nn = 0; nn < N1; ++nn) {
+        const int o = nn * st[axis] + l1 * st[t1] + l2 * st[t2];
+        sacc = fma(T.d1[k][nn], X1[o], fma(-T.d0[k][nn], X2[o], sacc));
+      }
+    }
+    Jt[job] = sacc;
+  }
+  __syncthreads();
+  for (int job = lane; job < NJ; job += NT) {
+    const int base = job - job % (N1 * N1), q1 = (job / N1) % N1, q2 = job % N1;
+    double sacc = 0.0;
+#pragma unroll
+    for (int l1 = 0; l1 < N1; ++l1)
+#pragma unroll
+      for (int l2 = 0; l2 < N1; ++l2) sacc = fma(T.M[q1][l1] * T.M[q2][l2], Jt[base + l1 * N1 + l2], sacc);
+    Jm[job] = sacc;
+  }
+  __syncthreads();
+  // per (cell, local row): cell term + the ghost faces of that cell
+  for (int job = lane; job < 8 * NB; job += NT) {
+    const int q = job / NB, t = job % NB;
+    const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+    const int kind = dkind3(d, dx + 1, dy + 1, dz + 1);
+    double y = 0.0;
+    if (kind != OUTSIDE) {
+      const int kx = t % N1, ky = (t / N1) % N1, kz = t / (N1 * N1);
+      const double* X = Wp + (P * (dz + 1) * WS + P * (dy + 1)) * WS + P * (dx + 1);
+      if (kind == INSIDE) {
+        y = inside_row3<P>(T, X, WS, WS * WS, kx, ky, kz, L.h);
+      } else {
+        const double* Er = L.ecut + ((size_t)d.cid[q] * NB + t) * NB;
+#pragma unroll
+        for (int l = 0; l < NB; ++l) y = fma(__ldg(Er + l), X[((l / (N1 * N1)) * WS + (l / N1) % N1) * WS + l % N1], y);
+      }
+      const int kk[3] = {kx, ky, kz}, dd[3] = {dx, dy, dz};
+#pragma unroll
+      for (int axis = 0; axis < 3; ++axis) {
+        const int t1 = axis == 0 ? 1 : 0, t2 = axis == 2 ? 1 : 2;
+        const int tt = dd[t1] + 2 * dd[t2];
+        const int flo = (axis * 3 + dd[axis]) * 4 + tt, fhi = (axis * 3 + dd[axis] + 1) * 4 + tt;
+#pragma unroll
+        for (int k = 1; k <= P; ++k) {
+          const int o = (k - 1) * N1 * N1 + kk[t1] * N1 + kk[t2];
+          y = fma(-L.gs[k] * T.d0[k][kk[axis]], Jm[flo * FJ + o], y);
+          y = fma(L.gs[k] * T.d1[k][kk[axis]], Jm[fhi * FJ + o], y);
+        }
+      }
+    }
+    Yc[job] = y;
+  }
+  __syncthreads();
+  // gather the interior rows (fixed cell order), residual
+  for (int loc = lane; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if (!((word >> (loc & 63)) & 1ull)) continue;
+    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    const int ra = loc % BS, rb = (loc / BS) % BS, rc = loc / (BS * BS);
+    double y = 0.0;
+    for (int q = 0; q < 8; ++q) {
+      const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+      const int kx = ra - P * dx, ky = rb - P * dy, kz = rc - P * dz;
+      if (kx < 0 || kx > P || ky < 0 || ky > P || kz < 0 || kz > P) continue;
+      y += Yc[q * NB + (kz * N1 + ky) * N1 + kx];
+    }
+    const double bv = b[((size_t)(P * (d.K - 1) + rc) * L.nl + P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra];
+    Rr[i] = bv - y;
+  }
+  __syncthreads();
+  const double* A = inv + d.inv_off;
+  for (int i = lane; i < m; i += NT) {
+    double z = 0.0;
+    for (int q = 0; q < m; ++q) z = fma(__ldg(A + (int64_t)q * m + i), Rr[q], z);
+    zbuf[d.e0 + i] = z;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) k_cut_colour3v2(LevelArgs L, const CutDesc3* desc, int np, const double* inv,
+                                                       const double* x, const double* b, double* zbuf) {
+  __shared__ SmTab T;
+  extern __shared__ double dsm[];
+  pdl_trigger();
+  load_smtab<P>(T);
+  __syncthreads();
+  const int k = blockIdx.x;
+  if (k >= np) return;
+  const CutDesc3 d = desc[k];
+  cut_patch_z3d<P, 128>(L, d, inv, x, b, zbuf, T, dsm);
+}
+
+}  // namespace cf

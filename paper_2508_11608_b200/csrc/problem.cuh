@@ -1094,6 +1094,12 @@ struct Problem {
         k_batched_inverse<<<ncp, 256, smb, st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp);
         CF_LAUNCHED();
       }
+      D.desc = alloc<CutDesc3>(ncp);
+      if (ncp) {
+        CF_DISPATCH3(p, (k_cut_desc3<P><<<ceil_div(ncp, 128), 128, 0, st>>>(L, D.cutp_list, ncp, D.cutp_ent, D.ent_loc,
+                                                                            D.cutp_inv, (CutDesc3*)D.desc)));
+        CF_LAUNCHED();
+      }
       sync();
     }
     build_coarse();
@@ -1136,10 +1142,23 @@ struct Problem {
     const int np = D.n_cutp[c];
     if (!np) return;
     const int base = D.cutp_off[c];
-    CF_DISPATCH3(prm.p, (launch(k_cut_colour3<P>, dim3(ceil_div(np, 2)), dim3(64), 0, D.a,
-                                (const int*)(D.cutp_list + base), np, base, (const int64_t*)D.cutp_ent,
-                                (const uint16_t*)D.ent_loc, (const int32_t*)D.ent_node, (const int64_t*)D.cutp_inv,
-                                (const double*)D.inv, (const double*)x, b, D.zbuf, prm.cut_mode)));
+    if (prm.cut_mode == 0) {
+      CF_DISPATCH3(prm.p, {
+        const size_t pw = Cut3Smem<P>::per_warp * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          attr = true;
+        }
+        launch(k_cut_colour3v2<P>, dim3(np), dim3(128), pw, D.a, (const CutDesc3*)D.desc + base, np,
+               (const double*)D.inv, (const double*)x, b, D.zbuf);
+      });
+    } else {
+      CF_DISPATCH3(prm.p, (launch(k_cut_colour3<P>, dim3(ceil_div(np, 2)), dim3(64), 0, D.a,
+                                  (const int*)(D.cutp_list + base), np, base, (const int64_t*)D.cutp_ent,
+                                  (const uint16_t*)D.ent_loc, (const int32_t*)D.ent_node, (const int64_t*)D.cutp_inv,
+                                  (const double*)D.inv, (const double*)x, b, D.zbuf, prm.cut_mode)));
+    }
     CF_LAUNCHED();
     const int64_t e0 = D.ent_col_off[c], e1 = D.ent_col_off[c + 1];
     if (e1 <= e0) return;
