@@ -949,24 +949,19 @@ __device__ void cut_patch_z3d(const LevelArgs& L, const CutDesc3& d, const doubl
     const int f = job / FJ, rem = job - f * FJ;
     const int k = rem / (N1 * N1) + 1, l1 = (rem / N1) % N1, l2 = rem % N1;
     const int axis = f / 12, s = (f / 4) % 3, t = f % 4;
-    const int t1 = axis == 0 ? 1 : 0, t2 = axis == 2 ? 1 : 2;
-    int w1[3];
-    w1[axis] = s;
-    w1[t1] = 1 + (t & 1);
-    w1[t2] = 1 + (t >> 1);
-    int w2[3] = {w1[0], w1[1], w1[2]};
-    w2[axis] += 1;
-    const int k1 = dkind3(d, w1[0], w1[1], w1[2]), k2 = dkind3(d, w2[0], w2[1], w2[2]);
+    // window cell of side 1 (w1x, w1y, w1z) and the strides of the normal / tangential axes
+    const int ta = 1 + (t & 1), tb = 1 + (t >> 1);
+    const int w1x = axis == 0 ? s : ta, w1y = axis == 1 ? s : (axis == 0 ? ta : tb), w1z = axis == 2 ? s : tb;
+    const int w2x = w1x + (axis == 0), w2y = w1y + (axis == 1), w2z = w1z + (axis == 2);
+    const int sn = axis == 0 ? 1 : (axis == 1 ? WS : WS * WS);
+    const int s1 = axis == 0 ? WS : 1, s2 = axis == 2 ? WS : WS * WS;
+    const int k1 = dkind3(d, w1x, w1y, w1z), k2 = dkind3(d, w2x, w2y, w2z);
     double sacc = 0.0;
     if (k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT)) {
-      const int st[3] = {1, WS, WS * WS};
-      const double* X1 = Wp + (P * w1[2] * WS + P * w1[1]) * WS + P * w1[0];
-      const double* X2 = Wp + (P * w2[2] * WS + P * w2[1]) * WS + P * w2[0];
+      const double* X1 = Wp + (P * w1z * WS + P * w1y) * WS + P * w1x + l1 * s1 + l2 * s2;
+      const double* X2 = X1 + P * sn;
 #pragma unroll
-      for (int nn = 0; nn < N1; ++nn) {
-        const int o = nn * st[axis] + l1 * st[t1] + l2 * st[t2];
-        sacc = fma(T.d1[k][nn], X1[o], fma(-T.d0[k][nn], X2[o], sacc));
-      }
+      for (int nn = 0; nn < N1; ++nn) sacc = fma(T.d1[k][nn], X1[nn * sn], fma(-T.d0[k][nn], X2[nn * sn], sacc));
     }
     Jt[job] = sacc;
   }
@@ -997,17 +992,18 @@ __device__ void cut_patch_z3d(const LevelArgs& L, const CutDesc3& d, const doubl
 #pragma unroll
         for (int l = 0; l < NB; ++l) y = fma(__ldg(Er + l), X[((l / (N1 * N1)) * WS + (l / N1) % N1) * WS + l % N1], y);
       }
-      const int kk[3] = {kx, ky, kz}, dd[3] = {dx, dy, dz};
 #pragma unroll
       for (int axis = 0; axis < 3; ++axis) {
-        const int t1 = axis == 0 ? 1 : 0, t2 = axis == 2 ? 1 : 2;
-        const int tt = dd[t1] + 2 * dd[t2];
-        const int flo = (axis * 3 + dd[axis]) * 4 + tt, fhi = (axis * 3 + dd[axis] + 1) * 4 + tt;
+        const int ka = axis == 0 ? kx : (axis == 1 ? ky : kz);
+        const int kt1 = axis == 0 ? ky : kx, kt2 = axis == 2 ? ky : kz;
+        const int da = axis == 0 ? dx : (axis == 1 ? dy : dz);
+        const int tt = axis == 0 ? dy + 2 * dz : (axis == 1 ? dx + 2 * dz : dx + 2 * dy);
+        const int flo = (axis * 3 + da) * 4 + tt, fhi = flo + 4;
 #pragma unroll
         for (int k = 1; k <= P; ++k) {
-          const int o = (k - 1) * N1 * N1 + kk[t1] * N1 + kk[t2];
-          y = fma(-L.gs[k] * T.d0[k][kk[axis]], Jm[flo * FJ + o], y);
-          y = fma(L.gs[k] * T.d1[k][kk[axis]], Jm[fhi * FJ + o], y);
+          const int o = (k - 1) * N1 * N1 + kt1 * N1 + kt2;
+          y = fma(-L.gs[k] * T.d0[k][ka], Jm[flo * FJ + o], y);
+          y = fma(L.gs[k] * T.d1[k][ka], Jm[fhi * FJ + o], y);
         }
       }
     }
