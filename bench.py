@@ -132,6 +132,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-3d", action="store_true", help="skip the secondary 3D (configs[2]) measurement")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -201,29 +202,28 @@ def main():
     peak, peak_src = measured_peak_hbm()
     cart_ms = float(np.mean(timed(lambda: g.colour_step(L, 2, 0, x, b), 50, 3)))
     cart_bytes = 24.0 * p * p * info.n_inside
-    cut_ms, cut_bytes = [], []
     off, _ = g.cut_interior(L)
-    m_all = np.diff(off)
+    m_all = np.diff(off).astype(np.float64)
     nb = (p + 1) ** 2
-    for c in range(4):
-        cut_ms.append(float(np.mean(timed(lambda: g.colour_step(L, 1, c, x, b), 50, 3))))
-        lo = int(sum(info.n_cutp[:c]))
-        m = m_all[lo:lo + info.n_cutp[c]].astype(np.float64)
-        cut_bytes.append(float(np.sum(8 * m * m + 8 * (2 * p + 1) ** 2 + 32 * m)) + 8.0 * nb * nb * info.n_cut / 4)
-    per_step = {"cart_sweep": cart_ms, "cut_colours": w.n_c * float(np.sum(cut_ms))}
+    n_cut_launch = 4 * w.n_c
+    sweeps_ms = float(np.mean(timed(lambda: g.colour_step(L, 3, 0, x, b), 50, 3)))
+    cut_ms = sweeps_ms / n_cut_launch
+    # per cut step (one colour): 8 m^2 (inverse) + 8 (2p+1)^2 (x block) + 8 m (b) + 16 m (x read, x write)
+    # per patch, + 8 ((p+1)^2)^2 per cut cell (element matrix); averaged over the colours
+    cut_bytes = (float(np.sum(8 * m_all * m_all + 8 * (2 * p + 1) ** 2 + 24 * m_all)) +
+                 8.0 * nb * nb * info.n_cut) / 4.0
+    per_step = {"cart_sweep": cart_ms, "cut_sweeps": sweeps_ms}
     kernels = {
-        "k_cart_fused_mma (4 Cartesian colours)": {
+        "k_cart_fused_tma (4 Cartesian colours, one launch)": {
             "launches_per_step": 1, "avg_launch_ms": cart_ms, "bytes_per_launch": cart_bytes,
             "achieved_gbs": cart_bytes / (cart_ms * 1e-3) / 1e9},
-        "k_cut_colour_v3 + k_cut_apply (one cut colour)": {
-            "launches_per_step": 8 * w.n_c, "avg_launch_ms": float(np.mean(cut_ms)),
-            "bytes_per_launch": float(np.mean(cut_bytes)),
-            "achieved_gbs": float(np.mean(cut_bytes)) / (float(np.mean(cut_ms)) * 1e-3) / 1e9}}
-    if per_step["cart_sweep"] >= per_step["cut_colours"]:
-        dom, d_bytes, d_ms = "k_cart_fused_mma<P=%d> (fused Cartesian sweep)" % p, cart_bytes, cart_ms
+        "k_cut_step (one cut colour)": {
+            "launches_per_step": n_cut_launch, "avg_launch_ms": cut_ms, "bytes_per_launch": cut_bytes,
+            "achieved_gbs": cut_bytes / (cut_ms * 1e-3) / 1e9}}
+    if per_step["cart_sweep"] >= per_step["cut_sweeps"]:
+        dom, d_bytes, d_ms = "k_cart_fused_tma<P=%d> (fused Cartesian sweep)" % p, cart_bytes, cart_ms
     else:
-        dom, d_bytes, d_ms = ("k_cut_colour_v3<P=%d> + k_cut_apply (cut colour step)" % p,
-                              float(np.mean(cut_bytes)), float(np.mean(cut_ms)))
+        dom, d_bytes, d_ms = "k_cut_step<P=%d> (cut colour step)" % p, cut_bytes, cut_ms
     achieved = d_bytes / (d_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -265,6 +265,39 @@ def main():
     e2e = {"value": n_dofs * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * nl * ld * 8,
            "d2h_bytes_per_step": nl * ld * 8}
 
+    # ---- BASELINE configs[2]: 3D sphere, Q2, 128^3 (secondary line, same timing rules)
+    cfg3 = None
+    if not args.no_3d:
+        g.close()
+        w3 = workloads.CONFIG2
+        g3 = cutfem.Problem.from_workload(w3)
+        L3 = w3.n_levels - 1
+        i3 = g3.level_info(L3)
+        x3 = g3.to_device(workloads.lattice_vector(w3, 1))
+        b3 = g3.to_device(workloads.lattice_vector(w3, 2))
+        ms3 = timed(lambda: g3.smooth(L3, x3, b3), 10, 3)
+        z3 = g3.zeros()
+        v3 = timed(lambda: (z3.zero_(), g3.vcycle(z3, b3)), 3, 1)
+        xs3 = g3.zeros()
+        g3.solve_cg_mg(xs3, b3, tol=w3.tol)
+        torch.cuda.synchronize()
+        c0 = torch.cuda.Event(enable_timing=True); c1 = torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        it3, rel3 = g3.solve_cg_mg(xs3, b3, tol=w3.tol)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        cart3 = float(np.mean(timed(lambda: g3.colour_step(L3, 0, 0, x3, b3), 10, 2)))
+        # Cartesian colour step: x read over the colour's blocks (~ all active nodes),
+        # b read and x written on the colour's interiors (~ 1/8 of the nodes each)
+        cart3_bytes = 8.0 * i3.n_dofs * (1.0 + 2.0 / 8.0)
+        cfg3 = {"workload": w3.name, "n_dofs": int(i3.n_dofs), "cells_per_side": i3.n, "degree": w3.p,
+                "smoothing_dofs_per_s": i3.n_dofs / (float(np.mean(ms3)) * 1e-3),
+                "ms_per_step": float(np.mean(ms3)), "vcycle_ms": float(np.median(v3)),
+                "cg_mg": {"time_to_solution_ms": c0.elapsed_time(c1), "iterations": it3, "rel_residual": rel3},
+                "cart_colour_ms": cart3, "cart_colour_achieved_gbs": cart3_bytes / (cart3 * 1e-3) / 1e9,
+                "l2": "flushed before every timed step (vectors 142 MB > L2)"}
+        g3.close()
+
     if rank == 0:
         cb = None
         if not args.no_cpu_baseline:
@@ -291,6 +324,7 @@ def main():
                       "dofs_per_s": n_dofs / (cg_ms * 1e-3)},
             "e2e": e2e,
             "cpu_baseline": cb,
+            "config2_3d": cfg3,
         }
         print(json.dumps(out), flush=True)
     if dist:

@@ -117,8 +117,9 @@ int cutfem_apply_operator(cutfem_problem pb, int level, const double* x, double*
 int cutfem_smooth(cutfem_problem pb, int level, double* x, const double* b, int reverse, void* stream);
 
 /* One colour step of the smoother (P l.179-181, R9): kind 0 = Cartesian,
- * 1 = cut patches; colour 0..3.  kind 2 runs the whole Cartesian sweep
- * (colours 0..3, or 3..0 if colour is odd) as the smoother does.  x <- x + sum_j Q_j^T A_j^{-1} Q_j (b - A x)
+ * 1 = cut patches; colour 0..3 (0..7 in 3D).  2D only: kind 2 runs the
+ * whole Cartesian sweep and kind 3 the n_c cut sweeps of a smoothing step
+ * (forward, or reversed if colour is odd) exactly as cutfem_smooth does.  x <- x + sum_j Q_j^T A_j^{-1} Q_j (b - A x)
  * with the residual taken before the step.  Used by the sampled full-size
  * parity tests. */
 int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, double* x, const double* b, void* stream);

@@ -145,13 +145,16 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
   return guarded([&]() {
     check_built(pb);
     check_level(pb, level);
-    cf::require(kind >= 0 && kind <= 2 && colour >= 0 && colour < 8, cf::ERR_ARG, "bad kind/colour");
+    cf::require(kind >= 0 && kind <= 3 && colour >= 0 && colour < 8, cf::ERR_ARG, "bad kind/colour");
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
     if (pb->p.prm.dim == 3) {
       cf::require(kind <= 1 && colour < 8, cf::ERR_ARG, "3D colour step: kind 0/1, colour 0..7");
       if (kind == 0) pb->p.cart_step3(level, colour, x, b);
       else pb->p.cut_step3(level, colour, x, b);
+    } else if (kind == 3) {
+      cf::require(pb->p.pingpong, cf::ERR_STATE, "kind 3 needs the ping-pong cut sweeps");
+      pb->p.cut_sweeps(level, x, b, colour & 1);
     } else if (kind == 0) pb->p.cart_step(level, colour, x, b);
     else if (kind == 1 && pb->p.pingpong) {
       cf::require(colour < 4, cf::ERR_ARG, "2D colours are 0..3");
