@@ -34,8 +34,11 @@ WORKLOAD = workloads.CONFIG1
 ORACLE_SAMPLE_LEVEL = 6           # 128 x 128 cells of the same hierarchy (bounded CPU sample)
 
 
+from paper_2508_11608_b200.dist import max_over_ranks, rank_env, replica_throughput  # noqa: E402
+
+
 def dist_env():
-    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+    return rank_env()
 
 
 def clock_sampler_start(path):
@@ -189,13 +192,10 @@ def main():
     launches = cutfem.launch_count() - l0
     torch.cuda.synchronize()
     clocks = clock_sampler_stop(clk, clk_path, local) if rank == 0 else None
-    total_ms = float(sum(ms))
+    total_ms = max_over_ranks(float(sum(ms)), dist, "cuda")
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
-    value = n_dofs * args.steps * world / (total_ms * 1e-3)
+    value = replica_throughput(n_dofs, args.steps, world, total_ms)
 
     # ---- kernels of the step, timed alone (live, CUDA events, L2 flushed)
     p = w.p

@@ -1,0 +1,51 @@
+"""world_size-2 gloo tests (CPU) of the multi-process bench plumbing."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2508_11608_b200.dist import max_over_ranks, rank_env, replica_throughput
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    r, w, lr = rank_env()
+    t = max_over_ranks(10.0 + 5.0 * rank, dist)        # rank 1 is slower
+    v = replica_throughput(1000, 4, w, t)
+    dist.barrier()
+    q.put((r, w, lr, t, v))
+    dist.destroy_process_group()
+
+
+def test_max_over_ranks_and_throughput_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[:3] for r in res] == [(0, 2, 0), (1, 2, 1)]
+    for r in res:
+        assert r[3] == 15.0                          # max over ranks
+        assert r[4] == pytest.approx(1000 * 4 * 2 / 15e-3)
+
+
+def test_single_process_identity():
+    assert max_over_ranks(3.5) == 3.5
+    assert replica_throughput(10, 2, 1, 1.0) == pytest.approx(2e4)
