@@ -61,6 +61,7 @@ struct Problem {
   bool use_mma = true;      // Cartesian patch map on fp64 tensor cores (env CUTFEM_MMA=0 disables)
   bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
   bool use_tma = true;      // TMA tile loads in the fused Cartesian sweep (env CUTFEM_TMA=0 disables)
+  bool cta_cut = true;      // CTA of 64 threads per cut patch (env CUTFEM_CTACUT=0: one warp per patch)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -175,6 +176,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_MMA")) use_mma = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_PINGPONG")) pingpong = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TMA")) use_tma = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_CTACUT")) cta_cut = std::atoi(e) != 0;
     host::cart_map(prm.p);  // dense Cartesian patch map (p <= 3), built outside any graph capture
     d_count = alloc<int>(1);
     const int p = prm.p;
@@ -721,22 +723,35 @@ struct Problem {
     if (!np && !ncopy) return;
     const CutDesc* desc = (const CutDesc*)D.desc + D.cutp_off[c];
     CF_DISPATCH(prm.p, {
-      const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
-      const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
-      const size_t smb = wpb * pw;
-      static bool attr = false;
-      if (!attr) {
-        CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
+      if (prm.cut_mode == 0 && cta_cut) {
+        constexpr int NT = 64;
+        const size_t smb = CutSmem4<P>::doubles * sizeof(double);
+        static bool attr4 = false;
+        if (!attr4) {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_step4<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          attr4 = true;
+        }
+        const int cb = ceil_div(ncopy, NT);
+        launch(k_cut_step4<P, NT>, dim3(np + cb), dim3(NT), smb, D.a, desc, np, np, (const double*)D.ecut,
+               (const double*)D.inv, R, W, b, cl, ncopy);
+      } else {
+        const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
+        const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
+        const size_t smb = wpb * pw;
+        static bool attr = false;
+        if (!attr) {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          attr = true;
+        }
+        const int pb = ceil_div(np, wpb), cb = ceil_div(ncopy, 128);
+        if (prm.cut_mode == 0)
+          launch(k_cut_step<P, false>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
+                 (const double*)D.inv, R, W, b, cl, ncopy);
+        else
+          launch(k_cut_step<P, true>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
+                 (const double*)D.inv, R, W, b, cl, ncopy);
       }
-      const int pb = ceil_div(np, wpb), cb = ceil_div(ncopy, 128);
-      if (prm.cut_mode == 0)
-        launch(k_cut_step<P, false>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
-               (const double*)D.inv, R, W, b, cl, ncopy);
-      else
-        launch(k_cut_step<P, true>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
-               (const double*)D.inv, R, W, b, cl, ncopy);
     });
     CF_LAUNCHED();
   }

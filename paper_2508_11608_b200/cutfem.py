@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libcutfem_mg.so")
+_LIB_PATH = os.environ.get("CUTFEM_LIB_OVERRIDE") or os.path.join(_HERE, "libcutfem_mg.so")
 
 
 class CutfemError(RuntimeError):

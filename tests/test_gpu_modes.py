@@ -44,8 +44,8 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
 
 
 @pytest.mark.parametrize("env", [{"CUTFEM_MMA": "0"}, {"CUTFEM_FUSED": "0"}, {"CUTFEM_PINGPONG": "0"},
-                                 {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}],
-                         ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma"])
+                                 {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}, {"CUTFEM_CTACUT": "0"}],
+                         ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
