@@ -58,10 +58,12 @@ struct Problem {
   bool built = false;
   bool persistent = false;  // one cooperative launch per smoothing step (env CUTFEM_PERSISTENT=1)
   bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
+  int persistent_below = 0; // levels with n <= this use the cooperative one-launch smoothing step (env)
   bool use_mma = true;      // Cartesian patch map on fp64 tensor cores (env CUTFEM_MMA=0 disables)
   bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
   bool use_tma = true;      // TMA tile loads in the fused Cartesian sweep (env CUTFEM_TMA=0 disables)
   bool cta_cut = true;      // CTA of 64 threads per cut patch (env CUTFEM_CTACUT=0: one warp per patch)
+  bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -177,6 +179,8 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_PINGPONG")) pingpong = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TMA")) use_tma = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CTACUT")) cta_cut = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_PERSISTENT_BELOW")) persistent_below = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
     host::cart_map(prm.p);  // dense Cartesian patch map (p <= 3), built outside any graph capture
     d_count = alloc<int>(1);
     const int p = prm.p;
@@ -559,6 +563,24 @@ struct Problem {
       }
       CF_LAUNCHED();
     }
+    bool tile_ok = false;
+    CF_DISPATCH(p, tile_ok = L.nl >= ApplySmem<P, 16>::RW && L.ld >= ApplySmem<P, 16>::RWP);
+    if (tile_apply && tile_ok) {   // the TMA box must fit inside the lattice
+      CF_DISPATCH(p, {
+        constexpr int TX = 16;
+        using S = ApplySmem<P, TX>;
+        const CUtensorMap tm = host::lattice_tmap(x, L.nl, L.ld, S::RWP, S::RW);
+        static bool attr = false;
+        if (!attr) {
+          CF_CUDA(cudaFuncSetAttribute(k_apply_tile<P, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+          attr = true;
+        }
+        const int nt = ceil_div(L.n, TX);
+        launch(k_apply_tile<P, TX>, dim3(nt, nt), dim3(256), S::bytes, tm, L, b, y);
+      });
+      CF_LAUNCHED();
+      return;
+    }
     CF_DISPATCH(p, (k_node_apply<P><<<dim3(ceil_div(L.ld, 32), ceil_div(L.nl, 8)), dim3(32, 8), 0, st>>>(L, x, b, y)));
     CF_LAUNCHED();
   }
@@ -672,7 +694,7 @@ struct Problem {
     CF_DISPATCH(prm.p, {
       constexpr int TC = fused_tc<P>();
       if constexpr (P <= 3) {
-        if (use_mma && use_tma) {
+        if (use_mma && use_tma && D.a.nl >= CartTmaSmem<P, TC>::RW && D.a.ld >= CartTmaSmem<P, TC>::RWP) {
           const double* G = host::cart_map(P);
           using S = CartTmaSmem<P, TC>;
           const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
@@ -773,6 +795,10 @@ struct Problem {
   void smooth(int l, double* x, const double* b, int reverse) {
     if (prm.dim == 3) {
       smooth3(l, x, b, reverse);
+      return;
+    }
+    if (persistent_below > 0 && lv[l].a.n <= persistent_below) {
+      smooth_persistent(l, x, b, reverse);
       return;
     }
     if (pingpong && fused) {

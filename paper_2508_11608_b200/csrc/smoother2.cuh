@@ -1280,3 +1280,79 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
 }
 
 }  // namespace cf
+
+namespace cf {
+
+// ---- operator A x (or b - A x) on a TMA-staged tile ------------------------
+// CTA per TX x TX cells; the x tile with a one-cell halo is loaded by TMA
+// (zero-filled outside the lattice); one thread per owned lattice node sums
+// the cell rows of its (up to 4) cells from shared memory, the cut-cell
+// outputs (ycut) and the ghost-face moments (jm) of k_band.
+template <int P, int TX>
+struct ApplySmem {
+  // the box starts at an even column (16-byte aligned inner coordinate), so
+  // it is one column wider than the region when P (i0 - 1) is odd
+  static constexpr int RW = (TX + 2) * P + 1, RWP = (RW + 2) & ~1;
+  static constexpr int tile = (RW * RWP + 15) & ~15;
+  static constexpr size_t bytes = 128 + tile * sizeof(double) + sizeof(SmTab);
+};
+
+template <int P, int TX>
+__global__ void __launch_bounds__(256) k_apply_tile(const __grid_constant__ CUtensorMap tmx, LevelArgs L,
+                                                    const double* b, double* y) {
+  using S = ApplySmem<P, TX>;
+  constexpr int NB = (P + 1) * (P + 1), RWP = S::RWP, RW = S::RW;
+  extern __shared__ __align__(128) unsigned char smraw[];   // no static shared memory: keeps the TMA tile 128-byte aligned
+  uint64_t* bar = (uint64_t*)smraw;
+  double* Xs = (double*)(smraw + 128);
+  SmTab& T = *(SmTab*)(smraw + 128 + S::tile * sizeof(double));
+  const int tid = threadIdx.x, n = L.n;
+  const int tx = blockIdx.x, ty = blockIdx.y;
+  const int i0 = tx * TX, j0 = ty * TX;
+  const int a0 = (P * (i0 - 1)) & ~1, b0 = P * (j0 - 1), sh = P * (i0 - 1) - a0;   // sh = 0 or 1
+  pdl_trigger();
+  load_smtab<P>(T);
+  if (tid == 0) mbar_init(bar, 1);
+  __syncthreads();
+  pdl_wait();
+  if (tid == 0) {
+    mbar_expect_tx(bar, (unsigned)(RW * RWP * sizeof(double)));
+    tma_load_2d(Xs, &tmx, a0, b0, bar);
+  }
+  mbar_wait(bar, 0);
+  // owned nodes [P i0, P (i0 + TX)) (+ the last lattice line)
+  const int ahi = min(P * (i0 + TX), L.nl - 1) + ((i0 + TX >= n) ? 1 : 0);
+  const int bhi = min(P * (j0 + TX), L.nl - 1) + ((j0 + TX >= n) ? 1 : 0);
+  const int aw = ahi - P * i0, bw = bhi - P * j0;
+  for (int e = tid; e < aw * bw; e += 256) {
+    const int a = P * i0 + e % aw, bb = P * j0 + e / aw;
+    const size_t o = (size_t)bb * L.ld + a;
+    if (!L.mask[o]) {
+      y[o] = 0.0;
+      continue;
+    }
+    const int ci0 = (a % P == 0) ? a / P - 1 : a / P, ci1 = min(a / P, n - 1);
+    const int cj0 = (bb % P == 0) ? bb / P - 1 : bb / P, cj1 = min(bb / P, n - 1);
+    double acc = 0.0;
+    for (int j = max(cj0, 0); j <= cj1; ++j)
+      for (int i = max(ci0, 0); i <= ci1; ++i) {
+        const int kind = L.ctype[j * n + i];
+        if (kind == OUTSIDE) continue;
+        const int kx = a - i * P, ky = bb - j * P;
+        if (kind == INSIDE) acc += inside_row<P>(T, Xs + (P * (j - j0 + 1)) * RWP + sh + P * (i - i0 + 1), RWP, kx, ky);
+        else acc += L.ycut[(size_t)L.cut_id[j * n + i] * NB + ky * (P + 1) + kx];
+        int g;
+        if (i >= 1 && (g = L.gx_id[j * n + i - 1]) >= 0) acc += face_test<P>(L, T, 0, 2, kx, ky, L.jm + (size_t)g * P * (P + 1));
+        if ((g = L.gx_id[j * n + i]) >= 0) acc += face_test<P>(L, T, 0, 1, kx, ky, L.jm + (size_t)g * P * (P + 1));
+        if (j >= 1 && (g = L.gy_id[(j - 1) * n + i]) >= 0) acc += face_test<P>(L, T, 1, 2, kx, ky, L.jm + (size_t)g * P * (P + 1));
+        if ((g = L.gy_id[j * n + i]) >= 0) acc += face_test<P>(L, T, 1, 1, kx, ky, L.jm + (size_t)g * P * (P + 1));
+      }
+    y[o] = b ? b[o] - acc : acc;
+  }
+  // zero the padding columns of the owned rows
+  if (i0 + TX >= n)
+    for (int bb = P * j0 + tid; bb < bhi; bb += 256)
+      for (int a = L.nl; a < L.ld; ++a) y[(size_t)bb * L.ld + a] = 0.0;
+}
+
+}  // namespace cf

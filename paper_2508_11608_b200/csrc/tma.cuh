@@ -2,7 +2,8 @@
 // (fp64, rows of LD doubles) copied into shared memory by one thread with
 // cp.async.bulk.tensor; out-of-range coordinates (negative or past the
 // lattice) are zero-filled by the hardware, which gives the halo of boundary
-// tiles for free.
+// tiles for free.  The inner start coordinate must be 16-byte aligned (an
+// even column for fp64): an odd one traps with an illegal instruction.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>

@@ -34,6 +34,9 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
     l = len(o.levels) - 1
     ld = o.levels[l]
     xl, bl = lattice_random(w, 60, l), lattice_random(w, 61, l)
+    y = g.zeros(l)
+    g.apply_operator(l, g.to_device(xl, l), y)
+    assert rel_err(compact(ld.lv, g.to_host(y, l)), ld.A @ compact(ld.lv, xl)) < TOL
     for rev in (False, True):
         x = g.to_device(xl, l)
         g.smooth(l, x, g.to_device(bl, l), rev)
@@ -44,8 +47,9 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
 
 
 @pytest.mark.parametrize("env", [{"CUTFEM_MMA": "0"}, {"CUTFEM_FUSED": "0"}, {"CUTFEM_PINGPONG": "0"},
-                                 {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}, {"CUTFEM_CTACUT": "0"}],
-                         ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch"])
+                                 {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}, {"CUTFEM_CTACUT": "0"},
+                                 {"CUTFEM_TILEAPPLY": "0"}],
+                         ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
