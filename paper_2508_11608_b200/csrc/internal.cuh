@@ -63,6 +63,7 @@ struct LevelArgs {
   const int* gx_id;                  // face (i,j)|(i+1,j) -> ghost id or -1, index j*n+i
   const int* gy_id;                  // face (i,j)|(i,j+1)
   const int* gz_id;                  // 3D: face (i,j,k)|(i,j,k+1)
+  const uint8_t* ccode;              // 2D: kind | ghost faces left/right/bottom/top << 2..5
   const int* ghost_list;             // packed axis | i << 1 | j << 16... see setup
   int n_ghost;
   double* ycut;                      // n_cut * (p+1)^2 scratch (operator apply)
@@ -87,6 +88,7 @@ struct LevelData {
   int* gx_id = nullptr;
   int* gy_id = nullptr;
   int* gz_id = nullptr;
+  uint8_t* ccode = nullptr;
   int* ghost_list = nullptr;
   double* ycut = nullptr;
   double* jm = nullptr;

@@ -262,6 +262,10 @@ struct Problem {
       }
       L.gx_id = D.gx_id;
       L.gy_id = D.gy_id;
+      D.ccode = alloc<uint8_t>((int64_t)n * n);
+      k_cell_codes<<<ceil_div((int64_t)n * n, 256), 256, 0, st>>>(L, D.ccode);
+      CF_LAUNCHED();
+      L.ccode = D.ccode;
       // cut-cell quadrature (R6)
       D.q_off = alloc<int>(L.n_cut + 1);
       D.s_off = alloc<int>(L.n_cut + 1);

@@ -102,6 +102,21 @@ __global__ void k_ghost_maps(const int* list, int ng, int n, int* gx, int* gy) {
   else gy[f - n * n] = k;
 }
 
+// compact per-cell code: bits 0-1 kind, bit 2..5 = ghost face on the left,
+// right, bottom, top (one byte per cell instead of five integer loads)
+__global__ void k_cell_codes(LevelArgs L, uint8_t* code) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = L.n;
+  if (c >= n * n) return;
+  const int i = c % n, j = c / n;
+  uint8_t v = (uint8_t)L.ctype[c];
+  if (i >= 1 && L.gx_id[c - 1] >= 0) v |= 4;
+  if (L.gx_id[c] >= 0) v |= 8;
+  if (j >= 1 && L.gy_id[c - n] >= 0) v |= 16;
+  if (L.gy_id[c] >= 0) v |= 32;
+  code[c] = v;
+}
+
 // ---- cut-cell quadrature (P l.190, reading R6) -----------------------------
 // One thread per cut cell.  WRITE = false counts the points.
 template <bool WRITE>

@@ -1294,7 +1294,7 @@ struct ApplySmem {
   // it is one column wider than the region when P (i0 - 1) is odd
   static constexpr int RW = (TX + 2) * P + 1, RWP = (RW + 2) & ~1;
   static constexpr int tile = (RW * RWP + 15) & ~15;
-  static constexpr size_t bytes = 128 + tile * sizeof(double) + sizeof(SmTab);
+  static constexpr size_t bytes = 128 + tile * sizeof(double) + sizeof(SmTab) + (TX + 2) * (TX + 2);
 };
 
 template <int P, int TX>
@@ -1306,12 +1306,17 @@ __global__ void __launch_bounds__(256) k_apply_tile(const __grid_constant__ CUte
   uint64_t* bar = (uint64_t*)smraw;
   double* Xs = (double*)(smraw + 128);
   SmTab& T = *(SmTab*)(smraw + 128 + S::tile * sizeof(double));
+  uint8_t* Cs = smraw + 128 + S::tile * sizeof(double) + sizeof(SmTab);   // cell codes of the tile + halo
   const int tid = threadIdx.x, n = L.n;
   const int tx = blockIdx.x, ty = blockIdx.y;
   const int i0 = tx * TX, j0 = ty * TX;
   const int a0 = (P * (i0 - 1)) & ~1, b0 = P * (j0 - 1), sh = P * (i0 - 1) - a0;   // sh = 0 or 1
   pdl_trigger();
   load_smtab<P>(T);
+  for (int e = tid; e < (TX + 2) * (TX + 2); e += 256) {
+    const int ci = i0 - 1 + e % (TX + 2), cj = j0 - 1 + e / (TX + 2);
+    Cs[e] = (ci >= 0 && cj >= 0 && ci < n && cj < n) ? L.ccode[cj * n + ci] : 0;
+  }
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
   pdl_wait();
@@ -1336,16 +1341,18 @@ __global__ void __launch_bounds__(256) k_apply_tile(const __grid_constant__ CUte
     double acc = 0.0;
     for (int j = max(cj0, 0); j <= cj1; ++j)
       for (int i = max(ci0, 0); i <= ci1; ++i) {
-        const int kind = L.ctype[j * n + i];
+        const int code = Cs[(j - j0 + 1) * (TX + 2) + i - i0 + 1];
+        const int kind = code & 3;
         if (kind == OUTSIDE) continue;
         const int kx = a - i * P, ky = bb - j * P;
         if (kind == INSIDE) acc += inside_row<P>(T, Xs + (P * (j - j0 + 1)) * RWP + sh + P * (i - i0 + 1), RWP, kx, ky);
         else acc += L.ycut[(size_t)L.cut_id[j * n + i] * NB + ky * (P + 1) + kx];
-        int g;
-        if (i >= 1 && (g = L.gx_id[j * n + i - 1]) >= 0) acc += face_test<P>(L, T, 0, 2, kx, ky, L.jm + (size_t)g * P * (P + 1));
-        if ((g = L.gx_id[j * n + i]) >= 0) acc += face_test<P>(L, T, 0, 1, kx, ky, L.jm + (size_t)g * P * (P + 1));
-        if (j >= 1 && (g = L.gy_id[(j - 1) * n + i]) >= 0) acc += face_test<P>(L, T, 1, 2, kx, ky, L.jm + (size_t)g * P * (P + 1));
-        if ((g = L.gy_id[j * n + i]) >= 0) acc += face_test<P>(L, T, 1, 1, kx, ky, L.jm + (size_t)g * P * (P + 1));
+        if (code & 60) {
+          if (code & 4) acc += face_test<P>(L, T, 0, 2, kx, ky, L.jm + (size_t)L.gx_id[j * n + i - 1] * P * (P + 1));
+          if (code & 8) acc += face_test<P>(L, T, 0, 1, kx, ky, L.jm + (size_t)L.gx_id[j * n + i] * P * (P + 1));
+          if (code & 16) acc += face_test<P>(L, T, 1, 2, kx, ky, L.jm + (size_t)L.gy_id[(j - 1) * n + i] * P * (P + 1));
+          if (code & 32) acc += face_test<P>(L, T, 1, 1, kx, ky, L.jm + (size_t)L.gy_id[j * n + i] * P * (P + 1));
+        }
       }
     y[o] = b ? b[o] - acc : acc;
   }

@@ -10,7 +10,8 @@ from paper_2508_11608_b200 import cutfem  # noqa: E402
 
 w = getattr(workloads, sys.argv[1] if len(sys.argv) > 1 else "CONFIG1")
 MODES = {"default": dict(CUTFEM_FUSED="1", CUTFEM_PDL="1", CUTFEM_MMA="1", CUTFEM_PINGPONG="1", CUTFEM_TMA="1", CUTFEM_CTACUT="1"),
-         "warp per cut patch": dict(CUTFEM_PERSISTENT_BELOW="0", CUTFEM_CTACUT="0"),
+         "node apply": dict(CUTFEM_TILEAPPLY="0"),
+         "warp per cut patch": dict(CUTFEM_TILEAPPLY="1", CUTFEM_CTACUT="0"),
          "no tma": dict(CUTFEM_CTACUT="1", CUTFEM_TMA="0"),
          "no mma (FD)": dict(CUTFEM_TMA="1", CUTFEM_MMA="0"),
          "no pdl": dict(CUTFEM_MMA="1", CUTFEM_PDL="0")}
