@@ -1049,4 +1049,197 @@ __global__ void __launch_bounds__(128) k_cut_colour3v2(LevelArgs L, const CutDes
   cut_patch_z3d<P, 128>(L, d, inv, x, b, zbuf, T, dsm);
 }
 
+// v3: one thread per (ghost face, derivative order) computes the face jumps in
+// registers and their (M x M) moments (no jump array in shared memory), a
+// 36-bit ghost-face mask lets the cell rows skip non-ghost faces, and the
+// cut-cell rows read column t of the symmetric element matrix (a warp's loads
+// of one cell are coalesced).  TMA = true: the (4p+1)^3 window arrives as one
+// 3D TMA box with rows padded to RS = 4p+2 doubles (16-byte box rows; the
+// hardware zero-fills coordinates outside the lattice).
+template <int P, bool TMA>
+struct Cut3SmemV3 {
+  static constexpr int N1 = P + 1, NB = N1 * N1 * N1, BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS * BS;
+  static constexpr int RS = TMA ? ((WS + 1) & ~1) : WS, PS = RS * WS;   // row / plane stride of the window
+  static constexpr int FJ = P * N1 * N1;
+  static constexpr int doubles = WS * PS + 36 * FJ + 8 * NB + MM + 1;
+  static constexpr size_t bytes = 128 + doubles * sizeof(double);
+};
+
+template <int P, int NT, bool TMA>
+__global__ void __launch_bounds__(NT) k_cut_colour3v3(const __grid_constant__ CUtensorMap tmx, LevelArgs L,
+                                                      const CutDesc3* desc, int np, const double* inv,
+                                                      const double* x, const double* b, double* zbuf) {
+  using S = Cut3SmemV3<P, TMA>;
+  constexpr int N1 = S::N1, NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, FJ = S::FJ, RS = S::RS, PS = S::PS;
+  __shared__ SmTab T;
+  __shared__ CutDesc3 d;
+  __shared__ unsigned long long gmask;
+  extern __shared__ __align__(128) unsigned char smraw3[];
+  uint64_t* bar = (uint64_t*)smraw3;
+  double* Wp = (double*)(smraw3 + 128);
+  double* Jm = Wp + WS * PS;        // [36 faces][P][N1][N1]
+  double* Yc = Jm + 36 * FJ;        // [8][NB]
+  double* Rr = Yc + 8 * NB;         // [MM]
+  const int lane = threadIdx.x;
+  pdl_trigger();
+  if ((int)blockIdx.x >= np) return;
+  load_smtab<P>(T);
+  if (lane == 0) {
+    d = desc[blockIdx.x];
+    gmask = 0ull;
+    if (TMA) mbar_init(bar, 1);
+  }
+  __syncthreads();
+  const int m = __popcll(d.mask[0]) + __popcll(d.mask[1]);
+  // setup-time data (element matrices of the cut cells, local inverse): start
+  // streaming it into L2 now, overlapping the previous kernel's tail (PDL)
+  if (lane < 8) {
+    if (d.cid[lane] >= 0) prefetch_l2(L.ecut + (size_t)d.cid[lane] * NB * NB, NB * NB * sizeof(double));
+  } else if (lane == 8) {
+    prefetch_l2(inv + d.inv_off, (size_t)m * m * sizeof(double));
+  }
+  pdl_wait();
+  if (TMA) {
+    if (lane == 0) {
+      mbar_expect_tx(bar, (unsigned)(RS * WS * WS * sizeof(double)));
+      tma_load_3d(Wp, &tmx, P * (d.I - 2), P * (d.J - 2), P * (d.K - 2), bar);
+    }
+  } else {
+    for (int e = lane; e < WS * WS * WS; e += NT) {
+      const int a = P * (d.I - 2) + e % WS, bb = P * (d.J - 2) + (e / WS) % WS, c = P * (d.K - 2) + e / (WS * WS);
+      const int o = (e / (WS * WS)) * PS + ((e / WS) % WS) * RS + e % WS;
+      if (a >= 0 && bb >= 0 && c >= 0 && a < L.nl && bb < L.nl && c < L.nl)
+        cp_async8(Wp + o, x + ((size_t)c * L.nl + bb) * L.ld + a);
+      else Wp[o] = 0.0;
+    }
+    cp_async_wait_all();
+  }
+  // residual rhs of the interior rows (independent of the window)
+  for (int loc = lane; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if (!((word >> (loc & 63)) & 1ull)) continue;
+    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    const int ra = loc % BS, rb = (loc / BS) % BS, rc = loc / (BS * BS);
+    Rr[i] = b[((size_t)(P * (d.K - 1) + rc) * L.nl + P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra];
+  }
+  if (TMA) mbar_wait(bar, 0);
+  __syncthreads();
+  // phase A: ghost-face moments (jobs < 36 P) and the cell parts of the
+  // per-(cell, row) outputs (the element-matrix loads overlap the face math)
+  for (int job = lane; job < 36 * P + 8 * NB; job += NT) {
+    if (job >= 36 * P) {
+      const int jr = job - 36 * P;
+      const int q = jr / NB, t = jr - q * NB;
+      const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+      const int kind = dkind3(d, dx + 1, dy + 1, dz + 1);
+      double y = 0.0;
+      if (kind != OUTSIDE) {
+        const int kx = t % N1, ky = (t / N1) % N1, kz = t / (N1 * N1);
+        const double* X = Wp + P * (dz + 1) * PS + P * (dy + 1) * RS + P * (dx + 1);
+        if (kind == INSIDE) {
+          y = inside_row3<P>(T, X, RS, PS, kx, ky, kz, L.h);
+        } else {
+          const double* Ec = L.ecut + (size_t)d.cid[q] * NB * NB + t;   // column t = row t (symmetric)
+#pragma unroll
+          for (int l = 0; l < NB; ++l) y = fma(__ldg(Ec + l * NB), X[(l / (N1 * N1)) * PS + ((l / N1) % N1) * RS + l % N1], y);
+        }
+      }
+      Yc[jr] = y;
+      continue;
+    }
+    const int f = job / P, k = job - f * P + 1;
+    const int axis = f / 12, s = (f / 4) % 3, t = f % 4;
+    const int ta = 1 + (t & 1), tb = 1 + (t >> 1);
+    const int w1x = axis == 0 ? s : ta, w1y = axis == 1 ? s : (axis == 0 ? ta : tb), w1z = axis == 2 ? s : tb;
+    const int w2x = w1x + (axis == 0), w2y = w1y + (axis == 1), w2z = w1z + (axis == 2);
+    const int k1 = dkind3(d, w1x, w1y, w1z), k2 = dkind3(d, w2x, w2y, w2z);
+    if (!(k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT))) continue;
+    if (k == 1) atomicOr(&gmask, 1ull << f);
+    double* out = Jm + f * FJ + (k - 1) * N1 * N1;
+    const int sn = axis == 0 ? 1 : (axis == 1 ? RS : PS);
+    const int s1 = axis == 0 ? RS : 1, s2 = axis == 2 ? RS : PS;
+    const double* X1 = Wp + P * w1z * PS + P * w1y * RS + P * w1x;
+    const double* X2 = X1 + P * sn;
+    double H[N1][N1];   // H[l1][q2] = sum_l2 M[q2][l2] J[l1][l2]
+#pragma unroll
+    for (int l1 = 0; l1 < N1; ++l1) {
+      double J[N1];
+#pragma unroll
+      for (int l2 = 0; l2 < N1; ++l2) {
+        double a = 0.0;
+        const int o = l1 * s1 + l2 * s2;
+#pragma unroll
+        for (int nn = 0; nn < N1; ++nn) a = fma(T.d1[k][nn], X1[o + nn * sn], fma(-T.d0[k][nn], X2[o + nn * sn], a));
+        J[l2] = a;
+      }
+#pragma unroll
+      for (int q2 = 0; q2 < N1; ++q2) {
+        double a = 0.0;
+#pragma unroll
+        for (int l2 = 0; l2 < N1; ++l2) a = fma(T.M[q2][l2], J[l2], a);
+        H[l1][q2] = a;
+      }
+    }
+#pragma unroll
+    for (int q1 = 0; q1 < N1; ++q1)
+#pragma unroll
+      for (int q2 = 0; q2 < N1; ++q2) {
+        double a = 0.0;
+#pragma unroll
+        for (int l1 = 0; l1 < N1; ++l1) a = fma(T.M[q1][l1], H[l1][q2], a);
+        out[q1 * N1 + q2] = a;
+      }
+  }
+  __syncthreads();
+  // phase B: interior rows gather the cell parts of their cells plus those
+  // cells' ghost-face terms; residual = b - A x on the interior
+  const unsigned long long gm = gmask;
+  for (int loc = lane; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if (!((word >> (loc & 63)) & 1ull)) continue;
+    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    const int ra = loc % BS, rb = (loc / BS) % BS, rc = loc / (BS * BS);
+    double y = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+      const int kx = ra - P * dx, ky = rb - P * dy, kz = rc - P * dz;
+      if (kx < 0 || kx > P || ky < 0 || ky > P || kz < 0 || kz > P) continue;
+      double yq = Yc[q * NB + (kz * N1 + ky) * N1 + kx];
+#pragma unroll
+      for (int axis = 0; axis < 3; ++axis) {
+        const int ka = axis == 0 ? kx : (axis == 1 ? ky : kz);
+        const int kt1 = axis == 0 ? ky : kx, kt2 = axis == 2 ? ky : kz;
+        const int da = axis == 0 ? dx : (axis == 1 ? dy : dz);
+        const int tt = axis == 0 ? dy + 2 * dz : (axis == 1 ? dx + 2 * dz : dx + 2 * dy);
+        const int flo = (axis * 3 + da) * 4 + tt, fhi = flo + 4;
+        if ((gm >> flo) & 1ull) {
+#pragma unroll
+          for (int k = 1; k <= P; ++k)
+            yq = fma(-L.gs[k] * T.d0[k][ka], Jm[flo * FJ + (k - 1) * N1 * N1 + kt1 * N1 + kt2], yq);
+        }
+        if ((gm >> fhi) & 1ull) {
+#pragma unroll
+          for (int k = 1; k <= P; ++k)
+            yq = fma(L.gs[k] * T.d1[k][ka], Jm[fhi * FJ + (k - 1) * N1 * N1 + kt1 * N1 + kt2], yq);
+        }
+      }
+      y += yq;
+    }
+    Rr[i] -= y;
+  }
+  __syncthreads();
+  const double* A = inv + d.inv_off;
+  for (int i = lane; i < m; i += NT) {
+    double z0 = 0.0, z1 = 0.0;
+    int q = 0;
+    for (; q + 1 < m; q += 2) {
+      z0 = fma(__ldg(A + (int64_t)q * m + i), Rr[q], z0);
+      z1 = fma(__ldg(A + (int64_t)(q + 1) * m + i), Rr[q + 1], z1);
+    }
+    if (q < m) z0 = fma(__ldg(A + (int64_t)q * m + i), Rr[q], z0);
+    zbuf[d.e0 + i] = z0 + z1;
+  }
+}
+
 }  // namespace cf

@@ -63,6 +63,7 @@ struct Problem {
   bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
   bool use_tma = true;      // TMA tile loads in the fused Cartesian sweep (env CUTFEM_TMA=0 disables)
   bool cta_cut = true;      // CTA of 64 threads per cut patch (env CUTFEM_CTACUT=0: one warp per patch)
+  int cut3_v = 3;           // 3D cut-patch kernel version (env CUTFEM_CUT3=2: lane-parallel jump array)
   bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
   // coarse
   int n0 = 0;
@@ -167,11 +168,6 @@ struct Problem {
 
   // ---------------------------------------------------------------- setup
   void setup_mesh() {
-    if (prm.dim == 3) {
-      setup_mesh3();
-      return;
-    }
-    host::upload_tables();
     if (const char* e = std::getenv("CUTFEM_PERSISTENT")) persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_FUSED")) fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_PDL")) pdl = std::atoi(e) != 0;
@@ -179,8 +175,14 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_PINGPONG")) pingpong = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TMA")) use_tma = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CTACUT")) cta_cut = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_CUT3")) cut3_v = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_PERSISTENT_BELOW")) persistent_below = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
+    if (prm.dim == 3) {
+      setup_mesh3();
+      return;
+    }
+    host::upload_tables();
     host::cart_map(prm.p);  // dense Cartesian patch map (p <= 3), built outside any graph capture
     d_count = alloc<int>(1);
     const int p = prm.p;
@@ -1188,6 +1190,26 @@ struct Problem {
     if (!np) return;
     const int base = D.cutp_off[c];
     if (prm.cut_mode == 0) {
+      if (cut3_v >= 3) {
+        CF_DISPATCH3(prm.p, {
+          const bool tma3 = use_tma && P == 2;
+          CUtensorMap tm;
+          std::memset(&tm, 0, sizeof(tm));
+          if (tma3) tm = host::lattice_tmap3(x, D.a.nl, D.a.ld, Cut3SmemV3<P, true>::RS, 4 * P + 1, 4 * P + 1);
+          static bool attr3 = false;
+          if (!attr3) {
+            CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v3<P, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v3<P, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr3 = true;
+          }
+          if (tma3)
+            launch(k_cut_colour3v3<P, 128, true>, dim3(np), dim3(128), Cut3SmemV3<P, true>::bytes, tm, D.a,
+                   (const CutDesc3*)D.desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
+          else
+            launch(k_cut_colour3v3<P, 128, false>, dim3(np), dim3(128), Cut3SmemV3<P, false>::bytes, tm, D.a,
+                   (const CutDesc3*)D.desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
+        });
+      } else
       CF_DISPATCH3(prm.p, {
         const size_t pw = Cut3Smem<P>::per_warp * sizeof(double);
         static bool attr = false;

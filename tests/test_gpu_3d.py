@@ -107,3 +107,21 @@ def test_transfer_vcycle_cg_3d(w):
     xo, ito, _ = o.solve_cg(bl[lf.dof_nodes], 1e-8, 100)
     assert it == ito and rel <= 1e-8
     assert rel_err(g.to_host(x)[lf.dof_nodes], xo) < 1e-7
+
+
+@pytest.mark.parametrize("env", [{"CUTFEM_CUT3": "2"}, {"CUTFEM_TMA": "0"}], ids=["cut3-v2", "cut3-no-tma"])
+def test_alternative_cut_kernels_3d(env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = CASES[2]
+    o, g = oracle(w), gpu(w)
+    l = len(o.levels) - 1
+    ld = o.levels[l]
+    dn = ld.lv.dof_nodes
+    xl, bl = rnd(w, 42, l), rnd(w, 43, l)
+    for c in range(8):
+        x = g.to_device(xl, l)
+        g.colour_step(l, 1, c, x, g.to_device(bl, l))
+        xo = xl[dn].copy()
+        ld.colour_step(xo, bl[dn], KIND[1], c)
+        assert rel_err(g.to_host(x, l)[dn], xo) < TOL, c
