@@ -23,10 +23,13 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, out=None, extra=()):
+    """Compile capi.cu into `out` (default: the in-tree library); `extra` =
+    additional nvcc flags (e.g. -D variants for A/B timing runs)."""
+    out = out or OUT
+    if out == OUT and not force and not needs_build():
         return OUT
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), SRC, "-o", OUT + ".tmp"]
+    cmd = [NVCC] + FLAGS + list(extra) + ["-I", os.path.join(ROOT, "include"), SRC, "-o", out + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr
     with open(os.path.join(HERE, "build.log"), "w") as f:
@@ -34,12 +37,17 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         sys.stderr.write(log[-8000:])
         raise RuntimeError("nvcc failed (see paper_2508_11608_b200/build.log)")
-    os.replace(OUT + ".tmp", OUT)
+    os.replace(out + ".tmp", out)
     if verbose:
         print(log)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(OUT)
+    args = [a for a in sys.argv[1:] if a not in ("--force", "-v")]
+    out = None
+    if "--out" in args:
+        i = args.index("--out")
+        out = args[i + 1]
+        del args[i:i + 2]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=out, extra=args))

@@ -40,6 +40,13 @@ extern "C" {
 const char* cutfem_last_error(void) { return g_err.c_str(); }
 int64_t cutfem_launch_count(void) { return cf::g_launches; }
 
+#ifdef CF_TIMING
+// debug builds only: copy the per-block phase timestamps of the last instrumented launch
+int cutfem_debug_timers(unsigned long long* host, int nblocks) {
+  return cudaMemcpyFromSymbol(host, g_dbg, sizeof(unsigned long long) * 8 * nblocks) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* out) {
   return guarded([&]() {
     cf::require(prm != nullptr && out != nullptr, cf::ERR_ARG, "null argument");

@@ -63,6 +63,12 @@ struct Problem {
   bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
   bool use_tma = true;      // TMA tile loads in the fused Cartesian sweep (env CUTFEM_TMA=0 disables)
   bool cta_cut = true;      // CTA of 64 threads per cut patch (env CUTFEM_CTACUT=0: one warp per patch)
+  // cut sweeps in one cluster launch when every colour has <= cluster_max cut
+  // patches (env CUTFEM_CLUSTER_MAX).  Off by default: measured no faster than
+  // one PDL launch per colour (the per-patch latency chain dominates either way)
+  int cluster_max = 0;
+  int cluster_size = 16;    // CTAs per cluster (non-portable 16; falls back to 8)
+  int cut2_v = 6;           // 2D CTA-per-patch cut step version (env CUTFEM_CUT2=4: six-barrier v4)
   int cut3_v = 3;           // 3D cut-patch kernel version (env CUTFEM_CUT3=2: lane-parallel jump array)
   bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
   // coarse
@@ -166,6 +172,26 @@ struct Problem {
     CF_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
   }
 
+  // launch as one thread-block cluster of `cs` CTAs (grid = cs), with PDL
+  template <typename... KArgs, typename... Args>
+  cudaError_t launch_cluster(void (*kern)(KArgs...), int cs, dim3 b, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+  }
+
   // ---------------------------------------------------------------- setup
   void setup_mesh() {
     if (const char* e = std::getenv("CUTFEM_PERSISTENT")) persistent = std::atoi(e) != 0;
@@ -176,6 +202,8 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_TMA")) use_tma = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CTACUT")) cta_cut = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT3")) cut3_v = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_CUT2")) cut2_v = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_CLUSTER_MAX")) cluster_max = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_PERSISTENT_BELOW")) persistent_below = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
     if (prm.dim == 3) {
@@ -708,6 +736,7 @@ struct Problem {
           static bool attr3 = false;
           if (!attr3) {
             CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+            CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
             attr3 = true;
           }
           launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tmx, tmb, D.a,
@@ -760,8 +789,25 @@ struct Problem {
           attr4 = true;
         }
         const int cb = ceil_div(ncopy, NT);
-        launch(k_cut_step4<P, NT>, dim3(np + cb), dim3(NT), smb, D.a, desc, np, np, (const double*)D.ecut,
-               (const double*)D.inv, R, W, b, cl, ncopy);
+        static bool attr5 = false;
+        if (!attr5) {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_step5<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          attr5 = true;
+        }
+        if (cut2_v >= 6) {
+          static bool attr6 = false;
+          if (!attr6) {
+            CF_CUDA(cudaFuncSetAttribute(k_cut_step6<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr6 = true;
+          }
+          launch(k_cut_step6<P, NT>, dim3(np + cb), dim3(NT), (size_t)CutGroup6<P>::bytes, D.a, desc, np,
+                 (const double*)D.ecut, (const double*)D.inv, R, W, b, cl, ncopy);
+        } else if (cut2_v >= 5)
+          launch(k_cut_step5<P, NT>, dim3(np + cb), dim3(NT), smb, D.a, desc, np, np, (const double*)D.ecut,
+                 (const double*)D.inv, R, W, b, cl, ncopy);
+        else
+          launch(k_cut_step4<P, NT>, dim3(np + cb), dim3(NT), smb, D.a, desc, np, np, (const double*)D.ecut,
+                 (const double*)D.inv, R, W, b, cl, ncopy);
       } else {
         const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
         const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
@@ -786,7 +832,56 @@ struct Problem {
 
   // the n_c sweeps over the cut colours with ping-pong buffers (x, xs); an
   // even number of steps (4 n_c) leaves the result in x
+  // all cut sweeps of a smoothing step in one cluster-resident launch
+  // (levels whose colours have at most cluster_max cut patches)
+  bool cut_sweeps_cluster(int l, double* x, const double* b, int reverse) {
+    LevelData& D = lv[l];
+    CutSweepArgs A;
+    A.L = D.a;
+    A.desc = (const CutDesc*)D.desc;
+    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.cutp_off[c];
+    A.copy = D.copy_lists;
+    for (int i = 0; i < 5; ++i)
+      for (int c = 0; c < 4; ++c) {
+        A.copy_off[i][c] = D.copy_off[i][c];
+        A.copy_n[i][c] = D.copy_n[i][c];
+      }
+    A.ecut = D.ecut;
+    A.inv = D.inv;
+    A.x = x;
+    A.xs = D.xs;
+    A.b = b;
+    A.n_c = prm.n_c;
+    A.reverse = reverse;
+    bool ok = false;
+    CF_DISPATCH(prm.p, {
+      constexpr int G = P <= 2 ? 8 : (P == 3 ? 4 : 2);
+      const size_t smb = (size_t)G * ((CutGroup6<P>::bytes + 127) & ~127);
+      static int cs_ok = 0;
+      if (!cs_ok) {
+        CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+        CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster<P, G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cs_ok = 1;
+      }
+      cudaError_t e = launch_cluster(k_cut_sweeps_cluster<P, G>, cluster_size, dim3(64 * G), smb, A);
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        require(cluster_size > 8, ERR_CUDA, "cluster launch of the cut sweeps failed");
+        cluster_size = 8;
+        CF_CUDA(launch_cluster(k_cut_sweeps_cluster<P, G>, cluster_size, dim3(64 * G), smb, A));
+      }
+      ok = true;
+    });
+    CF_LAUNCHED();
+    return ok;
+  }
+
   void cut_sweeps(int l, double* x, const double* b, int reverse) {
+    if (cluster_max > 0 && prm.cut_mode == 0 && cta_cut && (prm.n_c * 4) % 2 == 0) {
+      int npmax = 0;
+      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].n_cutp[c]);
+      if (npmax <= cluster_max && cut_sweeps_cluster(l, x, b, reverse)) return;
+    }
     double* bufs[2] = {x, lv[l].xs};
     int prev = 4, s = 0;
     for (int rep = 0; rep < prm.n_c; ++rep)

@@ -16,6 +16,27 @@
 
 #include "kernels.cuh"
 
+#ifdef CF_TIMING
+// debug-only phase timestamps (variant builds with -DCF_TIMING): [block][slot]
+__device__ unsigned long long g_dbg[8192][8];
+#define CF_TSTAMP(slot)                                                                        \
+  do {                                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 8192) {                                               \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      g_dbg[blockIdx.x][slot] = t_;                                                            \
+    }                                                                                          \
+  } while (0)
+#else
+#define CF_TSTAMP(slot) \
+  do {                  \
+  } while (0)
+#endif
+
+#ifndef CF_CART_MINB
+#define CF_CART_MINB 4   // resident CTAs per SM the fused Cartesian kernel is compiled for
+#endif
+
 namespace cf {
 
 struct __align__(16) CutDesc {
@@ -1010,7 +1031,7 @@ struct CartTmaSmem {
 };
 
 template <int P, int TC>
-__global__ void __launch_bounds__(256) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(256, CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* x, int reverse) {
@@ -1143,6 +1164,7 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
   __shared__ SmTab T;
   extern __shared__ double sm4[];
   const int tid = threadIdx.x;
+  CF_TSTAMP(0);
   pdl_trigger();
   if ((int)blockIdx.x >= patch_blocks) {
     const int e = (blockIdx.x - patch_blocks) * NT + tid;
@@ -1165,6 +1187,7 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
   if (tid == 0) sd = desc[blockIdx.x];
   load_smtab<P>(T);
   __syncthreads();
+  CF_TSTAMP(1);
   const CutDesc& d = sd;
   const int m = mask_count(d);
   const double* Ag = inv + d.inv_off;
@@ -1174,6 +1197,7 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
     if (d.cid[q] >= 0)
       for (int e = tid; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
   pdl_wait();
+  CF_TSTAMP(2);
   for (int e = tid; e < WS * WS; e += NT) {
     const int r = e / WS, c = e - r * WS;
     const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
@@ -1199,6 +1223,7 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
   }
   cp_async_wait_all();
   __syncthreads();
+  CF_TSTAMP(3);
   for (int job = tid; job < NJ; job += NT) {
     const int f = job / PP, rem = job - f * PP, k = rem / (P + 1) + 1, l = rem % (P + 1);
     int axis, w1x, w1y, w2x, w2y;
@@ -1264,6 +1289,7 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
     Rr[iidx[t]] = bv[t] - y;
   }
   __syncthreads();
+  CF_TSTAMP(4);
   for (int i = tid; i < m; i += NT) {
     double z = 0.0;
     for (int q = 0; q < m; ++q) z = fma(Ai[q * m + i], Rr[q], z);
@@ -1277,6 +1303,169 @@ __global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* de
     const int ra = loc % BS, rb = loc / BS;
     W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + zs[iidx[t]];
   }
+  CF_TSTAMP(5);
+}
+
+
+// v5: the v4 step with three barriers instead of six: (1) ghost-face jumps and
+// their M-moments computed in registers by one thread per (face, order)
+// together with the cell parts of the (cell, row) outputs, (2) the interior
+// rows gather their cells' outputs plus those cells' ghost-face terms (a
+// 12-bit ghost mask skips the others), (3) thread i applies row i of the
+// local inverse and writes its node directly.
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) k_cut_step5(LevelArgs L, const CutDesc* desc, int np, int patch_blocks,
+                                                  const double* ecut, const double* inv, const double* R, double* W,
+                                                  const double* b, const int32_t* copy, int ncopy) {
+  using S = CutSmem4<P>;
+  constexpr int NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, PP = P * (P + 1), N1 = P + 1;
+  __shared__ SmTab T;
+  __shared__ CutDesc sd;
+  __shared__ unsigned gmask;
+  __shared__ short Lc[MM];
+  extern __shared__ double sm5[];
+  const int tid = threadIdx.x;
+  CF_TSTAMP(0);
+  pdl_trigger();
+  if ((int)blockIdx.x >= patch_blocks) {
+    const int e = (blockIdx.x - patch_blocks) * NT + tid;
+    if (e < ncopy) {
+      const int32_t node = copy[e];
+      pdl_wait();
+      W[node] = R[node];
+    }
+    return;
+  }
+  double* Wp = sm5;
+  double* Jm = Wp + WS * WS;   // [12 faces][P][N1]
+  double* Yc = Jm + 12 * PP;   // [4][NB]
+  double* Rr = Yc + 4 * NB;    // [MM]
+  double* Ai = Rr + MM;        // [MM*MM]
+  double* Ec = Ai + MM * MM;   // [4][NB*NB]
+  if (tid == 0) {
+    sd = desc[blockIdx.x];
+    gmask = 0u;
+  }
+  load_smtab<P>(T);
+  __syncthreads();
+  CF_TSTAMP(1);
+  const CutDesc& d = sd;
+  const int m = mask_count(d);
+  const double* Ag = inv + d.inv_off;
+  for (int e = tid; e < m * m; e += NT) cp_async8(Ai + e, Ag + e);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (d.cid[q] >= 0)
+      for (int e = tid; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
+  pdl_wait();
+  CF_TSTAMP(2);
+  for (int e = tid; e < WS * WS; e += NT) {
+    const int r = e / WS, c = e - r * WS;
+    const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, R + (size_t)bb * L.ld + a);
+    else Wp[e] = 0.0;
+  }
+  for (int loc = tid; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if ((word >> (loc & 63)) & 1ull) {
+      const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+      Lc[i] = (short)loc;
+      Rr[i] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  CF_TSTAMP(3);
+  // (1) face moments and cell parts
+  for (int job = tid; job < 12 * P + 4 * NB; job += NT) {
+    if (job >= 12 * P) {
+      const int jr = job - 12 * P, q = jr / NB, t = jr - q * NB;
+      const int dx = q & 1, dy = q >> 1, kx = t % N1, ky = t / N1;
+      const int kind = desc_kind(d, dx + 1, dy + 1);
+      double y = 0.0;
+      if (kind != OUTSIDE) {
+        const double* X = Wp + (P * (dy + 1)) * WS + P * (dx + 1);
+        if (kind == INSIDE) {
+          y = inside_row<P>(T, X, WS, kx, ky);
+        } else {
+          const double* Er = Ec + q * NB * NB + t * NB;
+#pragma unroll
+          for (int l = 0; l < NB; ++l) y = fma(Er[l], X[(l / N1) * WS + l % N1], y);
+        }
+      }
+      Yc[jr] = y;
+      continue;
+    }
+    const int f = job / P, k = job - f * P + 1;
+    int axis, w1x, w1y, w2x, w2y;
+    face_cells(f, axis, w1x, w1y, w2x, w2y);
+    const int k1 = desc_kind(d, w1x, w1y), k2 = desc_kind(d, w2x, w2y);
+    if (!(k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT))) continue;
+    if (k == 1) atomicOr(&gmask, 1u << f);
+    const double* X1 = Wp + (P * w1y) * WS + P * w1x;
+    const double* X2 = Wp + (P * w2y) * WS + P * w2x;
+    const int sn = axis == 0 ? 1 : WS, st = axis == 0 ? WS : 1;
+    double J[N1];
+#pragma unroll
+    for (int l = 0; l < N1; ++l) {
+      double a = 0.0;
+#pragma unroll
+      for (int nn = 0; nn <= P; ++nn) a = fma(T.d1[k][nn], X1[l * st + nn * sn], fma(-T.d0[k][nn], X2[l * st + nn * sn], a));
+      J[l] = a;
+    }
+#pragma unroll
+    for (int q = 0; q < N1; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < N1; ++l) a = fma(T.M[q][l], J[l], a);
+      Jm[f * PP + (k - 1) * N1 + q] = a;
+    }
+  }
+  __syncthreads();
+  CF_TSTAMP(4);
+  // (2) residual on the interior rows
+  const unsigned gm = gmask;
+  for (int i = tid; i < m; i += NT) {
+    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
+    double y = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int dx = q & 1, dy = q >> 1;
+      const int kx = ra - P * dx, ky = rb - P * dy;
+      if (kx < 0 || kx > P || ky < 0 || ky > P) continue;
+      double yq = Yc[q * NB + ky * N1 + kx];
+      const int fl = 2 * dx + dy, fr = 2 * (dx + 1) + dy, fb = 6 + 2 * dy + dx, ft = 6 + 2 * (dy + 1) + dx;
+      if ((gm >> fl) & 1u)
+#pragma unroll
+        for (int kk = 1; kk <= P; ++kk) yq = fma(-L.gs[kk] * T.d0[kk][kx], Jm[fl * PP + (kk - 1) * N1 + ky], yq);
+      if ((gm >> fr) & 1u)
+#pragma unroll
+        for (int kk = 1; kk <= P; ++kk) yq = fma(L.gs[kk] * T.d1[kk][kx], Jm[fr * PP + (kk - 1) * N1 + ky], yq);
+      if ((gm >> fb) & 1u)
+#pragma unroll
+        for (int kk = 1; kk <= P; ++kk) yq = fma(-L.gs[kk] * T.d0[kk][ky], Jm[fb * PP + (kk - 1) * N1 + kx], yq);
+      if ((gm >> ft) & 1u)
+#pragma unroll
+        for (int kk = 1; kk <= P; ++kk) yq = fma(L.gs[kk] * T.d1[kk][ky], Jm[ft * PP + (kk - 1) * N1 + kx], yq);
+      y += yq;
+    }
+    Rr[i] -= y;
+  }
+  __syncthreads();
+  CF_TSTAMP(5);
+  // (3) z = A_j^{-1} r, written to the interior nodes
+  for (int i = tid; i < m; i += NT) {
+    double z0 = 0.0, z1 = 0.0;
+    int q = 0;
+    for (; q + 1 < m; q += 2) {
+      z0 = fma(Ai[q * m + i], Rr[q], z0);
+      z1 = fma(Ai[(q + 1) * m + i], Rr[q + 1], z1);
+    }
+    if (q < m) z0 = fma(Ai[q * m + i], Rr[q], z0);
+    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
+    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + (z0 + z1);
+  }
+  CF_TSTAMP(6);
 }
 
 }  // namespace cf
@@ -1360,6 +1549,305 @@ __global__ void __launch_bounds__(256) k_apply_tile(const __grid_constant__ CUte
   if (i0 + TX >= n)
     for (int bb = P * j0 + tid; bb < bhi; bb += 256)
       for (int a = L.nl; a < L.ld; ++a) y[(size_t)bb * L.ld + a] = 0.0;
+}
+
+
+// ---- v6: one cut-patch step as a device routine for a group of NT threads
+// (a whole CTA, or one of several groups of a cluster-resident CTA, with its
+// own named barrier `bar`).  Four barriers: (1) ghost-face jumps + moments
+// (registers) and the cell parts of the (cell, row) outputs; (2) the ghost
+// terms of each (cell, row) output; (3) gather of the interior rows and the
+// residual; (4) z = A_j^{-1} r written to the interior nodes of W.
+template <int P>
+struct CutGroup6 {
+  static constexpr int NB = (P + 1) * (P + 1), BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, PP = P * (P + 1);
+  // doubles: window, face moments, cell outputs, residual, inverse, element matrices
+  static constexpr int doubles = WS * WS + 12 * PP + 4 * NB + MM + MM * MM + 4 * NB * NB;
+  static constexpr int bytes = doubles * 8 + 128 + 2 * MM + 8;   // + descriptor, interior locations, ghost mask
+};
+
+__device__ __forceinline__ void group_sync(int bar, int nt) { asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(nt) : "memory"); }
+
+// prologue (independent of the previous step): descriptor, inverse and
+// element matrices by cp.async.  Returns after the descriptor is visible.
+template <int P, int NT>
+__device__ __forceinline__ void cut6_prologue(const CutDesc* desc, int k, const double* ecut, const double* inv,
+                                              unsigned char* gsm, int gt, int bar) {
+  using S = CutGroup6<P>;
+  constexpr int NB = S::NB, WS = S::WS, MM = S::MM, PP = S::PP;
+  CutDesc& d = *(CutDesc*)gsm;
+  double* Wp = (double*)(gsm + 128);
+  double* Ai = Wp + WS * WS + 12 * PP + 4 * NB + MM;
+  double* Ec = Ai + MM * MM;
+  if (gt < (int)(sizeof(CutDesc) / 16)) ((int4*)&d)[gt] = ((const int4*)(desc + k))[gt];
+  group_sync(bar, NT);
+  const int m = mask_count(d);
+  const double* Ag = inv + d.inv_off;
+  for (int e = gt; e < m * m; e += NT) cp_async8(Ai + e, Ag + e);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (d.cid[q] >= 0)
+      for (int e = gt; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
+}
+
+// main part (after the previous step's W is visible)
+template <int P, int NT>
+__device__ __forceinline__ void cut6_main(const LevelArgs& L, const SmTab& T, const double* R, double* W,
+                                          const double* b, unsigned char* gsm, int gt, int bar) {
+  using S = CutGroup6<P>;
+  constexpr int NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, PP = S::PP, N1 = P + 1;
+  const CutDesc& d = *(const CutDesc*)gsm;
+  double* Wp = (double*)(gsm + 128);
+  double* Jm = Wp + WS * WS;
+  double* Yc = Jm + 12 * PP;
+  double* Rr = Yc + 4 * NB;
+  double* Ai = Rr + MM;
+  double* Ec = Ai + MM * MM;
+  short* Lc = (short*)(Ec + 4 * NB * NB);
+  unsigned* gmask = (unsigned*)(Lc + MM + (MM & 1));
+  const int m = mask_count(d);
+  if (gt == 0) *gmask = 0u;
+  for (int e = gt; e < WS * WS; e += NT) {
+    const int r = e / WS, c = e - r * WS;
+    const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, R + (size_t)bb * L.ld + a);
+    else Wp[e] = 0.0;
+  }
+  for (int loc = gt; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if ((word >> (loc & 63)) & 1ull) {
+      const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+      Lc[i] = (short)loc;
+      Rr[i] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
+    }
+  }
+  cp_async_wait_all();
+  group_sync(bar, NT);
+  // (1) cell parts (jobs < 4 NB) and ghost-face moments
+  for (int job = gt; job < 4 * NB + 12 * P; job += NT) {
+    if (job < 4 * NB) {
+      const int q = job / NB, t = job - q * NB;
+      const int dx = q & 1, dy = q >> 1, kx = t % N1, ky = t / N1;
+      const int kind = desc_kind(d, dx + 1, dy + 1);
+      double y = 0.0;
+      if (kind != OUTSIDE) {
+        const double* X = Wp + (P * (dy + 1)) * WS + P * (dx + 1);
+        if (kind == INSIDE) {
+          y = inside_row<P>(T, X, WS, kx, ky);
+        } else {
+          const double* Er = Ec + q * NB * NB + t * NB;
+          double y1 = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int l = 0; l < NB; l += 3) {
+            y = fma(Er[l], X[(l / N1) * WS + l % N1], y);
+            if (l + 1 < NB) y1 = fma(Er[l + 1], X[((l + 1) / N1) * WS + (l + 1) % N1], y1);
+            if (l + 2 < NB) y2 = fma(Er[l + 2], X[((l + 2) / N1) * WS + (l + 2) % N1], y2);
+          }
+          y += y1 + y2;
+        }
+      }
+      Yc[job] = y;
+      continue;
+    }
+    const int jf = job - 4 * NB, f = jf / P, k = jf - f * P + 1;
+    int axis, w1x, w1y, w2x, w2y;
+    face_cells(f, axis, w1x, w1y, w2x, w2y);
+    const int k1 = desc_kind(d, w1x, w1y), k2 = desc_kind(d, w2x, w2y);
+    if (!(k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT))) continue;
+    if (k == 1) atomicOr(gmask, 1u << f);
+    const double* X1 = Wp + (P * w1y) * WS + P * w1x;
+    const double* X2 = Wp + (P * w2y) * WS + P * w2x;
+    const int sn = axis == 0 ? 1 : WS, st = axis == 0 ? WS : 1;
+    double J[N1];
+#pragma unroll
+    for (int l = 0; l < N1; ++l) {
+      double a1 = 0.0, a2 = 0.0;
+#pragma unroll
+      for (int nn = 0; nn <= P; ++nn) {
+        a1 = fma(T.d1[k][nn], X1[l * st + nn * sn], a1);
+        a2 = fma(T.d0[k][nn], X2[l * st + nn * sn], a2);
+      }
+      J[l] = a1 - a2;
+    }
+#pragma unroll
+    for (int q = 0; q < N1; ++q) {
+      double a = 0.0;
+#pragma unroll
+      for (int l = 0; l < N1; ++l) a = fma(T.M[q][l], J[l], a);
+      Jm[f * PP + (k - 1) * N1 + q] = a;
+    }
+  }
+  group_sync(bar, NT);
+  // (2) ghost terms of the (cell, row) outputs
+  const unsigned gm = *gmask;
+  if (gm)
+    for (int job = gt; job < 4 * NB; job += NT) {
+      const int q = job / NB, t = job - q * NB;
+      const int dx = q & 1, dy = q >> 1, kx = t % N1, ky = t / N1;
+      const int fl = 2 * dx + dy, fr = 2 * (dx + 1) + dy, fb = 6 + 2 * dy + dx, ft = 6 + 2 * (dy + 1) + dx;
+      if (!(gm & ((1u << fl) | (1u << fr) | (1u << fb) | (1u << ft)))) continue;
+      double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+      for (int kk = 1; kk <= P; ++kk) {
+        const double gk = L.gs[kk];
+        if ((gm >> fl) & 1u) y0 = fma(-gk * T.d0[kk][kx], Jm[fl * PP + (kk - 1) * N1 + ky], y0);
+        if ((gm >> fr) & 1u) y1 = fma(gk * T.d1[kk][kx], Jm[fr * PP + (kk - 1) * N1 + ky], y1);
+        if ((gm >> fb) & 1u) y0 = fma(-gk * T.d0[kk][ky], Jm[fb * PP + (kk - 1) * N1 + kx], y0);
+        if ((gm >> ft) & 1u) y1 = fma(gk * T.d1[kk][ky], Jm[ft * PP + (kk - 1) * N1 + kx], y1);
+      }
+      Yc[job] += y0 + y1;
+    }
+  group_sync(bar, NT);
+  // (3) residual on the interior rows
+  for (int i = gt; i < m; i += NT) {
+    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
+    double y = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kx = ra - P * (q & 1), ky = rb - P * (q >> 1);
+      if (kx >= 0 && kx <= P && ky >= 0 && ky <= P) y += Yc[q * NB + ky * N1 + kx];
+    }
+    Rr[i] -= y;
+  }
+  group_sync(bar, NT);
+  // (4) z = A_j^{-1} r on the interior nodes
+  for (int i = gt; i < m; i += NT) {
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+    int q = 0;
+    for (; q + 3 < m; q += 4) {
+      z0 = fma(Ai[q * m + i], Rr[q], z0);
+      z1 = fma(Ai[(q + 1) * m + i], Rr[q + 1], z1);
+      z2 = fma(Ai[(q + 2) * m + i], Rr[q + 2], z2);
+      z3 = fma(Ai[(q + 3) * m + i], Rr[q + 3], z3);
+    }
+    for (; q < m; ++q) z0 = fma(Ai[q * m + i], Rr[q], z0);
+    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
+    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + ((z0 + z1) + (z2 + z3));
+  }
+}
+
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) k_cut_step6(LevelArgs L, const CutDesc* desc, int np, const double* ecut,
+                                                  const double* inv, const double* R, double* W, const double* b,
+                                                  const int32_t* copy, int ncopy) {
+  __shared__ SmTab T;
+  extern __shared__ __align__(128) unsigned char sm6[];
+  const int tid = threadIdx.x;
+  CF_TSTAMP(0);
+  pdl_trigger();
+  if ((int)blockIdx.x >= np) {
+    const int e = (blockIdx.x - np) * NT + tid;
+    if (e < ncopy) {
+      const int32_t node = copy[e];
+      pdl_wait();
+      W[node] = R[node];
+    }
+    return;
+  }
+  load_smtab<P>(T);
+  cut6_prologue<P, NT>(desc, blockIdx.x, ecut, inv, sm6, tid, 0);
+  CF_TSTAMP(1);
+  pdl_wait();
+  CF_TSTAMP(2);
+  cut6_main<P, NT>(L, T, R, W, b, sm6, tid, 0);
+  CF_TSTAMP(3);
+}
+
+// ---- all n_c x 4 cut colour steps of one smoothing step in ONE launch: a
+// cluster of CS CTAs, each with G groups of 64 threads (one patch per group
+// at a time); the ping-pong steps are separated by cluster barriers
+// (barrier.cluster arrive.release / wait.acquire orders the global-memory
+// writes of one step before the reads of the next), which replaces a kernel
+// boundary on levels whose colours have at most a few hundred cut patches.
+struct CutSweepArgs {
+  LevelArgs L;
+  const CutDesc* desc;
+  int cut_off[5];           // patches of colour c: [cut_off[c], cut_off[c+1])
+  const int32_t* copy;      // copy lists N_prev \ N_cur
+  int copy_off[5][4], copy_n[5][4];
+  const double* ecut;
+  const double* inv;
+  double* x;                // in: x; out: x (even step count) or xs
+  double* xs;
+  const double* b;
+  int n_c, reverse;
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctas() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+template <int P, int G>
+__global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster(CutSweepArgs A) {
+  using S = CutGroup6<P>;
+  __shared__ SmTab T;
+  extern __shared__ __align__(128) unsigned char smc[];
+  const int tid = threadIdx.x, grp = tid >> 6, gt = tid & 63;
+  const int cr = (int)cluster_rank(), cs = (int)cluster_nctas();
+  unsigned char* gsm = smc + (size_t)grp * ((S::bytes + 127) & ~127);
+  CF_TSTAMP(0);
+  pdl_trigger();
+  // stream this level's setup data (descriptors, inverses, element matrices)
+  // into L2 while the first step starts
+  if (tid == 0) {
+    const int np = A.cut_off[4];
+    const size_t dsz = (size_t)np * sizeof(CutDesc), chunk = (dsz + cs - 1) / cs;
+    if (chunk && cr * chunk < dsz) prefetch_l2((const char*)A.desc + cr * chunk, min(chunk, dsz - cr * chunk));
+  }
+  load_smtab<P>(T);
+  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
+  auto first_patch = [&](int s) { return cr * G + grp; };   // round-0 patch index of this group in step s
+  // prologue of step 0 (independent of x)
+  {
+    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c], k = first_patch(0);
+    if (k < np) cut6_prologue<P, 64>(A.desc, A.cut_off[c] + k, A.ecut, A.inv, gsm, gt, 1 + grp);
+  }
+  __syncthreads();
+  pdl_wait();
+  CF_TSTAMP(1);
+  double* bufs[2] = {A.x, A.xs};
+  int prev = 4;
+  const int nsteps = A.n_c * 4;
+  for (int s = 0; s < nsteps; ++s) {
+    const int c = step_colour(s);
+    const double* R = bufs[s & 1];
+    double* W = bufs[(s + 1) & 1];
+    // copy list of this step (W <- R on N_prev \ N_c)
+    const int nco = A.copy_n[prev][c];
+    const int32_t* cl = A.copy + A.copy_off[prev][c];
+    for (int e = cr * 64 * G + tid; e < nco; e += cs * 64 * G) W[cl[e]] = R[cl[e]];
+    // the patches of colour c, one per group per round (round 0's prologue
+    // was issued before the previous barrier)
+    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
+    const int rounds = (np + cs * G - 1) / (cs * G);
+    for (int r = 0; r < rounds; ++r) {
+      const int k = (r * cs + cr) * G + grp;
+      if (k < np) {
+        if (r > 0) cut6_prologue<P, 64>(A.desc, p0 + k, A.ecut, A.inv, gsm, gt, 1 + grp);
+        cut6_main<P, 64>(A.L, T, R, W, A.b, gsm, gt, 1 + grp);
+        group_sync(1 + grp, 64);   // the group's shared buffers are reused next
+      }
+    }
+    // prologue of the next step's round-0 patch, overlapping the barrier
+    if (s + 1 < nsteps) {
+      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn], kn = first_patch(s + 1);
+      if (kn < npn) cut6_prologue<P, 64>(A.desc, A.cut_off[cn] + kn, A.ecut, A.inv, gsm, gt, 1 + grp);
+    }
+    prev = c;
+    cluster_sync_all();
+    if (s < 5) CF_TSTAMP(2 + s);
+  }
+  CF_TSTAMP(7);
 }
 
 }  // namespace cf

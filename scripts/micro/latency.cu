@@ -28,6 +28,13 @@ __global__ void k_grid(double* x, int iters) {
   }
 }
 
+__global__ void k_cl_chain(double* x, int pdl) {
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;");
+  if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) x[blockIdx.x] += 1.0;
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 int main() {
   double* x;
   cudaMalloc(&x, 1 << 20);
@@ -65,6 +72,44 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       printf("chain grid=%d pdl=%d: %.2f us per launch\n", grid, pdl, ms * 1e3 / 1000);
     }
+  cudaFuncSetAttribute(k_cl_chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_cl_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  for (int cs : {8, 16})
+    for (int smem : {0, 80 * 1024})
+      for (int pdl = 0; pdl < 2; ++pdl) {
+        cudaGraph_t gr;
+        cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
+        for (int i = 0; i < 200; ++i) {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = cs;
+          cfg.blockDim = 512;
+          cfg.dynamicSmemBytes = smem;
+          cfg.stream = s;
+          cudaLaunchAttribute at[2];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = cs;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[1].val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1 + pdl;
+          cudaLaunchKernelEx(&cfg, k_cl_chain, x, pdl);
+        }
+        cudaStreamEndCapture(s, &gr);
+        cudaGraphExec_t ge;
+        cudaGraphInstantiate(&ge, gr, 0);
+        cudaGraphLaunch(ge, s);
+        cudaStreamSynchronize(s);
+        cudaEventRecord(a, s);
+        for (int r = 0; r < 5; ++r) cudaGraphLaunch(ge, s);
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("cluster chain cs=%d smem=%d pdl=%d: %.2f us per launch (%s)\n", cs, smem, pdl, ms * 1e3 / 1000,
+               cudaGetErrorString(cudaGetLastError()));
+      }
   {
     cudaFuncSetAttribute(k_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     k_cluster<<<16, 1024, 0, s>>>(x, 10);

@@ -48,8 +48,10 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
 
 @pytest.mark.parametrize("env", [{"CUTFEM_MMA": "0"}, {"CUTFEM_FUSED": "0"}, {"CUTFEM_PINGPONG": "0"},
                                  {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}, {"CUTFEM_CTACUT": "0"},
-                                 {"CUTFEM_TILEAPPLY": "0"}],
-                         ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply"])
+                                 {"CUTFEM_TILEAPPLY": "0"}, {"CUTFEM_CUT2": "4", "CUTFEM_CLUSTER_MAX": "0"},
+                                 {"CUTFEM_CUT2": "5", "CUTFEM_CLUSTER_MAX": "0"}, {"CUTFEM_CLUSTER_MAX": "512"}],
+                         ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply",
+                              "cut-step-v4", "cut-step-v5", "cluster-cut-sweeps"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
