@@ -7,8 +7,9 @@ CG+MG time-to-solution.
 
 Prints ONE JSON line (rank 0).  `value` = active DoFs x steps x ranks / max
 over ranks of the device time of the timed steps (CUDA events on the
-launching stream, L2 flushed between timed steps).  N > 1 runs independent
-replicas (one problem per GPU, no data-path collective; DESIGN.md
+launching stream, L2 flushed between timed steps).  N > 1 partitions the
+same background mesh into N slabs, one per GPU, with NCCL halo exchanges
+after every colour sweep and residual (strong scaling; DESIGN.md
 "Multi-GPU").  `--impl reference` times the CPU oracle (as it stands) on a
 bounded sample of the same workload.
 """
@@ -34,7 +35,7 @@ WORKLOAD = workloads.CONFIG1
 ORACLE_SAMPLE_LEVEL = 6           # 128 x 128 cells of the same hierarchy (bounded CPU sample)
 
 
-from paper_2508_11608_b200.dist import max_over_ranks, rank_env, replica_throughput  # noqa: E402
+from paper_2508_11608_b200.dist import max_over_ranks, rank_env, strong_throughput  # noqa: E402
 
 
 def dist_env():
@@ -153,6 +154,9 @@ def main():
 
     w = WORKLOAD
     g = cutfem.Problem.from_workload(w)
+    if world > 1:   # slab partition of the mesh over the ranks (NCCL halo exchanges inside the library)
+        g.partition(cutfem.Comm.nccl_from_torch(dist))
+        args.no_3d = True
     L = w.n_levels - 1
     info = g.level_info(L)
     nl, ld = info.nl, info.ld
@@ -195,23 +199,24 @@ def main():
     total_ms = max_over_ranks(float(sum(ms)), dist, "cuda")
     if dist:
         dist.barrier()
-    value = replica_throughput(n_dofs, args.steps, world, total_ms)
+    value = strong_throughput(n_dofs, args.steps, total_ms)
 
     # ---- kernels of the step, timed alone (live, CUDA events, L2 flushed)
     p = w.p
     peak, peak_src = measured_peak_hbm()
-    cart_ms = float(np.mean(timed(lambda: g.colour_step(L, 2, 0, x, b), 50, 3)))
-    cart_bytes = 24.0 * p * p * info.n_inside
+    # (N > 1: the rank's sweeps incl. their halo exchanges; bytes = the slab's share, global / N)
+    cart_ms = max_over_ranks(float(np.mean(timed(lambda: g.colour_step(L, 2, 0, x, b), 50, 3))), dist, "cuda")
+    cart_bytes = 24.0 * p * p * info.n_inside / world
     off, _ = g.cut_interior(L)
     m_all = np.diff(off).astype(np.float64)
     nb = (p + 1) ** 2
     n_cut_launch = 4 * w.n_c
-    sweeps_ms = float(np.mean(timed(lambda: g.colour_step(L, 3, 0, x, b), 50, 3)))
+    sweeps_ms = max_over_ranks(float(np.mean(timed(lambda: g.colour_step(L, 3, 0, x, b), 50, 3))), dist, "cuda")
     cut_ms = sweeps_ms / n_cut_launch
     # per cut step (one colour): 8 m^2 (inverse) + 8 (2p+1)^2 (x block) + 8 m (b) + 16 m (x read, x write)
     # per patch, + 8 ((p+1)^2)^2 per cut cell (element matrix); averaged over the colours
     cut_bytes = (float(np.sum(8 * m_all * m_all + 8 * (2 * p + 1) ** 2 + 24 * m_all)) +
-                 8.0 * nb * nb * info.n_cut) / 4.0
+                 8.0 * nb * nb * info.n_cut) / 4.0 / world
     per_step = {"cart_sweep": cart_ms, "cut_sweeps": sweeps_ms}
     kernels = {
         "k_cart_fused_tma (4 Cartesian colours, one launch)": {
@@ -247,7 +252,8 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
         t_cg.append(t0.elapsed_time(t1))
-    cg_ms = float(np.median(t_cg))
+    cg_ms = max_over_ranks(float(np.median(t_cg)), dist, "cuda")
+    v_ms = max_over_ranks(v_ms, dist, "cuda")
 
     # ---- e2e: the same smoothing step through the C ABI with pinned host buffers
     xh = torch.empty(nl * ld, dtype=torch.float64).pin_memory()
@@ -261,9 +267,9 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         g.smooth_host(L, xn, bn)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e = {"value": n_dofs * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * nl * ld * 8,
-           "d2h_bytes_per_step": nl * ld * 8}
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, dist, "cuda")
+    e2e = {"value": n_dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * nl * ld * 8 * world,
+           "d2h_bytes_per_step": nl * ld * 8 * world}
 
     # ---- BASELINE configs[2]: 3D sphere, Q2, 128^3 (secondary line, same timing rules)
     cfg3 = None
@@ -300,18 +306,19 @@ def main():
 
     if rank == 0:
         cb = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             cb, _ = oracle_sample(2)
             cb["cores"] = 1
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded N(0,1) x0 and b on the lattice; analytic circle level set)",
             "config": {"workload": w.name, "box": [w.x0, w.x0 + w.length], "circle_r": w.r, "degree": w.p,
                        "cells_per_side": info.n, "levels": w.n_levels, "n_dofs": int(n_dofs), "n_c": w.n_c,
                        "l2": "flushed (512 MB write) before every timed step",
-                       "parallelism": "replicas" if world > 1 else "single GPU"},
+                       "parallelism": f"slab{world} (NCCL halo exchange per colour sweep / residual)"
+                       if world > 1 else "single GPU"},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -150,6 +150,48 @@ int cutfem_solve_cg_mg_host(cutfem_problem pb, double* x_host, const double* b_h
 int cutfem_prolongate_add(cutfem_problem pb, int level, const double* x_coarse, double* x_fine, void* stream);
 int cutfem_restrict(cutfem_problem pb, int level, const double* r_fine, double* b_coarse, void* stream);
 
+/* ---- slab partition over ranks (north_star: "the background mesh is
+ * partitioned into slabs across the GPUs ... halo exchange per colour sweep
+ * and per residual, coarse-grid solve on one rank") --
+ *
+ * A communicator endpoint is one rank's view of a group.  cutfem_partition
+ * attaches it to a built 2D problem, which takes ownership of it.  Rank r of W
+ * then owns the cell rows [r s, (r+1) s), s = n/W, of every level whose slab
+ * is a whole number of fused Cartesian tiles and thicker than the halo, from
+ * the finest level down; the remaining coarse levels (incl. the exact coarse
+ * solve) are computed redundantly by every rank after one all-reduce of the
+ * restricted residual.  Vectors stay full-size lattice vectors on every rank;
+ * only the rank's rows are meaningful:
+ *  - cutfem_smooth / cutfem_vcycle: x and b valid on the rows [v0, v1)
+ *    (owned rows + halo, cutfem_partition_info); x is valid there on return.
+ *  - cutfem_apply_operator: x valid on [v0, v1); y valid on the owned rows.
+ *  - cutfem_solve_cg_mg(_host): b valid on the owned rows; x valid on the
+ *    owned rows on return; iteration counts and residuals identical on all ranks.
+ * Every rank must make the same sequence of calls (the exchanges pair up).
+ * cutfem_colour_step: only kinds 2 and 3 (with their halo exchanges) on
+ * partitioned levels. */
+typedef struct cutfem_comm_s* cutfem_comm;
+#define CUTFEM_NCCL_ID_BYTES 128
+
+/* `world` endpoints of an in-process group (ranks = host threads of this
+ * process sharing one device; halo rows copied device-to-device).  The
+ * single-GPU harness of the decomposition. */
+int cutfem_comm_local_create(int world, cutfem_comm* out /* [world] */);
+/* NCCL (libnccl.so.2, loaded at first use): rank 0 creates the unique id, the
+ * caller broadcasts its CUTFEM_NCCL_ID_BYTES bytes, every rank then calls
+ * cutfem_comm_nccl_create (collective, blocking) on its own device. */
+int cutfem_comm_nccl_unique_id(unsigned char* id_out);
+int cutfem_comm_nccl_create(const unsigned char* id, int rank, int world, cutfem_comm* out);
+/* destroys an endpoint that was not attached to a problem */
+int cutfem_comm_destroy(cutfem_comm comm);
+int cutfem_partition(cutfem_problem pb, cutfem_comm comm);
+/* out[7] = {partitioned, r0, r1, v0, v1, rank, world}: owned lattice rows
+ * [r0, r1) and valid rows [v0, v1) of `level` (the whole lattice if the level
+ * is not partitioned) */
+int cutfem_partition_info(cutfem_problem pb, int level, int* out);
+/* exchange the halo rows of a lattice vector of `level` with the neighbours */
+int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream);
+
 /* ---- export (host copies, blocking; used by the parity tests) ---------- */
 
 /* cell types [j*n + i]: 0 outside, 1 inside, 2 cut */

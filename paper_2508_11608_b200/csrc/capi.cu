@@ -9,6 +9,10 @@ struct cutfem_problem_s {
   cf::Problem p;
 };
 
+struct cutfem_comm_s {
+  cf::Comm* c;
+};
+
 static thread_local std::string g_err;
 
 template <class F>
@@ -153,6 +157,8 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
     check_built(pb);
     check_level(pb, level);
     cf::require(kind >= 0 && kind <= 3 && colour >= 0 && colour < 8, cf::ERR_ARG, "bad kind/colour");
+    cf::require(!pb->p.lv[level].part || (pb->p.prm.dim == 2 && kind >= 2), cf::ERR_STATE,
+                "a partitioned level only exposes the whole sweeps (kind 2, 3)");
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
     if (pb->p.prm.dim == 3) {
@@ -170,6 +176,77 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
       pb->p.cut_pp_step(level, colour, -1, D.xs, x, b);
     } else if (kind == 1) pb->p.cut_step(level, colour, x, b);
     else pb->p.cart_fused(level, x, b, colour & 1);
+  });
+}
+
+int cutfem_comm_local_create(int world, cutfem_comm* out) {
+  return guarded([&]() {
+    cf::require(world >= 1 && out != nullptr, cf::ERR_ARG, "world must be >= 1, out non-null");
+    auto* hub = new cf::LocalHub(world);
+    for (int r = 0; r < world; ++r) out[r] = new cutfem_comm_s{new cf::LocalComm(hub, r)};
+  });
+}
+
+int cutfem_comm_nccl_unique_id(unsigned char* id_out) {
+  return guarded([&]() {
+    cf::require(id_out != nullptr, cf::ERR_ARG, "null output");
+    static_assert(sizeof(ncclUniqueId) == CUTFEM_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    CF_NCCL(cf::nccl_api().GetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int cutfem_comm_nccl_create(const unsigned char* id, int rank, int world, cutfem_comm* out) {
+  return guarded([&]() {
+    cf::require(id != nullptr && out != nullptr, cf::ERR_ARG, "null argument");
+    cf::require(world >= 1 && rank >= 0 && rank < world, cf::ERR_ARG, "bad rank / world");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    *out = new cutfem_comm_s{new cf::NcclComm(uid, rank, world)};
+  });
+}
+
+int cutfem_comm_destroy(cutfem_comm comm) {
+  return guarded([&]() {
+    if (!comm) return;
+    delete comm->c;
+    delete comm;
+  });
+}
+
+int cutfem_partition(cutfem_problem pb, cutfem_comm comm) {
+  return guarded([&]() {
+    check_built(pb);
+    cf::require(comm != nullptr && comm->c != nullptr, cf::ERR_ARG, "null or already attached comm");
+    pb->p.partition(comm->c);
+    comm->c = nullptr;   // owned by the problem now
+    delete comm;
+  });
+}
+
+int cutfem_partition_info(cutfem_problem pb, int level, int* out) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(out != nullptr, cf::ERR_ARG, "null output");
+    const cf::LevelData& D = pb->p.lv[level];
+    const int nl = D.a.nl;
+    out[0] = D.part;
+    out[1] = D.part ? D.r0 : 0;
+    out[2] = D.part ? D.r1 : nl;
+    out[3] = D.part ? D.v0 : 0;
+    out[4] = D.part ? D.v1 : nl;
+    out[5] = pb->p.comm ? pb->p.comm->rank : 0;
+    out[6] = pb->p.comm ? pb->p.comm->world : 1;
+  });
+}
+
+int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream) {
+  return guarded([&]() {
+    check_level(pb, level);
+    cf::require(v != nullptr, cf::ERR_ARG, "null vector");
+    use_stream(pb, stream);
+    pb->p.halo(level, v);
   });
 }
 

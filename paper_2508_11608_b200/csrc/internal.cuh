@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #define CF_MAXP 4
 #define CF_MAXNQ 12
@@ -71,6 +72,14 @@ struct LevelArgs {
   const double* ecut;                // n_cut * ((p+1)^2)^2 cut-cell matrices (bulk + Nitsche), cut_mode 0
 };
 
+// One halo transfer of the slab partition (comm.cuh): rows of a lattice
+// vector sent to / received from a neighbouring rank, as double offsets.
+struct Xfer {
+  int peer;
+  int64_t send_off, send_n;   // doubles of my vector sent to `peer` (land at the same offset there)
+  int64_t recv_off, recv_n;   // doubles of my vector received from `peer`
+};
+
 // Per-level device data owned by the problem.
 struct LevelData {
   LevelArgs a;
@@ -102,6 +111,9 @@ struct LevelData {
   int cart_tile_off[5] = {0, 0, 0, 0, 0};
   int* fused_tiles = nullptr;        // TC x TC cell tiles for the fused Cartesian sweep
   int n_fused_tiles = 0;
+  int tc = 16;                       // cells per side of the fused tiles of this level
+  int* fused_ext = nullptr;          // fused tiles dilated by one tile (split sweep through xs)
+  int n_fused_ext = 0;
   int n_cutp[8] = {};
   int cutp_off[9] = {};
   int* cutp_list = nullptr;          // packed I + (n+1) J
@@ -123,6 +135,18 @@ struct LevelData {
   int copy_n[5][4] = {};
   // workspace lattice vectors for the V-cycle
   double *x = nullptr, *b = nullptr, *r = nullptr;
+  // slab partition; part = 0: not partitioned (every
+  // rank holds and computes the whole level)
+  int part = 0;
+  int c0 = 0, c1 = 0;                // owned cell rows
+  int r0 = 0, r1 = 0;                // owned lattice rows (the last rank also owns the top line)
+  int v0 = 0, v1 = 0;                // rows valid after a halo exchange
+  int rc0 = 0, rc1 = 0;              // coarse lattice rows this rank restricts into
+  int band[6] = {0, 0, 0, 0, 0, 0};  // k_band range (BandRange): cut cells, two ghost-face ranges
+  int at0 = 0, at1 = 0;              // tile rows of the TMA operator (k_apply_tile)
+  const void* act_desc = nullptr;    // cut-patch descriptors the sweeps run (this rank's subset)
+  int act_off[5] = {0, 0, 0, 0, 0};
+  std::vector<Xfer> halo;            // transfers of one halo exchange
 };
 
 struct Params {

@@ -463,13 +463,21 @@ __global__ void __launch_bounds__(TP* TP) k_cart_colour(LevelArgs L, const int* 
 // ---------------------------------------------------------------------------
 // Operator A x, pass 1: cut cells (warp each, quadrature) and ghost faces
 // (thread each, jump moments) into the level's scratch buffers.
+// BandRange selects the cut cells [cut_lo, cut_lo + cut_n) and the ghost
+// faces [g_lo0, g_lo0 + g_n0) U [g_lo1, g_lo1 + g_n1) (a rank's rows under the
+// slab partition; everything otherwise).
+struct BandRange {
+  int cut_lo, cut_n, g_lo0, g_n0, g_lo1, g_n1;
+};
+
 template <int P, bool QUAD>
-__global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x) {
+__global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x, BandRange R) {
   constexpr int NB = (P + 1) * (P + 1);
   __shared__ double sX[4][NB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * 4 + w;
-  if (gw < L.n_cut) {
+  const int gw0 = blockIdx.x * 4 + w;
+  if (gw0 < R.cut_n) {
+    const int gw = R.cut_lo + gw0;
     const int c = L.cut_list[gw], i = c % L.n, j = c / L.n;
     for (int t = lane; t < NB; t += 32)
       sX[w][t] = x[(size_t)(j * P + t / (P + 1)) * L.ld + i * P + t % (P + 1)];
@@ -489,8 +497,9 @@ __global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x) {
     }
     return;
   }
-  const int g = (gw - L.n_cut) * 32 + lane;
-  if (g >= L.n_ghost) return;
+  const int k = (gw0 - R.cut_n) * 32 + lane;
+  if (k >= R.g_n0 + R.g_n1) return;
+  const int g = k < R.g_n0 ? R.g_lo0 + k : R.g_lo1 + (k - R.g_n0);
   const int f = L.ghost_list[g], n = L.n;
   const int axis = f >= n * n, c = f - axis * n * n, i = c % n, j = c / n;
   const double* X1 = x + (size_t)(j * P) * L.ld + i * P;
@@ -507,13 +516,14 @@ __global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x) {
 // the cells containing it (tensor rows on uncut cells, the cut-cell buffer)
 // and of the ghost faces of those cells.  y = A x, or y = b - A x if b != 0.
 template <int P>
-__global__ void __launch_bounds__(256) k_node_apply(LevelArgs L, const double* x, const double* b, double* y) {
+__global__ void __launch_bounds__(256) k_node_apply(LevelArgs L, const double* x, const double* b, double* y, int row0,
+                                                    int row1) {
   constexpr int NB = (P + 1) * (P + 1);
   __shared__ SmTab T;
   load_smtab<P>(T);
   __syncthreads();
-  const int a = blockIdx.x * blockDim.x + threadIdx.x, bb = blockIdx.y * blockDim.y + threadIdx.y;
-  if (a >= L.ld || bb >= L.nl) return;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x, bb = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (a >= L.ld || bb >= row1) return;
   const size_t o = (size_t)bb * L.ld + a;
   if (!L.mask[o]) {
     y[o] = 0.0;
@@ -547,13 +557,13 @@ __global__ void __launch_bounds__(256) k_node_apply(LevelArgs L, const double* x
 // coarse cell is the parent of the fine cell min(a/p, n_f-1); weights
 // L_m((child + xi_k)/2).
 template <int P>
-__global__ void k_prolongate_add(LevelArgs Lf, LevelArgs Lc, const double* xc, double* xf) {
+__global__ void k_prolongate_add(LevelArgs Lf, LevelArgs Lc, const double* xc, double* xf, int row0, int row1) {
   __shared__ double pw[2 * P + 1][P + 1];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   if (tid < (2 * P + 1) * (P + 1)) pw[tid / (P + 1)][tid % (P + 1)] = c_tab[P].pw[tid / (P + 1)][tid % (P + 1)];
   __syncthreads();
-  const int a = blockIdx.x * blockDim.x + threadIdx.x, bb = blockIdx.y * blockDim.y + threadIdx.y;
-  if (a >= Lf.nl || bb >= Lf.nl) return;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x, bb = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (a >= Lf.nl || bb >= row1) return;
   const size_t o = (size_t)bb * Lf.ld + a;
   if (!Lf.mask[o]) return;
   const int Ia = min(min(a / P, Lf.n - 1) / 2, Lc.n - 1), Ib = min(min(bb / P, Lf.n - 1) / 2, Lc.n - 1);
@@ -572,13 +582,13 @@ __global__ void k_prolongate_add(LevelArgs Lf, LevelArgs Lc, const double* xc, d
 // b_c = P^T r_f: one thread per coarse node gathers the fine nodes of the
 // support of its basis function with weights phi^c(x_f) (tensor of 1D).
 template <int P>
-__global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double* bc) {
+__global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double* bc, int row0, int row1) {
   __shared__ double tw[P][4 * P + 1];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   if (tid < P * (4 * P + 1)) tw[tid / (4 * P + 1)][tid % (4 * P + 1)] = c_tab[P].tw[tid / (4 * P + 1)][tid % (4 * P + 1)];
   __syncthreads();
-  const int A = blockIdx.x * blockDim.x + threadIdx.x, B = blockIdx.y * blockDim.y + threadIdx.y;
-  if (A >= Lc.ld || B >= Lc.nl) return;
+  const int A = blockIdx.x * blockDim.x + threadIdx.x, B = row0 + blockIdx.y * blockDim.y + threadIdx.y;
+  if (A >= Lc.ld || B >= row1) return;
   const size_t o = (size_t)B * Lc.ld + A;
   if (A >= Lc.nl || !Lc.mask[o]) {
     bc[o] = 0.0;
@@ -658,6 +668,14 @@ __global__ void __launch_bounds__(DOT_THREADS) k_dot_final(const double* part, d
     else if (mode == 1) { sc[1] = s; sc[2] = sc[0] / s; }
     else { sc[4] = s; sc[5] = s / sc[0]; sc[0] = s; }
   }
+}
+
+// the mode logic of k_dot_final applied to an all-reduced sum sc[7] (slab partition)
+__global__ void k_dot_mode(double* sc, int mode, int slot) {
+  const double s = sc[7];
+  if (mode == 0) sc[slot] = s;
+  else if (mode == 1) { sc[1] = s; sc[2] = sc[0] / s; }
+  else { sc[4] = s; sc[5] = s / sc[0]; sc[0] = s; }
 }
 
 // x += alpha p, r -= alpha q

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -20,6 +21,7 @@
 #include "smoother2.cuh"
 #include "dim3.cuh"
 #include "tables.cuh"
+#include "comm.cuh"
 
 namespace cf {
 
@@ -43,6 +45,8 @@ int64_t g_launches = 0;
 
 template <int P> constexpr int cart_tp() { return P == 1 ? 16 : (P == 2 ? 8 : (P == 3 ? 7 : 6)); }
 constexpr int CUT_WPB = 4;
+// fused Cartesian tile (cells per side); p = 2 uses 32-cell tiles on large
+// levels of the TMA/tensor-core sweep (Problem::tc_big_n) and 16 otherwise
 template <int P> constexpr int fused_tc() { return P == 1 ? 32 : (P <= 3 ? 16 : 8); }
 
 struct GraphRec {
@@ -71,6 +75,12 @@ struct Problem {
   int cut2_v = 6;           // 2D CTA-per-patch cut step version (env CUTFEM_CUT2=4: six-barrier v4)
   int cut3_v = 3;           // 3D cut-patch kernel version (env CUTFEM_CUT3=2: lane-parallel jump array)
   bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
+  bool cart_split = false;  // force the two-launch Cartesian sweep through xs (env CUTFEM_CART_SPLIT=1)
+  int tc_big_n = 512;       // levels with n >= this use 32-cell fused tiles for p = 2 (env CUTFEM_TC32_MIN_N)
+  bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
+  // slab partition: comm != nullptr after partition()
+  Comm* comm = nullptr;
+  static constexpr int HALO = 4;   // halo width in cells (the fused Cartesian apron)
   // coarse
   int n0 = 0;
   int* c_nodes = nullptr;
@@ -88,6 +98,7 @@ struct Problem {
   std::map<std::tuple<int, const void*, const void*, int>, GraphRec> graphs;
 
   ~Problem() {
+    delete comm;
     for (auto& g : graphs)
       if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
     for (void* p : allocs) cudaFree(p);
@@ -159,17 +170,40 @@ struct Problem {
   bool pdl = true;
   template <typename... KArgs, typename... Args>
   void launch(void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, Args... args) {
+    launch_ex(false, kern, g, b, smem, args...);
+  }
+  // coop = cooperative launch (all CTAs co-resident; the kernel may grid-sync)
+  template <typename... KArgs, typename... Args>
+  void launch_ex(bool coop, void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
     cfg.blockDim = b;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    if (coop) {
+      attr[na].id = cudaLaunchAttributeCooperative;
+      attr[na].val.cooperative = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     CF_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
+  }
+  // CTAs of `kern` (256 threads, smem bytes) that fit on the device at once
+  template <typename K>
+  int coresident(K kern, size_t smem) {
+    int nsm = 0, dev = 0, per = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem));
+    return per * nsm;
   }
 
   // launch as one thread-block cluster of `cs` CTAs (grid = cs), with PDL
@@ -206,6 +240,9 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_CLUSTER_MAX")) cluster_max = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_PERSISTENT_BELOW")) persistent_below = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_CART_SPLIT")) cart_split = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (prm.dim == 3) {
       setup_mesh3();
       return;
@@ -417,10 +454,15 @@ struct Problem {
       {
         int TC = 0;
         CF_DISPATCH(p, TC = fused_tc<P>());
+        if (p == 2 && use_mma && use_tma && n >= tc_big_n) TC = 32;   // (p = 3: 32-cell tiles exceed shared memory)
+        D.tc = TC;
         const int tx = ceil_div(n, TC), nt = tx * tx;
         uint8_t* tf = alloc<uint8_t>(nt);
         int* ts = alloc<int>(nt);
         k_fused_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(n, D.vkind, TC, tx, tf, nt);
+        CF_LAUNCHED();
+        uint8_t* tfe = alloc<uint8_t>(nt);
+        k_dilate_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(tx, tf, tfe);
         CF_LAUNCHED();
         D.n_fused_tiles = select(tf, nt, ts);
         if (D.n_fused_tiles) {
@@ -428,6 +470,13 @@ struct Problem {
           CF_LAUNCHED();
         }
         D.fused_tiles = ts;
+        int* te = alloc<int>(nt);
+        D.n_fused_ext = select(tfe, nt, te);
+        if (D.n_fused_ext) {
+          k_pack_tiles<<<ceil_div(D.n_fused_ext, 128), 128, 0, st>>>(te, D.n_fused_ext, tx, te);
+          CF_LAUNCHED();
+        }
+        D.fused_ext = te;
       }
       D.cart_tiles = alloc<int>(tiles.size());
       if (!tiles.empty())
@@ -485,7 +534,9 @@ struct Problem {
                                                                           D.cutp_inv, (CutDesc*)D.desc)));
         CF_LAUNCHED();
       }
-      build_copy_lists(D);
+      D.act_desc = D.desc;
+      for (int c = 0; c < 5; ++c) D.act_off[c] = D.cutp_off[c];
+      build_copy_lists(D, D.ent_node, D.ent_col_off, (const CutDesc*)D.desc, ncp);
       sync();
     }
     build_coarse();
@@ -506,22 +557,25 @@ struct Problem {
 
   // ping-pong copy lists (see k_cut_step): [prev][cur] = N_prev \ N_cur for
   // prev, cur colours, and [4][cur] = band \ N_cur for the first step
-  void build_copy_lists(LevelData& D) {
+  // (ent_node, col_off[0..4]: the interior nodes of the swept patches per
+  // colour; desc/ncp: their descriptors)
+  void build_copy_lists(LevelData& D, const int32_t* ent_node, const int64_t* col_off, const CutDesc* desc, int ncp) {
     const LevelArgs& L = D.a;
     const int64_t nv = (int64_t)L.nl * L.ld;
-    D.xs = alloc<double>(nv);
-    CF_CUDA(cudaMemsetAsync(D.xs, 0, nv * 8, st));
+    if (!D.xs) {
+      D.xs = alloc<double>(nv);
+      CF_CUDA(cudaMemsetAsync(D.xs, 0, nv * 8, st));
+    }
     uint8_t* marks = alloc<uint8_t>(5 * nv);
     CF_CUDA(cudaMemsetAsync(marks, 0, 5 * nv, st));
     for (int c = 0; c < 4; ++c)
-      if (D.ent_col_off[c + 1] > D.ent_col_off[c]) {
-        k_mark_entries<<<ceil_div(D.ent_col_off[c + 1] - D.ent_col_off[c], 256), 256, 0, st>>>(
-            D.ent_node, D.ent_col_off[c], D.ent_col_off[c + 1], marks + c * nv);
+      if (col_off[c + 1] > col_off[c]) {
+        k_mark_entries<<<ceil_div(col_off[c + 1] - col_off[c], 256), 256, 0, st>>>(ent_node, col_off[c], col_off[c + 1],
+                                                                                 marks + c * nv);
         CF_LAUNCHED();
       }
-    const int ncp = D.cutp_off[4];
     if (ncp) {
-      k_mark_band<<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, ncp, L, marks + 4 * nv);
+      k_mark_band<<<ncp, 128, 0, st>>>(desc, ncp, L, marks + 4 * nv);
       CF_LAUNCHED();
     }
     uint8_t* fl = alloc<uint8_t>(nv);
@@ -545,6 +599,114 @@ struct Problem {
     if (!all.empty())
       CF_CUDA(cudaMemcpyAsync(D.copy_lists, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
     sync();
+    for (void* q : {(void*)marks, (void*)fl, (void*)tmp}) {
+      cudaFree(q);
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), q), allocs.end());
+    }
+  }
+
+  // ------------------------------------------------------- slab partition
+  // Rank c->rank of c->world owns the cell rows [c0, c1) = [rank s, (rank+1) s),
+  // s = n / world, of every level whose slabs are whole fused Cartesian tiles
+  // (s % TC == 0) at least HALO + 1 cells thick, from the finest level down;
+  // the coarser levels (and level 0, the exact coarse solve) are replicated on
+  // every rank.  Each rank keeps the whole hierarchy (setup is replicated) and
+  // restricts its work lists to its rows: fused tiles of its rows, cut patches
+  // whose interiors meet its rows (vertex rows [c0 - 1, c1]: the patches on
+  // the slab boundary are computed by both neighbours, identically), cut cells
+  // and ghost faces within HALO cells.  Lattice vectors are full-size; the
+  // rows [v0, v1) = owned rows + HALO cells are valid after a halo exchange.
+  void partition(Comm* c) {
+    require(prm.dim == 2, ERR_ARG, "the slab partition is implemented for 2D problems");
+    require(built, ERR_STATE, "cutfem_build_patches has not been called");
+    require(comm == nullptr, ERR_STATE, "the problem is already partitioned");
+    require(c->world >= 1 && c->rank >= 0 && c->rank < c->world, ERR_ARG, "bad rank / world");
+    const int W = c->world, R = c->rank, p = prm.p;
+    fused = true;
+    pingpong = true;
+    persistent = false;
+    persistent_below = 0;
+    cluster_max = 0;
+    bool finer = true;
+    for (int l = prm.n_levels - 1; l >= 1; --l) {
+      LevelData& D = lv[l];
+      const int n = D.a.n, nl = D.a.nl, ld = D.a.ld, s = n / W, TC = D.tc;
+      const bool ok = finer && W > 1 && n % W == 0 && s % TC == 0 && s >= HALO + 1;
+      finer = ok;
+      if (!ok) continue;
+      D.part = 1;
+      D.c0 = R * s;
+      D.c1 = D.c0 + s;
+      D.r0 = D.c0 * p;
+      D.r1 = R == W - 1 ? nl : D.c1 * p;
+      D.v0 = std::max(0, D.r0 - HALO * p);
+      D.v1 = std::min(nl, D.r1 + HALO * p + 1);
+      D.rc0 = p * (D.c0 / 2);
+      D.rc1 = R == W - 1 ? lv[l - 1].a.nl : p * (D.c1 / 2);
+      D.halo.clear();
+      const int64_t hr = (int64_t)HALO * p;
+      if (R > 0) D.halo.push_back({R - 1, (int64_t)D.r0 * ld, (hr + 1) * ld, (D.r0 - hr) * ld, hr * ld});
+      if (R < W - 1) D.halo.push_back({R + 1, (D.r1 - hr) * ld, hr * ld, (int64_t)D.r1 * ld, (hr + 1) * ld});
+      // fused tiles (packed ti | tj << 16) of the owned rows
+      auto own_tiles = [&](int*& list, int& cnt) {
+        std::vector<int> h(cnt), keep;
+        if (cnt) CF_CUDA(cudaMemcpy(h.data(), list, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+        for (int t : h)
+          if ((t >> 16) * TC >= D.c0 && (t >> 16) * TC < D.c1) keep.push_back(t);
+        cnt = (int)keep.size();
+        list = alloc<int>(cnt);
+        if (cnt) CF_CUDA(cudaMemcpy(list, keep.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice));
+      };
+      own_tiles(D.fused_tiles, D.n_fused_tiles);
+      own_tiles(D.fused_ext, D.n_fused_ext);
+      // cut patches with vertex rows [c0 - 1, c1]
+      const int ncp = D.cutp_off[4];
+      std::vector<CutDesc> hd(ncp), kd;
+      std::vector<int64_t> he(ncp + 1);
+      std::vector<int32_t> hn(D.n_ent), kn;
+      if (ncp) {
+        CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
+        CF_CUDA(cudaMemcpy(he.data(), D.cutp_ent, sizeof(int64_t) * (ncp + 1), cudaMemcpyDeviceToHost));
+      }
+      if (D.n_ent) CF_CUDA(cudaMemcpy(hn.data(), D.ent_node, sizeof(int32_t) * D.n_ent, cudaMemcpyDeviceToHost));
+      int64_t col_off[5] = {0, 0, 0, 0, 0};
+      D.act_off[0] = 0;
+      for (int cc = 0; cc < 4; ++cc) {
+        for (int k = D.cutp_off[cc]; k < D.cutp_off[cc + 1]; ++k)
+          if (hd[k].J >= D.c0 - 1 && hd[k].J <= D.c1) {
+            kd.push_back(hd[k]);
+            kn.insert(kn.end(), hn.begin() + he[k], hn.begin() + he[k + 1]);
+          }
+        D.act_off[cc + 1] = (int)kd.size();
+        col_off[cc + 1] = (int64_t)kn.size();
+      }
+      CutDesc* dd = alloc<CutDesc>(kd.size());
+      int32_t* dn = alloc<int32_t>(kn.size());
+      if (!kd.empty()) CF_CUDA(cudaMemcpy(dd, kd.data(), sizeof(CutDesc) * kd.size(), cudaMemcpyHostToDevice));
+      if (!kn.empty()) CF_CUDA(cudaMemcpy(dn, kn.data(), sizeof(int32_t) * kn.size(), cudaMemcpyHostToDevice));
+      D.act_desc = dd;
+      build_copy_lists(D, dn, col_off, dd, (int)kd.size());
+      // k_band ranges: cut cells and x-faces in cell rows [c0 - HALO, c1 + HALO),
+      // y-faces (j | j+1) with j in [c0 - HALO, c1 + HALO - 1); the lists are sorted by j n + i
+      const int lo = std::max(0, D.c0 - HALO), hi = std::min(n, D.c1 + HALO);
+      std::vector<int> hc(D.a.n_cut), hg(D.a.n_ghost);
+      if (D.a.n_cut) CF_CUDA(cudaMemcpy(hc.data(), D.cut_list, sizeof(int) * D.a.n_cut, cudaMemcpyDeviceToHost));
+      if (D.a.n_ghost) CF_CUDA(cudaMemcpy(hg.data(), D.ghost_list, sizeof(int) * D.a.n_ghost, cudaMemcpyDeviceToHost));
+      auto range = [](const std::vector<int>& v, int a, int b, int& first, int& cnt) {
+        first = (int)(std::lower_bound(v.begin(), v.end(), a) - v.begin());
+        cnt = (int)(std::lower_bound(v.begin(), v.end(), b) - v.begin()) - first;
+      };
+      const int nn = n * n;
+      range(hc, lo * n, hi * n, D.band[0], D.band[1]);
+      range(hg, lo * n, hi * n, D.band[2], D.band[3]);
+      const int yhi = std::max(lo, std::min(n - 1, D.c1 + HALO - 1));
+      range(hg, nn + lo * n, nn + yhi * n, D.band[4], D.band[5]);
+      // TMA operator tiles (16 cells) covering the cell rows [c0 - 2, c1 + 2)
+      const int nt = ceil_div(n, 16);
+      D.at0 = std::max(0, (D.c0 - 2) / 16);
+      D.at1 = std::min(nt, ceil_div(D.c1 + 2, 16));
+    }
+    comm = c;
   }
 
   void build_coarse() {
@@ -586,14 +748,19 @@ struct Problem {
       apply3(l, x, y, b);
       return;
     }
-    const LevelArgs& L = lv[l].a;
+    const LevelData& D = lv[l];
+    const LevelArgs& L = D.a;
     const int p = prm.p;
-    const int warps = L.n_cut + ceil_div(L.n_ghost, 32);
+    // under the slab partition: cut cells / ghost faces and tile rows around
+    // the owned rows (the residual is needed 2 cells beyond them by the restriction)
+    const BandRange R = D.part ? BandRange{D.band[0], D.band[1], D.band[2], D.band[3], D.band[4], D.band[5]}
+                               : BandRange{0, L.n_cut, 0, L.n_ghost, 0, 0};
+    const int warps = R.cut_n + ceil_div(R.g_n0 + R.g_n1, 32);
     if (warps) {
       if (prm.cut_mode == 0) {
-        CF_DISPATCH(p, (k_band<P, false><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+        CF_DISPATCH(p, (k_band<P, false><<<ceil_div(warps, 4), 128, 0, st>>>(L, x, R)));
       } else {
-        CF_DISPATCH(p, (k_band<P, true><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+        CF_DISPATCH(p, (k_band<P, true><<<ceil_div(warps, 4), 128, 0, st>>>(L, x, R)));
       }
       CF_LAUNCHED();
     }
@@ -610,12 +777,15 @@ struct Problem {
           attr = true;
         }
         const int nt = ceil_div(L.n, TX);
-        launch(k_apply_tile<P, TX>, dim3(nt, nt), dim3(256), S::bytes, tm, L, b, y);
+        const int ty0 = D.part ? D.at0 : 0, ty1 = D.part ? D.at1 : nt;
+        if (ty1 > ty0) launch(k_apply_tile<P, TX>, dim3(nt, ty1 - ty0), dim3(256), S::bytes, tm, L, b, y, ty0);
       });
       CF_LAUNCHED();
       return;
     }
-    CF_DISPATCH(p, (k_node_apply<P><<<dim3(ceil_div(L.ld, 32), ceil_div(L.nl, 8)), dim3(32, 8), 0, st>>>(L, x, b, y)));
+    const int row0 = D.part ? std::max(0, (D.c0 - 2) * p) : 0, row1 = D.part ? std::min(L.nl, (D.c1 + 2) * p + 1) : L.nl;
+    CF_DISPATCH(p, (k_node_apply<P><<<dim3(ceil_div(L.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
+                       L, x, b, y, row0, row1)));
     CF_LAUNCHED();
   }
 
@@ -720,65 +890,119 @@ struct Problem {
     CF_LAUNCHED();
   }
 
+  // the TMA / tensor-core fused sweep with TC x TC cell tiles (see cart_fused)
+  template <int P, int TC>
+  void cart_fused_tma(int l, double* x, const double* b, int reverse) {
+    LevelData& D = lv[l];
+    const double* G = host::cart_map(P);
+    using S = CartTmaSmem<P, TC>;
+    const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
+    const CUtensorMap tmb = host::lattice_tmap(b, D.a.nl, D.a.ld, S::RWP, S::RW);
+    static int cap = -1;
+    if (cap < 0) {
+      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      cap = coresident(k_cart_fused_tma<P, TC>, S::bytes);
+    }
+    if (verbose) {
+      std::fprintf(stderr, "[cutfem] level %d: %d fused tiles (%d ext), %d co-resident -> %s\n", l,
+                   D.n_fused_tiles, D.n_fused_ext, cap, (!cart_split && D.n_fused_tiles <= cap) ? "in place" : "split");
+    }
+    if (!cart_split && D.n_fused_tiles <= cap) {
+      launch_ex(true, k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tmx, tmb, D.a,
+                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, 1);
+      CF_LAUNCHED();
+      halo(l, x);
+      return;
+    }
+    const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
+    if (D.n_fused_ext)
+      launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_ext), dim3(256), S::bytes, tmx, tmb, D.a,
+             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, 0);
+    CF_LAUNCHED();
+    halo(l, D.xs);
+    launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tms, tmb, D.a,
+           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, 0);
+    CF_LAUNCHED();
+    halo(l, x);
+    return;
+  }
+
   // all four Cartesian colours in one launch (temporal blocking); p <= 3 on
-  // the fp64 tensor cores (dense patch map), p = 4 by fast diagonalisation
+  // the fp64 tensor cores (dense patch map), p = 4 by fast diagonalisation.
+  // The sweep is in place: a cooperative launch whose grid barrier orders
+  // every CTA's region load before any write.  When the tiles do not fit on
+  // the device at once (or CUTFEM_CART_SPLIT=1) the TMA sweep runs as two
+  // launches through the shadow buffer xs (passes 0-1: x -> xs over the tiles
+  // dilated by one tile, passes 2-3: xs -> x); the other variants fall back to
+  // one launch per colour.
   void cart_fused(int l, double* x, const double* b, int reverse) {
     LevelData& D = lv[l];
     if (!D.n_fused_tiles) return;
     CF_DISPATCH(prm.p, {
+      if constexpr (P == 2) {
+        if (D.tc == 32) {
+          cart_fused_tma<P, 32>(l, x, b, reverse);
+          return;
+        }
+      }
       constexpr int TC = fused_tc<P>();
       if constexpr (P <= 3) {
         if (use_mma && use_tma && D.a.nl >= CartTmaSmem<P, TC>::RW && D.a.ld >= CartTmaSmem<P, TC>::RWP) {
-          const double* G = host::cart_map(P);
-          using S = CartTmaSmem<P, TC>;
-          const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
-          const CUtensorMap tmb = host::lattice_tmap(b, D.a.nl, D.a.ld, S::RWP, S::RW);
-          static bool attr3 = false;
-          if (!attr3) {
-            CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
-            CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            attr3 = true;
-          }
-          launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tmx, tmb, D.a,
-                 (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse);
-          CF_LAUNCHED();
+          cart_fused_tma<P, TC>(l, x, b, reverse);
           return;
         }
         if (use_mma) {
           const double* G = host::cart_map(P);
           const size_t smb = CartMMASmem<P, TC>::doubles * sizeof(double) + CartMMASmem<P, TC>::ints * sizeof(int);
-          static bool attr = false;
-          if (!attr) {
+          static int cap = -1;
+          if (cap < 0) {
             CF_CUDA(cudaFuncSetAttribute(k_cart_fused_mma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-            attr = true;
+            cap = coresident(k_cart_fused_mma<P, TC>, smb);
           }
-          launch(k_cart_fused_mma<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
-                 (const uint8_t*)D.vkind, G, x, b, reverse);
-          CF_LAUNCHED();
+          if (!cart_split && D.n_fused_tiles <= cap) {
+            launch_ex(true, k_cart_fused_mma<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a,
+                      (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, b, reverse, 1);
+            CF_LAUNCHED();
+            halo(l, x);
+            return;
+          }
+          for (int s = 0; s < 4; ++s) {
+            cart_step(l, reverse ? 3 - s : s, x, b);
+            halo(l, x);
+          }
           return;
         }
       }
       const size_t smb = CartFusedSmem<P, TC>::doubles * sizeof(double);
-      static bool attr2 = false;
-      if (!attr2) {
+      static int cap2 = -1;
+      if (cap2 < 0) {
         CF_CUDA(cudaFuncSetAttribute(k_cart_fused<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-        attr2 = true;
+        cap2 = coresident(k_cart_fused<P, TC>, smb);
       }
-      launch(k_cart_fused<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
-             (const uint8_t*)D.vkind, x, b, reverse);
+      if (!cart_split && D.n_fused_tiles <= cap2) {
+        launch_ex(true, k_cart_fused<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
+                  (const uint8_t*)D.vkind, x, b, reverse, 1);
+        CF_LAUNCHED();
+        halo(l, x);
+        return;
+      }
+      for (int s = 0; s < 4; ++s) {
+        cart_step(l, reverse ? 3 - s : s, x, b);
+        halo(l, x);
+      }
     });
-    CF_LAUNCHED();
   }
 
   // one ping-pong cut step: read R, write W (k_cut_step); prev = colour of the
   // previous step (4 = first step of the sweep: copy the read band)
   void cut_pp_step(int l, int c, int prev, const double* R, double* W, const double* b) {
     LevelData& D = lv[l];
-    const int np = D.n_cutp[c];
+    const int np = D.act_off[c + 1] - D.act_off[c];
     const int ncopy = prev < 0 ? 0 : D.copy_n[prev][c];
     const int32_t* cl = D.copy_lists + (prev < 0 ? 0 : D.copy_off[prev][c]);
     if (!np && !ncopy) return;
-    const CutDesc* desc = (const CutDesc*)D.desc + D.cutp_off[c];
+    const CutDesc* desc = (const CutDesc*)D.act_desc + D.act_off[c];
     CF_DISPATCH(prm.p, {
       if (prm.cut_mode == 0 && cta_cut) {
         constexpr int NT = 64;
@@ -888,14 +1112,26 @@ struct Problem {
       for (int cc = 0; cc < 4; ++cc, ++s) {
         const int c = reverse ? 3 - cc : cc;
         cut_pp_step(l, c, prev, bufs[s & 1], bufs[(s + 1) & 1], b);
+        halo(l, bufs[(s + 1) & 1]);
         prev = c;
       }
+  }
+
+  // halo exchange of a lattice vector of a partitioned level (no-op otherwise)
+  void halo(int l, double* v) {
+    if (comm && lv[l].part) comm->exchange(v, lv[l].halo, st);
   }
 
   // x <- S(x, b) (P eq. smoother-split, l.196-210; reverse = adjoint order, R9)
   void smooth(int l, double* x, const double* b, int reverse) {
     if (prm.dim == 3) {
       smooth3(l, x, b, reverse);
+      return;
+    }
+    if (lv[l].part) {   // slab partition: fused Cartesian sweep + ping-pong cut steps, halo after each write
+      if (!reverse) cart_fused(l, x, b, 0);
+      cut_sweeps(l, x, b, reverse);
+      if (reverse) cart_fused(l, x, b, 1);
       return;
     }
     if (persistent_below > 0 && lv[l].a.n <= persistent_below) {
@@ -938,7 +1174,10 @@ struct Problem {
       CF_LAUNCHED();
       return;
     }
-    CF_DISPATCH(prm.p, (k_restrict<P><<<dim3(ceil_div(Lc.ld, 32), ceil_div(Lc.nl, 8)), dim3(32, 8), 0, st>>>(Lf, Lc, rf, bc)));
+    const LevelData& F = lv[l];
+    const int row0 = F.part ? F.rc0 : 0, row1 = F.part ? F.rc1 : Lc.nl;
+    CF_DISPATCH(prm.p, (k_restrict<P><<<dim3(ceil_div(Lc.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
+                           Lf, Lc, rf, bc, row0, row1)));
     CF_LAUNCHED();
   }
   void prolongate_add(int l, const double* xc, double* xf) {
@@ -949,7 +1188,10 @@ struct Problem {
       CF_LAUNCHED();
       return;
     }
-    CF_DISPATCH(prm.p, (k_prolongate_add<P><<<dim3(ceil_div(Lf.nl, 32), ceil_div(Lf.nl, 8)), dim3(32, 8), 0, st>>>(Lf, Lc, xc, xf)));
+    const LevelData& F = lv[l];
+    const int row0 = F.part ? F.v0 : 0, row1 = F.part ? F.v1 : Lf.nl;
+    CF_DISPATCH(prm.p, (k_prolongate_add<P><<<dim3(ceil_div(Lf.nl, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
+                           Lf, Lc, xc, xf, row0, row1)));
     CF_LAUNCHED();
   }
   void coarse_solve(const double* b, double* x) {
@@ -968,6 +1210,10 @@ struct Problem {
     smooth(l, x, b, 0);
     apply(l, x, D.r, b);
     restrict_(l, D.r, C.b);
+    if (D.part) {
+      if (C.part) halo(l - 1, C.b);
+      else replicate(l - 1, C.b, D.rc0, D.rc1);   // the coarse levels run on every rank
+    }
     CF_CUDA(cudaMemsetAsync(C.x, 0, vsize(l - 1) * 8, st));
     vcycle(l - 1, C.x, C.b);
     prolongate_add(l, C.x, x);
@@ -977,6 +1223,10 @@ struct Problem {
   // run `body` through a cached CUDA graph keyed by (tag, ptrs)
   template <class F>
   void graphed(int tag, const void* p1, const void* p2, int extra, F&& body) {
+    if (comm) {   // the halo exchanges synchronise ranks on the host (LocalComm): no capture
+      body();
+      return;
+    }
     auto key = std::make_tuple(tag, p1, p2, extra);
     auto it = graphs.find(key);
     if (it == graphs.end()) {
@@ -1015,10 +1265,30 @@ struct Problem {
   }
 
   void dot(const double* a, const double* b, int mode, int slot) {
+    const LevelData& F = lv[prm.n_levels - 1];
+    if (comm && F.part) {   // owned rows, then the sum over ranks
+      const int64_t o = (int64_t)F.r0 * F.a.ld, n = (int64_t)(F.r1 - F.r0) * F.a.ld;
+      k_dot_partial<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(a + o, b + o, n, part);
+      CF_LAUNCHED();
+      k_dot_final<<<1, DOT_THREADS, 0, st>>>(part, sc, 0, 7);
+      CF_LAUNCHED();
+      comm->allreduce_sum(sc + 7, 1, st);
+      k_dot_mode<<<1, 1, 0, st>>>(sc, mode, slot);
+      CF_LAUNCHED();
+      return;
+    }
     k_dot_partial<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(a, b, vsize(prm.n_levels - 1), part);
     CF_LAUNCHED();
     k_dot_final<<<1, DOT_THREADS, 0, st>>>(part, sc, mode, slot);
     CF_LAUNCHED();
+  }
+
+  // v (a replicated level) <- sum over ranks of the rows [r0, r1) each rank computed
+  void replicate(int l, double* v, int r0, int r1) {
+    const LevelArgs& L = lv[l].a;
+    if (r0 > 0) CF_CUDA(cudaMemsetAsync(v, 0, (size_t)r0 * L.ld * 8, st));
+    if (r1 < L.nl) CF_CUDA(cudaMemsetAsync(v + (size_t)r1 * L.ld, 0, (size_t)(L.nl - r1) * L.ld * 8, st));
+    comm->allreduce_sum(v, (int64_t)L.nl * L.ld, st);
   }
 
   // ================================================================ 3D
@@ -1346,8 +1616,12 @@ struct Problem {
     const int Lf = prm.n_levels - 1;
     LevelData& F = lv[Lf];
     const int64_t nv = vsize(Lf);
+    // vector updates and dot products over the owned rows under the slab
+    // partition (the dot products are then summed over the ranks)
+    const bool dist = comm && F.part;
+    const int64_t o = dist ? (int64_t)F.r0 * F.a.ld : 0, no = dist ? (int64_t)(F.r1 - F.r0) * F.a.ld : nv;
     const int grid = 4 * 148;
-    k_masked_copy<<<grid, 256, 0, st>>>(cg_r, b, F.mask, nv);
+    k_masked_copy<<<grid, 256, 0, st>>>(cg_r + o, b + o, F.mask + o, no);
     CF_LAUNCHED();
     CF_CUDA(cudaMemsetAsync(cg_x, 0, nv * 8, st));
     dot(cg_r, cg_r, 0, 3);
@@ -1359,6 +1633,7 @@ struct Problem {
     if (r0 > 0.0) {
       auto precond = [&]() {
         CF_CUDA(cudaMemsetAsync(cg_z, 0, nv * 8, st));
+        halo(Lf, cg_r);
         vcycle(Lf, cg_z, cg_r);
       };
       graphed(100, cg_z, cg_r, 0, [&]() {
@@ -1368,9 +1643,10 @@ struct Problem {
       });
       while (it < max_it) {
         graphed(101, cg_p, cg_q, 0, [&]() {
+          halo(Lf, cg_p);
           apply(Lf, cg_p, cg_q, nullptr);
           dot(cg_p, cg_q, 1, 0);
-          k_cg_update<<<grid, 256, 0, st>>>(cg_x, cg_r, cg_p, cg_q, sc, nv);
+          k_cg_update<<<grid, 256, 0, st>>>(cg_x + o, cg_r + o, cg_p + o, cg_q + o, sc, no);
           CF_LAUNCHED();
           dot(cg_r, cg_r, 0, 3);
           CF_CUDA(cudaMemcpyAsync(sc_host, sc, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1382,7 +1658,7 @@ struct Problem {
         graphed(102, cg_z, cg_r, 0, [&]() {
           precond();
           dot(cg_r, cg_z, 2, 0);
-          k_cg_direction<<<grid, 256, 0, st>>>(cg_p, cg_z, sc, nv);
+          k_cg_direction<<<grid, 256, 0, st>>>(cg_p + o, cg_z + o, sc, no);
           CF_LAUNCHED();
         });
       }

@@ -483,7 +483,7 @@ struct CartFusedSmem {
 
 template <int P, int TC>
 __global__ void __launch_bounds__(256) k_cart_fused(LevelArgs L, const int* tiles, const uint8_t* vk, double* x,
-                                                    const double* b, int reverse) {
+                                                    const double* b, int reverse, int gsync) {
   using S = CartFusedSmem<P, TC>;
   constexpr int NE = S::NE, NI = S::NI, H = S::H, RW = S::RW, NPR = S::NPR;
   extern __shared__ double sm[];
@@ -612,6 +612,8 @@ __global__ void __launch_bounds__(256) k_cart_fused(LevelArgs L, const int* tile
       __syncthreads();
     }
   }
+  // in place: every CTA of the (cooperative) grid has read its region before any write
+  if (gsync) cooperative_groups::this_grid().sync();
   // owned nodes: [P ci0, P (ci0 + TC)) (+ the last lattice line on the mesh boundary)
   const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   const int aw = ahi - P * ci0, bw = bhi - P * cj0;
@@ -619,6 +621,21 @@ __global__ void __launch_bounds__(256) k_cart_fused(LevelArgs L, const int* tile
     const int a = P * ci0 + e % aw, bb = P * cj0 + e / aw;
     x[(size_t)bb * L.ld + a] = Xs[(bb - b0) * RW + (a - a0)];
   }
+}
+
+// tiles within one tile of a flagged tile (the tiles whose owned nodes the
+// split Cartesian sweep must carry through the shadow buffer)
+__global__ void k_dilate_tile_flags(int tx, const uint8_t* in, uint8_t* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= tx * tx) return;
+  const int ti = t % tx, tj = t / tx;
+  uint8_t f = 0;
+  for (int dj = -1; dj <= 1; ++dj)
+    for (int di = -1; di <= 1; ++di) {
+      const int i = ti + di, j = tj + dj;
+      if (i >= 0 && j >= 0 && i < tx && j < tx && in[j * tx + i]) f = 1;
+    }
+  out[t] = f;
 }
 
 // tiles of TC x TC cells whose owned vertex range holds a Cartesian patch
@@ -853,7 +870,8 @@ struct CartMMASmem {
 // tensor cores (mma.sync m8n8k4 .f64), G from host::cart_affine_map.
 template <int P, int TC>
 __global__ void __launch_bounds__(256) k_cart_fused_mma(LevelArgs L, const int* tiles, const uint8_t* vk,
-                                                        const double* G, double* x, const double* b, int reverse) {
+                                                        const double* G, double* x, const double* b, int reverse,
+                                                        int gsync) {
   using C = CartMMA<P>;
   using S = CartMMASmem<P, TC>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS, MT = C::MT, H = S::H, RW = S::RW;
@@ -928,6 +946,7 @@ __global__ void __launch_bounds__(256) k_cart_fused_mma(LevelArgs L, const int* 
     }
     __syncthreads();
   }
+  if (gsync) cooperative_groups::this_grid().sync();
   const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   const int aw = ahi - P * ci0, bw = bhi - P * cj0;
   for (int e = tid; e < aw * bw; e += 256) {
@@ -1030,11 +1049,17 @@ struct CartTmaSmem {
   static constexpr size_t bytes = head + 2 * tile_doubles * sizeof(double);
 };
 
+// Passes s0..s1-1 of the four colour passes (halo radius s1-1-s).  The tile
+// region is read from the tensor map `tmx` and the owned nodes are written to
+// `xout`.  In place (xout = the source of tmx) only with gsync = 1 in a
+// cooperative launch: the grid barrier before the write keeps every CTA's
+// apron load ahead of its neighbours' writes.  Otherwise the sweep is split
+// into two launches through the shadow buffer (passes 0-1 x -> xs, 2-3 xs -> x).
 template <int P, int TC>
-__global__ void __launch_bounds__(256, CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(256, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
-                                                        double* x, int reverse) {
+                                                        double* xout, int reverse, int s0, int s1, int gsync) {
   using C = CartMMA<P>;
   using S = CartTmaSmem<P, TC>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
@@ -1079,8 +1104,8 @@ __global__ void __launch_bounds__(256, CF_CART_MINB) k_cart_fused_tma(const __gr
     tma_load_2d(Xs, &tmx, a0, b0, bar);
     tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
   }
-  for (int s = 0; s < 4; ++s) {
-    const int c = reverse ? 3 - s : s, rad = 3 - s;
+  for (int s = s0; s < s1; ++s) {
+    const int c = reverse ? 3 - s : s, rad = s1 - 1 - s;
     const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
     const int nvx = (ci0 + TC + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
     // compact the Cartesian patches of this pass
@@ -1092,7 +1117,7 @@ __global__ void __launch_bounds__(256, CF_CART_MINB) k_cart_fused_tma(const __gr
       if (I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART)
         plist[atomicAdd(pcount, 1)] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
     }
-    if (s == 0) mbar_wait(bar, 0);
+    if (s == s0) mbar_wait(bar, 0);
     __syncthreads();
     const int np = *pcount, ng = (np + 7) / 8;
     for (int g = warp; g < ng; g += 8) {
@@ -1131,11 +1156,13 @@ __global__ void __launch_bounds__(256, CF_CART_MINB) k_cart_fused_tma(const __gr
     }
     __syncthreads();
   }
+  if (s1 == s0) mbar_wait(bar, 0);
+  if (gsync) cooperative_groups::this_grid().sync();
   // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
   const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   for (int bb = P * cj0 + warp; bb < bhi; bb += 8) {
     const double* src = Xs + (bb - b0) * RWP - a0;
-    double* dst = x + (size_t)bb * L.ld;
+    double* dst = xout + (size_t)bb * L.ld;
     for (int a = P * ci0 + lane; a < ahi; a += 32) dst[a] = src[a];
   }
 }
@@ -1488,7 +1515,7 @@ struct ApplySmem {
 
 template <int P, int TX>
 __global__ void __launch_bounds__(256) k_apply_tile(const __grid_constant__ CUtensorMap tmx, LevelArgs L,
-                                                    const double* b, double* y) {
+                                                    const double* b, double* y, int ty0) {
   using S = ApplySmem<P, TX>;
   constexpr int NB = (P + 1) * (P + 1), RWP = S::RWP, RW = S::RW;
   extern __shared__ __align__(128) unsigned char smraw[];   // no static shared memory: keeps the TMA tile 128-byte aligned
@@ -1497,7 +1524,7 @@ __global__ void __launch_bounds__(256) k_apply_tile(const __grid_constant__ CUte
   SmTab& T = *(SmTab*)(smraw + 128 + S::tile * sizeof(double));
   uint8_t* Cs = smraw + 128 + S::tile * sizeof(double) + sizeof(SmTab);   // cell codes of the tile + halo
   const int tid = threadIdx.x, n = L.n;
-  const int tx = blockIdx.x, ty = blockIdx.y;
+  const int tx = blockIdx.x, ty = ty0 + blockIdx.y;
   const int i0 = tx * TX, j0 = ty * TX;
   const int a0 = (P * (i0 - 1)) & ~1, b0 = P * (j0 - 1), sh = P * (i0 - 1) - a0;   // sh = 0 or 1
   pdl_trigger();

@@ -69,6 +69,13 @@ _sig = {
     "cutfem_export_patches": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, ctypes.POINTER(ctypes.c_int)],
     "cutfem_export_cut_interior": [_P, ctypes.c_int, _D, _D, ctypes.POINTER(ctypes.c_int),
                                    ctypes.POINTER(ctypes.c_int64)],
+    "cutfem_comm_local_create": [ctypes.c_int, ctypes.POINTER(_P)],
+    "cutfem_comm_nccl_unique_id": [ctypes.c_char_p],
+    "cutfem_comm_nccl_create": [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
+    "cutfem_comm_destroy": [_P],
+    "cutfem_partition": [_P, _P],
+    "cutfem_partition_info": [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+    "cutfem_halo_exchange": [_P, ctypes.c_int, _D, _P],
 }
 for _name, _args in _sig.items():
     getattr(_lib, _name).argtypes = _args
@@ -109,6 +116,55 @@ def make_params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D=0
     g = (ctypes.c_double * 4)(*[float(v) for v in (list(gamma_k) + [-1] * 4)[:4]])
     return Params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D, g, sigma, n_q, n_c, symmetric,
                   cut_mode, dim, z0, cz)
+
+
+NCCL_ID_BYTES = 128
+
+
+class Comm:
+    """One rank's communicator endpoint (cutfem_comm), handed to
+    Problem.partition, which takes ownership."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @staticmethod
+    def local(world):
+        """`world` endpoints of an in-process group (ranks = threads sharing one device)."""
+        arr = (_P * world)()
+        _check(_lib.cutfem_comm_local_create(world, arr))
+        return [Comm(_P(arr[r])) for r in range(world)]
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+        _check(_lib.cutfem_comm_nccl_unique_id(buf))
+        return buf.raw
+
+    @staticmethod
+    def nccl(uid, rank, world):
+        """NCCL endpoint; uid = the bytes of rank 0's nccl_unique_id() (collective)."""
+        h = _P()
+        _check(_lib.cutfem_comm_nccl_create(ctypes.c_char_p(bytes(uid)), rank, world, ctypes.byref(h)))
+        return Comm(h)
+
+    @staticmethod
+    def nccl_from_torch(dist):
+        """NCCL endpoint of the current torch.distributed group (id broadcast over it)."""
+        from .dist import broadcast_nccl_id
+        uid = broadcast_nccl_id(dist, Comm.nccl_unique_id)
+        return Comm.nccl(uid, dist.get_rank(), dist.get_world_size())
+
+    def close(self):
+        if self._h:
+            _check(_lib.cutfem_comm_destroy(self._h))
+            self._h = _P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Problem:
@@ -174,6 +230,20 @@ class Problem:
         """padded device vector -> (NL^dim,) numpy lattice vector."""
         rows, nl, ld = self._rows(level)
         return t.detach().cpu().numpy().reshape(rows, ld)[:, :nl].ravel().copy()
+
+    # --- slab partition
+    def partition(self, comm):
+        _check(_lib.cutfem_partition(self._h, comm._h))
+        comm._h = _P()   # owned by the problem
+
+    def partition_info(self, level=-1):
+        """dict(part, r0, r1, v0, v1, rank, world): owned / valid lattice rows of `level`."""
+        out = (ctypes.c_int * 7)()
+        _check(_lib.cutfem_partition_info(self._h, level % self.n_levels, out))
+        return dict(zip(("part", "r0", "r1", "v0", "v1", "rank", "world"), list(out)))
+
+    def halo_exchange(self, level, v, stream=None):
+        _check(_lib.cutfem_halo_exchange(self._h, level % self.n_levels, _dptr(v), _stream(stream)))
 
     # --- hot path (names of the C ABI)
     def apply_operator(self, level, x, y, stream=None):

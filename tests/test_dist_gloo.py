@@ -7,7 +7,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2508_11608_b200.dist import max_over_ranks, rank_env, replica_throughput
+from paper_2508_11608_b200.dist import (broadcast_nccl_id, max_over_ranks, rank_env, replica_throughput,
+                                         strong_throughput)
 
 
 def _free_port():
@@ -49,3 +50,31 @@ def test_max_over_ranks_and_throughput_world2():
 def test_single_process_identity():
     assert max_over_ranks(3.5) == 3.5
     assert replica_throughput(10, 2, 1, 1.0) == pytest.approx(2e4)
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_11608_b200 import cutfem
+    uid = broadcast_nccl_id(dist, cutfem.Comm.nccl_unique_id)
+    t = strong_throughput(680065, 10, max_over_ranks(2.0 + rank, dist))
+    dist.barrier()
+    q.put((rank, uid, t))
+    dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast_world2():
+    """the slab partition's NCCL endpoint: rank 0's unique id (cutfem_comm_nccl_unique_id,
+    128 bytes) reaches every rank; strong-scaling throughput uses the max time"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert len(res[0][1]) == 128 and res[0][1] == res[1][1]
+    assert res[0][2] == res[1][2] == pytest.approx(680065 * 10 / 3e-3)

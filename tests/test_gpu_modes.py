@@ -49,9 +49,13 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
 @pytest.mark.parametrize("env", [{"CUTFEM_MMA": "0"}, {"CUTFEM_FUSED": "0"}, {"CUTFEM_PINGPONG": "0"},
                                  {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}, {"CUTFEM_CTACUT": "0"},
                                  {"CUTFEM_TILEAPPLY": "0"}, {"CUTFEM_CUT2": "4", "CUTFEM_CLUSTER_MAX": "0"},
-                                 {"CUTFEM_CUT2": "5", "CUTFEM_CLUSTER_MAX": "0"}, {"CUTFEM_CLUSTER_MAX": "512"}],
+                                 {"CUTFEM_CUT2": "5", "CUTFEM_CLUSTER_MAX": "0"}, {"CUTFEM_CLUSTER_MAX": "512"},
+                                 {"CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CART_SPLIT": "1", "CUTFEM_TMA": "0"},
+                                 {"CUTFEM_CART_SPLIT": "1", "CUTFEM_MMA": "0"}, {"CUTFEM_TC32_MIN_N": "32"},
+                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_CART_SPLIT": "1"}],
                          ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply",
-                              "cut-step-v4", "cut-step-v5", "cluster-cut-sweeps"])
+                              "cut-step-v4", "cut-step-v5", "cluster-cut-sweeps", "cart-split-tma",
+                              "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
@@ -102,3 +106,29 @@ def test_edge_geometries_and_degrees(w):
     it, rel = g.solve_cg_mg(x, g.to_device(bl), tol=1e-8, max_it=200)
     xo, ito, _ = o.solve_cg(compact(o.fine.lv, bl), 1e-8, 200)
     assert it == ito and rel <= 1e-8
+
+
+def test_cart_split_equals_inplace_fullsize():
+    """config1 (512^2, Q2): the two-launch Cartesian sweep through the shadow
+    buffer (used when the tiles are not co-resident) gives bit-identical
+    smoothing steps to the in-place cooperative sweep"""
+    from paper_2508_11608_b200 import cutfem
+    import torch
+    w = workloads.CONFIG1
+    L = w.n_levels - 1
+    xl, bl = lattice_random(w, 70, L), lattice_random(w, 71, L)
+    outs = []
+    for split in ("0", "1"):
+        os.environ["CUTFEM_CART_SPLIT"] = split
+        try:
+            g = cutfem.Problem.from_workload(w)
+        finally:
+            os.environ.pop("CUTFEM_CART_SPLIT", None)
+        x = g.to_device(xl)
+        b = g.to_device(bl)
+        for rev in (False, True, False):
+            g.smooth(L, x, b, rev)
+        torch.cuda.synchronize()
+        outs.append(g.to_host(x))
+        g.close()
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -1,0 +1,250 @@
+"""Slab partition of the background mesh (north_star:
+slabs with a halo exchange per colour sweep and per residual) on one GPU.
+
+W ranks run as W host threads of this process, each with its own problem
+handle and CUDA stream, joined by the in-process communicator
+(cutfem_comm_local_create): the decomposition (row ownership, work-list
+filtering, halo schedule, replicated coarse levels, distributed dot products)
+is the code under test; only the transport differs from the NCCL endpoint.
+
+Every node of a partitioned smoothing step / V-cycle is computed from the same
+inputs in the same order as on one rank, so the owned rows must agree
+BIT-EXACTLY with the single-rank path (itself parity-tested against the
+oracle); CG sums its dot products per rank, so its iterates agree to rounding
+and its iteration counts exactly.
+"""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import workloads
+from workloads import Workload
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+# section-4 circle (R1) at 128^2 (Q2, Q3) / 256^2 (Q1); an off-centre circle for ragged cut patterns
+W_Q2 = workloads.paper_level(2, 9)                 # 2 .. 128 cells per side
+W_Q1 = workloads.paper_level(1, 9)                 # 2 .. 256
+W_Q3 = workloads.paper_level(3, 9)
+W_OFF = Workload("offcentre-Q2-256", -1.105, -1.105, 2.21, 2, 8, 0.0137, -0.0211, 0.9071, 2)
+
+
+def _cutfem():
+    from paper_2508_11608_b200 import cutfem
+    return cutfem
+
+
+def run_ranks(w, world, fn, timeout=300, env=None):
+    """fn(rank, problem, stream) on `world` threads; returns the per-rank results."""
+    cutfem = _cutfem()
+    comms = cutfem.Comm.local(world)
+    gs = []
+    for c in comms:
+        g = with_env(env, lambda: cutfem.Problem.from_workload(w))
+        g.partition(c)
+        gs.append(g)
+    torch.cuda.synchronize()
+    out, errs = [None] * world, []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(r, gs[r], s)
+            s.synchronize()
+        except BaseException as e:  # noqa: BLE001  (re-raised below)
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in th), "a rank hung (halo exchange mismatch)"
+    if errs:
+        raise errs[0]
+    torch.cuda.synchronize()
+    return out, gs
+
+
+def with_env(env, fn):
+    saved = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        return fn()
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def owned(g, v, level=-1):
+    info = g.partition_info(level)
+    nl, ld = g.lattice_shape(level)
+    a = v.detach().cpu().numpy().reshape(-1, ld)[:, :nl]
+    return info["r0"], info["r1"], a[info["r0"]:info["r1"]]
+
+
+def single(w):
+    return _cutfem().Problem.from_workload(w)
+
+
+@pytest.mark.parametrize("w,world", [(W_Q2, 2), (W_Q2, 4), (W_Q1, 2), (W_Q1, 8), (W_Q3, 2)])
+def test_partition_layout(w, world):
+    """owned rows tile the lattice; valid rows = owned + HALO cells; the levels
+    below the first non-partitionable one are replicated"""
+    _, gs = run_ranks(w, world, lambda r, g, s: None)
+    for level in range(w.n_levels):
+        infos = [g.partition_info(level) for g in gs]
+        nl, _ = gs[0].lattice_shape(level)
+        parts = {i["part"] for i in infos}
+        assert len(parts) == 1
+        if infos[0]["part"]:
+            assert infos[0]["r0"] == 0 and infos[-1]["r1"] == nl
+            for a, b in zip(infos, infos[1:]):
+                assert a["r1"] == b["r0"]
+            for i in infos:
+                assert i["v0"] == max(0, i["r0"] - 4 * w.p) and i["v1"] == min(nl, i["r1"] + 4 * w.p + 1)
+        else:
+            assert all(i["r0"] == 0 and i["r1"] == nl for i in infos)
+    top = [g.partition_info(-1)["part"] for g in gs]
+    assert all(top), "the finest level must be partitioned in these cases"
+    # monotone: partitioned levels form a suffix of the hierarchy
+    flags = [gs[0].partition_info(l)["part"] for l in range(w.n_levels)]
+    assert flags == sorted(flags)
+
+
+TC32 = {"CUTFEM_TC32_MIN_N": "128"}   # 32-cell fused tiles on the 128^2 / 256^2 levels
+SPLIT = {"CUTFEM_CART_SPLIT": "1"}    # two-launch Cartesian sweep through the shadow buffer
+
+
+@pytest.mark.parametrize("w,world,env", [(W_Q2, 2, None), (W_Q2, 4, None), (W_Q1, 2, None), (W_Q1, 8, None),
+                                         (W_Q3, 2, None), (W_OFF, 4, None), (W_Q2, 2, TC32), (W_OFF, 4, TC32),
+                                         (W_Q2, 4, SPLIT)])
+@pytest.mark.parametrize("reverse", [0, 1])
+def test_smooth_bitexact(w, world, env, reverse):
+    L = w.n_levels - 1
+    x0 = workloads.lattice_vector(w, 11)
+    b0 = workloads.lattice_vector(w, 12)
+    g1 = with_env(env, lambda: single(w))
+    x1 = g1.to_device(x0)
+    for _ in range(2):
+        g1.smooth(L, x1, g1.to_device(b0), reverse=bool(reverse))
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        x = g.to_device(x0)
+        b = g.to_device(b0)
+        for _ in range(2):
+            g.smooth(L, x, b, reverse=bool(reverse), stream=s.cuda_stream)
+        return x
+
+    xs, gs = run_ranks(w, world, fn, env=env)
+    ref = x1.cpu().numpy().reshape(-1, g1.lattice_shape(L)[1])[:, :g1.lattice_shape(L)[0]]
+    for g, x in zip(gs, xs):
+        r0, r1, a = owned(g, x, L)
+        np.testing.assert_array_equal(a, ref[r0:r1])
+
+
+@pytest.mark.parametrize("w,world", [(W_Q2, 2), (W_Q2, 4), (W_Q1, 8), (W_Q3, 2), (W_OFF, 2)])
+def test_operator_bitexact(w, world):
+    L = w.n_levels - 1
+    x0 = workloads.lattice_vector(w, 21)
+    g1 = single(w)
+    y1 = g1.zeros()
+    g1.apply_operator(L, g1.to_device(x0), y1)
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        y = g.zeros()
+        g.apply_operator(L, g.to_device(x0), y, stream=s.cuda_stream)
+        return y
+
+    ys, gs = run_ranks(w, world, fn)
+    nl, ld = g1.lattice_shape(L)
+    ref = y1.cpu().numpy().reshape(-1, ld)[:, :nl]
+    for g, y in zip(gs, ys):
+        r0, r1, a = owned(g, y, L)
+        np.testing.assert_array_equal(a, ref[r0:r1])
+
+
+@pytest.mark.parametrize("w,world,env", [(W_Q2, 2, None), (W_Q2, 4, None), (W_Q1, 2, None), (W_Q1, 8, None),
+                                         (W_Q3, 2, None), (W_OFF, 4, None), (W_OFF, 2, TC32)])
+def test_vcycle_bitexact(w, world, env):
+    b0 = workloads.lattice_vector(w, 31)
+    x0 = workloads.lattice_vector(w, 32)
+    g1 = with_env(env, lambda: single(w))
+    x1 = g1.to_device(x0)
+    g1.vcycle(x1, g1.to_device(b0))
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        x = g.to_device(x0)
+        g.vcycle(x, g.to_device(b0), stream=s.cuda_stream)
+        return x
+
+    xs, gs = run_ranks(w, world, fn, env=env)
+    nl, ld = g1.lattice_shape(-1)
+    ref = x1.cpu().numpy().reshape(-1, ld)[:, :nl]
+    for g, x in zip(gs, xs):
+        r0, r1, a = owned(g, x)
+        np.testing.assert_array_equal(a, ref[r0:r1])
+
+
+@pytest.mark.parametrize("w,world", [(W_Q2, 2), (W_Q2, 4), (W_Q1, 8), (W_OFF, 4)])
+def test_cg_iterations(w, world):
+    """identical iteration counts; solution within rounding of the single-rank
+    solve (the dot products are summed per rank first)"""
+    b0 = workloads.lattice_vector(w, 41)
+    g1 = single(w)
+    xs1 = g1.zeros()
+    it1, rel1 = g1.solve_cg_mg(xs1, g1.to_device(b0), tol=1e-9)
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        x = g.zeros()
+        it, rel = g.solve_cg_mg(x, g.to_device(b0), tol=1e-9, stream=s.cuda_stream)
+        return x, it, rel
+
+    res, gs = run_ranks(w, world, fn)
+    nl, ld = g1.lattice_shape(-1)
+    ref = xs1.cpu().numpy().reshape(-1, ld)[:, :nl]
+    scale = np.abs(ref).max()
+    for g, (x, it, rel) in zip(gs, res):
+        assert it == it1
+        assert abs(rel - rel1) <= 1e-6 * max(rel1, 1e-300) + 1e-14
+        r0, r1, a = owned(g, x)
+        assert np.abs(a - ref[r0:r1]).max() <= 1e-10 * scale
+
+
+def test_halo_exchange_rows():
+    """after an exchange, every rank's halo rows equal the owners' rows"""
+    w, world = W_Q2, 4
+    L = w.n_levels - 1
+
+    def fn(r, g, s):
+        nl, ld = g.lattice_shape(L)
+        v = torch.full((nl * ld,), -1.0, dtype=torch.float64, device="cuda")
+        info = g.partition_info(L)
+        rows = torch.arange(nl, dtype=torch.float64, device="cuda").repeat_interleave(ld)
+        lo, hi = info["r0"] * ld, info["r1"] * ld
+        v[lo:hi] = rows[lo:hi] + 1000.0 * r
+        g.halo_exchange(L, v, stream=s.cuda_stream)
+        return v
+
+    vs, gs = run_ranks(w, world, fn)
+    infos = [g.partition_info(L) for g in gs]
+    nl, ld = gs[0].lattice_shape(L)
+    for r, (g, v) in enumerate(zip(gs, vs)):
+        a = v.cpu().numpy().reshape(nl, ld)
+        i = infos[r]
+        for row in range(i["v0"], i["v1"]):
+            owner = next(q for q, j in enumerate(infos) if j["r0"] <= row < j["r1"])
+            assert a[row, 0] == row + 1000.0 * owner, (r, row)
