@@ -1617,8 +1617,10 @@ __device__ __forceinline__ void cut6_prologue(const CutDesc* desc, int k, const 
       for (int e = gt; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
 }
 
-// main part (after the previous step's W is visible)
-template <int P, int NT>
+// main part (after the previous step's W is visible).  LDCG: read the window
+// through L2 only (ld.global.cg) -- inside one launch whose earlier steps
+// wrote R from other SMs, where an L1-cached (cp.async.ca) line could be stale
+template <int P, int NT, bool LDCG = false>
 __device__ __forceinline__ void cut6_main(const LevelArgs& L, const SmTab& T, const double* R, double* W,
                                           const double* b, unsigned char* gsm, int gt, int bar) {
   using S = CutGroup6<P>;
@@ -1637,8 +1639,12 @@ __device__ __forceinline__ void cut6_main(const LevelArgs& L, const SmTab& T, co
   for (int e = gt; e < WS * WS; e += NT) {
     const int r = e / WS, c = e - r * WS;
     const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
-    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, R + (size_t)bb * L.ld + a);
-    else Wp[e] = 0.0;
+    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) {
+      if (LDCG) Wp[e] = __ldcg(R + (size_t)bb * L.ld + a);
+      else cp_async8(Wp + e, R + (size_t)bb * L.ld + a);
+    } else {
+      Wp[e] = 0.0;
+    }
   }
   for (int loc = gt; loc < MM; loc += NT) {
     const unsigned long long word = d.mask[loc >> 6];
@@ -1875,6 +1881,65 @@ __global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster(CutSweepArgs A) {
     if (s < 5) CF_TSTAMP(2 + s);
   }
   CF_TSTAMP(7);
+}
+
+}  // namespace cf
+
+namespace cf {
+
+// ---- all n_c x 4 cut colour steps of one smoothing step in ONE cooperative
+// launch over the whole GPU: CTAs of G groups of 64 threads (one patch per
+// group per round, the v6 group routine), grid-wide barriers between the
+// ping-pong steps instead of kernel boundaries.  The window of a step is read
+// with ld.global.cg (the previous step was written by other SMs in this
+// launch); the next step's descriptor / inverse / element-matrix prologue is
+// issued before the barrier.
+template <int P, int G>
+__global__ void __launch_bounds__(64 * G) k_cut_sweeps_grid(CutSweepArgs A) {
+  using S = CutGroup6<P>;
+  __shared__ SmTab T;
+  extern __shared__ __align__(128) unsigned char smg[];
+  const int tid = threadIdx.x, grp = tid >> 6, gt = tid & 63;
+  const int cr = (int)blockIdx.x, cs = (int)gridDim.x;
+  unsigned char* gsm = smg + (size_t)grp * ((S::bytes + 127) & ~127);
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  pdl_trigger();
+  load_smtab<P>(T);
+  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
+  const int k0 = cr * G + grp;   // round-0 patch of this group
+  {
+    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c];
+    if (k0 < np) cut6_prologue<P, 64>(A.desc, A.cut_off[c] + k0, A.ecut, A.inv, gsm, gt, 1 + grp);
+  }
+  __syncthreads();
+  pdl_wait();
+  double* bufs[2] = {A.x, A.xs};
+  int prev = 4;
+  const int nsteps = A.n_c * 4;
+  for (int s = 0; s < nsteps; ++s) {
+    const int c = step_colour(s);
+    const double* R = bufs[s & 1];
+    double* W = bufs[(s + 1) & 1];
+    const int nco = A.copy_n[prev][c];
+    const int32_t* cl = A.copy + A.copy_off[prev][c];
+    for (int e = cr * 64 * G + tid; e < nco; e += cs * 64 * G) W[cl[e]] = __ldcg(R + cl[e]);
+    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
+    const int rounds = (np + cs * G - 1) / (cs * G);
+    for (int r = 0; r < rounds; ++r) {
+      const int k = (r * cs + cr) * G + grp;
+      if (k < np) {
+        if (r > 0) cut6_prologue<P, 64>(A.desc, p0 + k, A.ecut, A.inv, gsm, gt, 1 + grp);
+        cut6_main<P, 64, true>(A.L, T, R, W, A.b, gsm, gt, 1 + grp);
+        group_sync(1 + grp, 64);
+      }
+    }
+    if (s + 1 < nsteps) {
+      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn];
+      if (k0 < npn) cut6_prologue<P, 64>(A.desc, A.cut_off[cn] + k0, A.ecut, A.inv, gsm, gt, 1 + grp);
+      grid.sync();
+    }
+    prev = c;
+  }
 }
 
 }  // namespace cf

@@ -248,3 +248,36 @@ def test_halo_exchange_rows():
         for row in range(i["v0"], i["v1"]):
             owner = next(q for q, j in enumerate(infos) if j["r0"] <= row < j["r1"])
             assert a[row, 0] == row + 1000.0 * owner, (r, row)
+
+
+@pytest.mark.parametrize("transport", ["nccl", "local"])
+def test_world1_transports(transport):
+    """a one-rank partition (every tile-aligned level "partitioned" into one
+    slab, no peers) through the NCCL endpoint (dlopen, ncclCommInitRank,
+    ncclAllReduce on the stream) and the in-process one: bit-identical smoothing
+    step and V-cycle, identical CG iterations"""
+    cutfem = _cutfem()
+    w = W_OFF
+    L = w.n_levels - 1
+    if transport == "nccl":
+        comm = cutfem.Comm.nccl(cutfem.Comm.nccl_unique_id(), 0, 1)
+    else:
+        comm = cutfem.Comm.local(1)[0]
+    g = cutfem.Problem.from_workload(w)
+    g.partition(comm)
+    assert g.partition_info(L)["part"] == 1
+    g1 = single(w)
+    x0, b0 = workloads.lattice_vector(w, 51), workloads.lattice_vector(w, 52)
+    outs = []
+    for h in (g1, g):
+        x = h.to_device(x0)
+        b = h.to_device(b0)
+        h.smooth(L, x, b)
+        h.vcycle(x, b)
+        xs = h.zeros()
+        it, _ = h.solve_cg_mg(xs, b, tol=1e-9)
+        torch.cuda.synchronize()
+        outs.append((h.to_host(x), it, h.to_host(xs)))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
+    assert np.abs(outs[0][2] - outs[1][2]).max() <= 1e-10 * np.abs(outs[0][2]).max()
