@@ -185,9 +185,11 @@ int cutfem_comm_nccl_create(const unsigned char* id, int rank, int world, cutfem
 /* destroys an endpoint that was not attached to a problem */
 int cutfem_comm_destroy(cutfem_comm comm);
 int cutfem_partition(cutfem_problem pb, cutfem_comm comm);
-/* out[7] = {partitioned, r0, r1, v0, v1, rank, world}: owned lattice rows
- * [r0, r1) and valid rows [v0, v1) of `level` (the whole lattice if the level
- * is not partitioned) */
+/* out[8] = {partitioned, r0, r1, v0, v1, rank, world, halo}: owned lattice
+ * rows [r0, r1) and valid rows [v0, v1) = owned rows +- `halo` cells of
+ * `level` (the whole lattice if the level is not partitioned).  halo = 4
+ * cells, or 12 n_c cells on levels whose slabs are thick enough for the
+ * wide-halo cut sweeps (one exchange per sweep instead of one per step) */
 int cutfem_partition_info(cutfem_problem pb, int level, int* out);
 /* exchange the halo rows of a lattice vector of `level` with the neighbours */
 int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream);

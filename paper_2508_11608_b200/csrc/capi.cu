@@ -238,6 +238,7 @@ int cutfem_partition_info(cutfem_problem pb, int level, int* out) {
     out[4] = D.part ? D.v1 : nl;
     out[5] = pb->p.comm ? pb->p.comm->rank : 0;
     out[6] = pb->p.comm ? pb->p.comm->world : 1;
+    out[7] = D.part ? D.hw : 0;
   });
 }
 

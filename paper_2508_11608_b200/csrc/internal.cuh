@@ -140,13 +140,20 @@ struct LevelData {
   int part = 0;
   int c0 = 0, c1 = 0;                // owned cell rows
   int r0 = 0, r1 = 0;                // owned lattice rows (the last rank also owns the top line)
-  int v0 = 0, v1 = 0;                // rows valid after a halo exchange
+  int v0 = 0, v1 = 0;                // rows valid after a (level) halo exchange: owned +- hw cells
+  int v0n = 0, v1n = 0;              // owned +- HALO cells (the narrow halo)
+  int wide = 0, hw = 0;              // wide-halo cut sweeps (hw = 3 * 4 n_c cells), else hw = HALO
   int rc0 = 0, rc1 = 0;              // coarse lattice rows this rank restricts into
   int band[6] = {0, 0, 0, 0, 0, 0};  // k_band range (BandRange): cut cells, two ghost-face ranges
   int at0 = 0, at1 = 0;              // tile rows of the TMA operator (k_apply_tile)
   const void* act_desc = nullptr;    // cut-patch descriptors the sweeps run (this rank's subset)
   int act_off[5] = {0, 0, 0, 0, 0};
-  std::vector<Xfer> halo;            // transfers of one halo exchange
+  std::vector<Xfer> halo;            // transfers of one halo exchange (hw cells)
+  std::vector<Xfer> halo_n;          // ... of the narrow halo
+  const void* wdesc = nullptr;       // wide-halo cut sweeps: descriptors of step s of direction d
+  std::vector<int> wd_off[2];        //   at wdesc + [wd_off[d][s], wd_off[d][s+1])
+  int32_t* wcopy = nullptr;          //   copy lists at wcopy + wc_off[d][s], wc_n[d][s] nodes
+  std::vector<int> wc_off[2], wc_n[2];
 };
 
 struct Params {

@@ -76,6 +76,7 @@ struct Problem {
   int cut3_v = 3;           // 3D cut-patch kernel version (env CUTFEM_CUT3=2: lane-parallel jump array)
   bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
   bool cart_split = false;  // force the two-launch Cartesian sweep through xs (env CUTFEM_CART_SPLIT=1)
+  bool wide_halo = true;    // partition: wide-halo cut sweeps where the slabs are thick enough (env CUTFEM_WIDE_HALO=0)
   // all cut sweeps of a smoothing step in one cooperative launch with grid
   // barriers (env CUTFEM_CUT_GRID=1).  Off: measured 57.5 us vs 43.2 us for
   // one PDL launch per step at config1 (a grid barrier costs more than a
@@ -247,6 +248,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_PERSISTENT_BELOW")) persistent_below = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CART_SPLIT")) cart_split = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_WIDE_HALO")) wide_halo = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT_GRID")) cut_grid = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT_GRID_MIN_N")) cut_grid_min_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
@@ -613,6 +615,91 @@ struct Problem {
     }
   }
 
+  // Wide-halo cut sweeps of a partitioned level: step s (of S = 4 n_c, per
+  // direction) runs the patches of its colour with vertex rows
+  // [c0 - e_s, c1 + e_s], e_s = 1 + 3 (S-1-s).  A patch reads the cell rows
+  // [J-2, J+2) and a node is final after step s if every step-s patch whose
+  // interior holds it ran, i.e. on the cell rows [c0 - e_s + 1, c1 + e_s - 1):
+  // exactly the rows step s+1 reads.  So one exchange of HW = e_0 + 2 = 3 S
+  // cells before the sweeps replaces the 4 n_c per-step exchanges, and the
+  // last step (e = 1) leaves the owned rows final.  Copy lists per step:
+  // N_{s-1} \ N_s, each N restricted to its step (for s = 0: the band of the
+  // windows of every patch of the sweep \ N_0).
+  void build_wide(LevelData& D, const std::vector<CutDesc>& hd, const std::vector<int64_t>& he,
+                  const std::vector<int32_t>& hn) {
+    const LevelArgs& L = D.a;
+    const int S = 4 * prm.n_c;
+    const int64_t nv = (int64_t)L.nl * L.ld;
+    std::vector<CutDesc> kd;
+    std::vector<std::vector<int32_t>> nodes;   // per (d, s)
+    for (int d = 0; d < 2; ++d) {
+      D.wd_off[d].assign(S + 1, 0);
+      for (int s = 0; s < S; ++s) {
+        const int c = d ? 3 - (s & 3) : (s & 3), e = 1 + 3 * (S - 1 - s);
+        D.wd_off[d][s] = (int)kd.size();
+        std::vector<int32_t> nn;
+        for (int k = D.cutp_off[c]; k < D.cutp_off[c + 1]; ++k)
+          if (hd[k].J >= D.c0 - e && hd[k].J <= D.c1 + e) {
+            kd.push_back(hd[k]);
+            nn.insert(nn.end(), hn.begin() + he[k], hn.begin() + he[k + 1]);
+          }
+        nodes.push_back(nn);
+      }
+      D.wd_off[d][S] = (int)kd.size();
+    }
+    CutDesc* dd = alloc<CutDesc>(kd.size());
+    if (!kd.empty()) CF_CUDA(cudaMemcpy(dd, kd.data(), sizeof(CutDesc) * kd.size(), cudaMemcpyHostToDevice));
+    D.wdesc = dd;
+    // marks of N_(d,s) and of the band of step 0, then the set differences
+    uint8_t* mk = alloc<uint8_t>(3 * nv);
+    uint8_t* fl = alloc<uint8_t>(nv);
+    int* tmp = alloc<int>(nv);
+    int32_t* dn = alloc<int32_t>(1);
+    std::vector<int32_t> all;
+    for (int d = 0; d < 2; ++d) {
+      D.wc_off[d].assign(S, 0);
+      D.wc_n[d].assign(S, 0);
+      for (int s = 0; s < S; ++s) {
+        CF_CUDA(cudaMemsetAsync(mk, 0, 2 * nv, st));
+        // mk[0] = previous set (band of step 0 for s = 0), mk[nv] = N_s
+        auto mark = [&](const std::vector<int32_t>& v, uint8_t* m) {
+          if (v.empty()) return;
+          int32_t* buf = alloc<int32_t>(v.size());
+          CF_CUDA(cudaMemcpy(buf, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice));
+          k_mark_entries<<<ceil_div((int64_t)v.size(), 256), 256, 0, st>>>(buf, 0, (int64_t)v.size(), m);
+          CF_LAUNCHED();
+          sync();
+          cudaFree(buf);
+          allocs.erase(std::remove(allocs.begin(), allocs.end(), (void*)buf), allocs.end());
+        };
+        if (s == 0) {   // the read band: windows of every patch the sweep runs
+          const int n0 = D.wd_off[d][S] - D.wd_off[d][0];
+          if (n0) {
+            k_mark_band<<<n0, 128, 0, st>>>(dd + D.wd_off[d][0], n0, L, mk);
+            CF_LAUNCHED();
+          }
+        } else {
+          mark(nodes[d * S + s - 1], mk);
+        }
+        mark(nodes[d * S + s], mk + nv);
+        k_andnot_flags<<<ceil_div(nv, 256), 256, 0, st>>>(mk, mk + nv, nv, fl);
+        CF_LAUNCHED();
+        const int cnt = select(fl, (int)nv, tmp);
+        std::vector<int32_t> h(cnt);
+        if (cnt) CF_CUDA(cudaMemcpy(h.data(), tmp, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+        D.wc_off[d][s] = (int)all.size();
+        D.wc_n[d][s] = cnt;
+        all.insert(all.end(), h.begin(), h.end());
+      }
+    }
+    D.wcopy = alloc<int32_t>(all.size());
+    if (!all.empty()) CF_CUDA(cudaMemcpy(D.wcopy, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
+    for (void* q : {(void*)mk, (void*)fl, (void*)tmp, (void*)dn}) {
+      cudaFree(q);
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), q), allocs.end());
+    }
+  }
+
   // ------------------------------------------------------- slab partition
   // Rank c->rank of c->world owns the cell rows [c0, c1) = [rank s, (rank+1) s),
   // s = n / world, of every level whose slabs are whole fused Cartesian tiles
@@ -647,14 +734,24 @@ struct Problem {
       D.c1 = D.c0 + s;
       D.r0 = D.c0 * p;
       D.r1 = R == W - 1 ? nl : D.c1 * p;
-      D.v0 = std::max(0, D.r0 - HALO * p);
-      D.v1 = std::min(nl, D.r1 + HALO * p + 1);
+      const int S = 4 * prm.n_c, HW = 3 * S;   // wide halo: 3 cells per cut step (see build_wide)
+      D.wide = wide_halo && s >= HW + 1;
+      D.hw = D.wide ? HW : HALO;
+      D.v0n = std::max(0, D.r0 - HALO * p);
+      D.v1n = std::min(nl, D.r1 + HALO * p + 1);
+      D.v0 = std::max(0, D.r0 - D.hw * p);
+      D.v1 = std::min(nl, D.r1 + D.hw * p + 1);
       D.rc0 = p * (D.c0 / 2);
       D.rc1 = R == W - 1 ? lv[l - 1].a.nl : p * (D.c1 / 2);
-      D.halo.clear();
-      const int64_t hr = (int64_t)HALO * p;
-      if (R > 0) D.halo.push_back({R - 1, (int64_t)D.r0 * ld, (hr + 1) * ld, (D.r0 - hr) * ld, hr * ld});
-      if (R < W - 1) D.halo.push_back({R + 1, (D.r1 - hr) * ld, hr * ld, (int64_t)D.r1 * ld, (hr + 1) * ld});
+      auto halo_list = [&](int hc) {
+        std::vector<Xfer> v;
+        const int64_t hr = (int64_t)hc * p;
+        if (R > 0) v.push_back({R - 1, (int64_t)D.r0 * ld, (hr + 1) * ld, (D.r0 - hr) * ld, hr * ld});
+        if (R < W - 1) v.push_back({R + 1, (D.r1 - hr) * ld, hr * ld, (int64_t)D.r1 * ld, (hr + 1) * ld});
+        return v;
+      };
+      D.halo = halo_list(D.hw);
+      D.halo_n = halo_list(HALO);
       // fused tiles (packed ti | tj << 16) of the owned rows
       auto own_tiles = [&](int*& list, int& cnt) {
         std::vector<int> h(cnt), keep;
@@ -694,6 +791,7 @@ struct Problem {
       if (!kn.empty()) CF_CUDA(cudaMemcpy(dn, kn.data(), sizeof(int32_t) * kn.size(), cudaMemcpyHostToDevice));
       D.act_desc = dd;
       build_copy_lists(D, dn, col_off, dd, (int)kd.size());
+      if (D.wide) build_wide(D, hd, he, hn);
       // k_band ranges: cut cells and x-faces in cell rows [c0 - HALO, c1 + HALO),
       // y-faces (j | j+1) with j in [c0 - HALO, c1 + HALO - 1); the lists are sorted by j n + i
       const int lo = std::max(0, D.c0 - HALO), hi = std::min(n, D.c1 + HALO);
@@ -898,6 +996,12 @@ struct Problem {
     CF_LAUNCHED();
   }
 
+  // exchange after the Cartesian sweep: none when the wide-halo cut sweeps
+  // follow (they start with their own wide exchange), else the narrow halo
+  void cart_done(int l, double* x, int reverse) {
+    if (!(lv[l].wide && !reverse)) halo_n(l, x);
+  }
+
   // the TMA / tensor-core fused sweep with TC x TC cell tiles (see cart_fused)
   template <int P, int TC>
   void cart_fused_tma(int l, double* x, const double* b, int reverse) {
@@ -920,7 +1024,7 @@ struct Problem {
       launch_ex(true, k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tmx, tmb, D.a,
                 (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, 1);
       CF_LAUNCHED();
-      halo(l, x);
+      cart_done(l, x, reverse);
       return;
     }
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
@@ -928,11 +1032,11 @@ struct Problem {
       launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_ext), dim3(256), S::bytes, tmx, tmb, D.a,
              (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, 0);
     CF_LAUNCHED();
-    halo(l, D.xs);
+    halo_n(l, D.xs);
     launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tms, tmb, D.a,
            (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, 0);
     CF_LAUNCHED();
-    halo(l, x);
+    cart_done(l, x, reverse);
     return;
   }
 
@@ -972,13 +1076,14 @@ struct Problem {
             launch_ex(true, k_cart_fused_mma<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a,
                       (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, b, reverse, 1);
             CF_LAUNCHED();
-            halo(l, x);
+            cart_done(l, x, reverse);
             return;
           }
           for (int s = 0; s < 4; ++s) {
             cart_step(l, reverse ? 3 - s : s, x, b);
-            halo(l, x);
+            if (s < 3) halo_n(l, x);
           }
+          cart_done(l, x, reverse);
           return;
         }
       }
@@ -992,13 +1097,14 @@ struct Problem {
         launch_ex(true, k_cart_fused<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
                   (const uint8_t*)D.vkind, x, b, reverse, 1);
         CF_LAUNCHED();
-        halo(l, x);
+        cart_done(l, x, reverse);
         return;
       }
       for (int s = 0; s < 4; ++s) {
         cart_step(l, reverse ? 3 - s : s, x, b);
-        halo(l, x);
+        if (s < 3) halo_n(l, x);
       }
+      cart_done(l, x, reverse);
     });
   }
 
@@ -1009,8 +1115,13 @@ struct Problem {
     const int np = D.act_off[c + 1] - D.act_off[c];
     const int ncopy = prev < 0 ? 0 : D.copy_n[prev][c];
     const int32_t* cl = D.copy_lists + (prev < 0 ? 0 : D.copy_off[prev][c]);
+    cut_pp_launch(l, (const CutDesc*)D.act_desc + D.act_off[c], np, cl, ncopy, R, W, b);
+  }
+  // one ping-pong cut step over the patches desc[0..np) with the copy list cl[0..ncopy)
+  void cut_pp_launch(int l, const CutDesc* desc, int np, const int32_t* cl, int ncopy, const double* R, double* W,
+                     const double* b) {
+    LevelData& D = lv[l];
     if (!np && !ncopy) return;
-    const CutDesc* desc = (const CutDesc*)D.act_desc + D.act_off[c];
     CF_DISPATCH(prm.p, {
       if (prm.cut_mode == 0 && cta_cut) {
         constexpr int NT = 64;
@@ -1161,19 +1272,35 @@ struct Problem {
       if (npmax <= cluster_max && cut_sweeps_cluster(l, x, b, reverse)) return;
     }
     double* bufs[2] = {x, lv[l].xs};
+    LevelData& D = lv[l];
+    if (comm && D.wide) {
+      // wide halo: one exchange, then every step on the rank's shrinking
+      // redundant patch sets (partition()), then the narrow halo
+      halo(l, x);
+      const int d = reverse ? 1 : 0, S = 4 * prm.n_c;
+      for (int s = 0; s < S; ++s)
+        cut_pp_launch(l, (const CutDesc*)D.wdesc + D.wd_off[d][s], D.wd_off[d][s + 1] - D.wd_off[d][s],
+                      D.wcopy + D.wc_off[d][s], D.wc_n[d][s], bufs[s & 1], bufs[(s + 1) & 1], b);
+      halo_n(l, x);
+      return;
+    }
     int prev = 4, s = 0;
     for (int rep = 0; rep < prm.n_c; ++rep)
       for (int cc = 0; cc < 4; ++cc, ++s) {
         const int c = reverse ? 3 - cc : cc;
         cut_pp_step(l, c, prev, bufs[s & 1], bufs[(s + 1) & 1], b);
-        halo(l, bufs[(s + 1) & 1]);
+        halo_n(l, bufs[(s + 1) & 1]);
         prev = c;
       }
   }
 
-  // halo exchange of a lattice vector of a partitioned level (no-op otherwise)
+  // halo exchange of a lattice vector of a partitioned level (no-op
+  // otherwise): the level's halo (wide on wide levels) / the narrow one
   void halo(int l, double* v) {
     if (comm && lv[l].part) comm->exchange(v, lv[l].halo, st);
+  }
+  void halo_n(int l, double* v) {
+    if (comm && lv[l].part) comm->exchange(v, lv[l].halo_n, st);
   }
 
   // x <- S(x, b) (P eq. smoother-split, l.196-210; reverse = adjoint order, R9)
@@ -1243,7 +1370,7 @@ struct Problem {
       return;
     }
     const LevelData& F = lv[l];
-    const int row0 = F.part ? F.v0 : 0, row1 = F.part ? F.v1 : Lf.nl;
+    const int row0 = F.part ? F.v0n : 0, row1 = F.part ? F.v1n : Lf.nl;
     CF_DISPATCH(prm.p, (k_prolongate_add<P><<<dim3(ceil_div(Lf.nl, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
                            Lf, Lc, xc, xf, row0, row1)));
     CF_LAUNCHED();
@@ -1697,7 +1824,7 @@ struct Problem {
       });
       while (it < max_it) {
         graphed(101, cg_p, cg_q, 0, [&]() {
-          halo(Lf, cg_p);
+          halo_n(Lf, cg_p);
           apply(Lf, cg_p, cg_q, nullptr);
           dot(cg_p, cg_q, 1, 0);
           k_cg_update<<<grid, 256, 0, st>>>(cg_x + o, cg_r + o, cg_p + o, cg_q + o, sc, no);

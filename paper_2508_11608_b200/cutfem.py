@@ -237,10 +237,10 @@ class Problem:
         comm._h = _P()   # owned by the problem
 
     def partition_info(self, level=-1):
-        """dict(part, r0, r1, v0, v1, rank, world): owned / valid lattice rows of `level`."""
-        out = (ctypes.c_int * 7)()
+        """dict(part, r0, r1, v0, v1, rank, world, halo): owned / valid lattice rows of `level`."""
+        out = (ctypes.c_int * 8)()
         _check(_lib.cutfem_partition_info(self._h, level % self.n_levels, out))
-        return dict(zip(("part", "r0", "r1", "v0", "v1", "rank", "world"), list(out)))
+        return dict(zip(("part", "r0", "r1", "v0", "v1", "rank", "world", "halo"), list(out)))
 
     def halo_exchange(self, level, v, stream=None):
         _check(_lib.cutfem_halo_exchange(self._h, level % self.n_levels, _dptr(v), _stream(stream)))

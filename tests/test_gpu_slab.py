@@ -110,8 +110,12 @@ def test_partition_layout(w, world):
             assert infos[0]["r0"] == 0 and infos[-1]["r1"] == nl
             for a, b in zip(infos, infos[1:]):
                 assert a["r1"] == b["r0"]
+            s = (infos[0]["r1"] - infos[0]["r0"]) // w.p       # slab thickness in cells
             for i in infos:
-                assert i["v0"] == max(0, i["r0"] - 4 * w.p) and i["v1"] == min(nl, i["r1"] + 4 * w.p + 1)
+                # wide halo (12 n_c cells) where the slab is thick enough, else 4 cells
+                assert i["halo"] == (12 * w.n_c if s >= 12 * w.n_c + 1 else 4)
+                h = i["halo"]
+                assert i["v0"] == max(0, i["r0"] - h * w.p) and i["v1"] == min(nl, i["r1"] + h * w.p + 1)
         else:
             assert all(i["r0"] == 0 and i["r1"] == nl for i in infos)
     top = [g.partition_info(-1)["part"] for g in gs]
@@ -123,11 +127,12 @@ def test_partition_layout(w, world):
 
 TC32 = {"CUTFEM_TC32_MIN_N": "128"}   # 32-cell fused tiles on the 128^2 / 256^2 levels
 SPLIT = {"CUTFEM_CART_SPLIT": "1"}    # two-launch Cartesian sweep through the shadow buffer
+NARROW = {"CUTFEM_WIDE_HALO": "0"}    # one exchange per cut step everywhere
 
 
 @pytest.mark.parametrize("w,world,env", [(W_Q2, 2, None), (W_Q2, 4, None), (W_Q1, 2, None), (W_Q1, 8, None),
                                          (W_Q3, 2, None), (W_OFF, 4, None), (W_Q2, 2, TC32), (W_OFF, 4, TC32),
-                                         (W_Q2, 4, SPLIT)])
+                                         (W_Q2, 4, SPLIT), (W_Q2, 2, NARROW), (W_OFF, 4, NARROW)])
 @pytest.mark.parametrize("reverse", [0, 1])
 def test_smooth_bitexact(w, world, env, reverse):
     L = w.n_levels - 1
@@ -176,7 +181,7 @@ def test_operator_bitexact(w, world):
 
 
 @pytest.mark.parametrize("w,world,env", [(W_Q2, 2, None), (W_Q2, 4, None), (W_Q1, 2, None), (W_Q1, 8, None),
-                                         (W_Q3, 2, None), (W_OFF, 4, None), (W_OFF, 2, TC32)])
+                                         (W_Q3, 2, None), (W_OFF, 4, None), (W_OFF, 2, TC32), (W_OFF, 4, NARROW)])
 def test_vcycle_bitexact(w, world, env):
     b0 = workloads.lattice_vector(w, 31)
     x0 = workloads.lattice_vector(w, 32)
@@ -231,7 +236,7 @@ def test_halo_exchange_rows():
 
     def fn(r, g, s):
         nl, ld = g.lattice_shape(L)
-        v = torch.full((nl * ld,), -1.0, dtype=torch.float64, device="cuda")
+        v = torch.full((nl * ld,), -1.0, dtype=torch.float64, device="cuda")   # (level halo: wide here)
         info = g.partition_info(L)
         rows = torch.arange(nl, dtype=torch.float64, device="cuda").repeat_interleave(ld)
         lo, hi = info["r0"] * ld, info["r1"] * ld
