@@ -1,1 +1,2 @@
-python -m pytest tests/test_gpu_slab.py -x -q > gpurun_out/slab.log 2>&1; tail -25 gpurun_out/slab.log
+python scripts/level_times.py 2>&1 | tail -9
+CUTFEM_CLUSTER_MAX=100000 python scripts/level_times.py 2>&1 | tail -9
