@@ -77,6 +77,7 @@ struct Problem {
   bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
   bool cart_split = false;  // force the two-launch Cartesian sweep through xs (env CUTFEM_CART_SPLIT=1)
   bool wide_halo = true;    // partition: wide-halo cut sweeps where the slabs are thick enough (env CUTFEM_WIDE_HALO=0)
+  bool cut_map = true;      // cut steps through the precomputed dense patch maps, p <= 3 (env CUTFEM_CUTMAP=0)
   // all cut sweeps of a smoothing step in one cooperative launch with grid
   // barriers (env CUTFEM_CUT_GRID=1).  Off: measured 57.5 us vs 43.2 us for
   // one PDL launch per step at config1 (a grid barrier costs more than a
@@ -249,6 +250,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CART_SPLIT")) cart_split = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_WIDE_HALO")) wide_halo = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_CUTMAP")) cut_map = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT_GRID")) cut_grid = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT_GRID_MIN_N")) cut_grid_min_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
@@ -544,6 +546,7 @@ struct Problem {
                                                                           D.cutp_inv, (CutDesc*)D.desc)));
         CF_LAUNCHED();
       }
+      if (ncp && cut_map && prm.cut_mode == 0 && p <= 3) build_cut_maps(D, ncp);
       D.act_desc = D.desc;
       for (int c = 0; c < 5; ++c) D.act_off[c] = D.cutp_off[c];
       build_copy_lists(D, D.ent_node, D.ent_col_off, (const CutDesc*)D.desc, ncp);
@@ -567,6 +570,33 @@ struct Problem {
 
   // ping-pong copy lists (see k_cut_step): [prev][cur] = N_prev \ N_cur for
   // prev, cur colours, and [4][cur] = band \ N_cur for the first step
+  // dense affine maps G_j = [A_j^{-1} | -A_j^{-1} A_{I,W}] of the cut patches
+  // (k_cut_map; offsets stored in the descriptors)
+  void build_cut_maps(LevelData& D, int ncp) {
+    const int p = prm.p, WS = 4 * p + 1, WW = WS * WS;
+    std::vector<CutDesc> hd(ncp);
+    CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
+    int64_t off = 0;
+    for (auto& d : hd) {
+      const int m = __builtin_popcountll(d.mask[0]) + __builtin_popcountll(d.mask[1]);
+      d.map_off = off;
+      off += (int64_t)m * (m + WW);
+    }
+    CF_CUDA(cudaMemcpy(D.desc, hd.data(), sizeof(CutDesc) * ncp, cudaMemcpyHostToDevice));
+    D.gmap = alloc<double>(off);
+    D.n_gmap = off;
+    CF_DISPATCH(p, {
+      if constexpr (P <= 3) {
+        const size_t smb = CutGroup6<P>::bytes;
+        CF_CUDA(cudaFuncSetAttribute(k_cut_map<P, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+        k_cut_map<P, 64><<<dim3(ncp, WW + 1), 64, smb, st>>>(D.a, (const CutDesc*)D.desc, (const double*)D.ecut,
+                                                              (const double*)D.inv, D.gmap);
+        CF_LAUNCHED();
+      }
+    });
+    sync();
+  }
+
   // (ent_node, col_off[0..4]: the interior nodes of the swept patches per
   // colour; desc/ncp: their descriptors)
   void build_copy_lists(LevelData& D, const int32_t* ent_node, const int64_t* col_off, const CutDesc* desc, int ncp) {
@@ -1122,6 +1152,23 @@ struct Problem {
                      const double* b) {
     LevelData& D = lv[l];
     if (!np && !ncopy) return;
+    if (D.gmap && cut_map && prm.cut_mode == 0 && cta_cut) {
+      CF_DISPATCH(prm.p, {
+        if constexpr (P <= 3) {
+          constexpr int NT = P <= 2 ? 64 : 128;
+          const size_t smb = CutMapSmem<P>::bytes;
+          static bool attr7 = false;
+          if (!attr7) {
+            CF_CUDA(cudaFuncSetAttribute(k_cut_step7<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+            attr7 = true;
+          }
+          launch(k_cut_step7<P, NT>, dim3(np + ceil_div(ncopy, NT)), dim3(NT), smb, D.a, desc, np,
+                 (const double*)D.gmap, R, W, b, cl, ncopy);
+          CF_LAUNCHED();
+          return;
+        }
+      });
+    }
     CF_DISPATCH(prm.p, {
       if (prm.cut_mode == 0 && cta_cut) {
         constexpr int NT = 64;

@@ -46,7 +46,9 @@ struct __align__(16) CutDesc {
   int cid[4];              // cut-cell ids of the patch cells (dx + 2 dy), -1 if not cut
   long long inv_off;       // offset of A_j^{-1}
   unsigned long long mask[2];  // interior set as bits over the (2p+1)^2 block, row-major
+  long long map_off;       // offset of the dense patch map G_j (k_cut_map), -1 if none
 };
+static_assert(sizeof(CutDesc) == 64, "CutDesc is one 64-byte line");
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -104,6 +106,7 @@ __global__ void k_cut_desc(LevelArgs L, const int* plist, int np, const int64_t*
   }
   d.e0 = (int)ent_off[k];
   d.inv_off = inv_off[k];
+  d.map_off = -1;
   d.mask[0] = d.mask[1] = 0ull;
   for (int64_t e = ent_off[k]; e < ent_off[k + 1]; ++e) {
     int loc = ent_loc[e];
@@ -1617,6 +1620,9 @@ __device__ __forceinline__ void cut6_prologue(const CutDesc* desc, int k, const 
       for (int e = gt; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
 }
 
+template <int P, int NT>
+__device__ __forceinline__ void cut6_resid(const LevelArgs& L, const SmTab& T, unsigned char* gsm, int gt, int bar);
+
 // main part (after the previous step's W is visible).  LDCG: read the window
 // through L2 only (ld.global.cg) -- inside one launch whose earlier steps
 // wrote R from other SMs, where an L1-cached (cp.async.ca) line could be stale
@@ -1656,6 +1662,41 @@ __device__ __forceinline__ void cut6_main(const LevelArgs& L, const SmTab& T, co
   }
   cp_async_wait_all();
   group_sync(bar, NT);
+  cut6_resid<P, NT>(L, T, gsm, gt, bar);
+  // (4) z = A_j^{-1} r on the interior nodes
+  for (int i = gt; i < m; i += NT) {
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+    int q = 0;
+    for (; q + 3 < m; q += 4) {
+      z0 = fma(Ai[q * m + i], Rr[q], z0);
+      z1 = fma(Ai[(q + 1) * m + i], Rr[q + 1], z1);
+      z2 = fma(Ai[(q + 2) * m + i], Rr[q + 2], z2);
+      z3 = fma(Ai[(q + 3) * m + i], Rr[q + 3], z3);
+    }
+    for (; q < m; ++q) z0 = fma(Ai[q * m + i], Rr[q], z0);
+    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
+    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + ((z0 + z1) + (z2 + z3));
+  }
+}
+
+// phases (1)-(3) of the group routine on the shared-memory window Wp and the
+// interior b values in Rr (Lc: interior locations): Rr <- b - A_{I,W} x_W
+// (cell terms by sum factorisation / cut-cell matrices, ghost-face terms);
+// ends with a group barrier
+template <int P, int NT>
+__device__ __forceinline__ void cut6_resid(const LevelArgs& L, const SmTab& T, unsigned char* gsm, int gt, int bar) {
+  using S = CutGroup6<P>;
+  constexpr int NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, PP = S::PP, N1 = P + 1;
+  const CutDesc& d = *(const CutDesc*)gsm;
+  double* Wp = (double*)(gsm + 128);
+  double* Jm = Wp + WS * WS;
+  double* Yc = Jm + 12 * PP;
+  double* Rr = Yc + 4 * NB;
+  double* Ai = Rr + MM;
+  double* Ec = Ai + MM * MM;
+  short* Lc = (short*)(Ec + 4 * NB * NB);
+  unsigned* gmask = (unsigned*)(Lc + MM + (MM & 1));
+  const int m = mask_count(d);
   // (1) cell parts (jobs < 4 NB) and ghost-face moments
   for (int job = gt; job < 4 * NB + 12 * P; job += NT) {
     if (job < 4 * NB) {
@@ -1743,20 +1784,6 @@ __device__ __forceinline__ void cut6_main(const LevelArgs& L, const SmTab& T, co
     Rr[i] -= y;
   }
   group_sync(bar, NT);
-  // (4) z = A_j^{-1} r on the interior nodes
-  for (int i = gt; i < m; i += NT) {
-    double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-    int q = 0;
-    for (; q + 3 < m; q += 4) {
-      z0 = fma(Ai[q * m + i], Rr[q], z0);
-      z1 = fma(Ai[(q + 1) * m + i], Rr[q + 1], z1);
-      z2 = fma(Ai[(q + 2) * m + i], Rr[q + 2], z2);
-      z3 = fma(Ai[(q + 3) * m + i], Rr[q + 3], z3);
-    }
-    for (; q < m; ++q) z0 = fma(Ai[q * m + i], Rr[q], z0);
-    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
-    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + ((z0 + z1) + (z2 + z3));
-  }
 }
 
 template <int P, int NT>
@@ -1939,6 +1966,147 @@ __global__ void __launch_bounds__(64 * G) k_cut_sweeps_grid(CutSweepArgs A) {
       grid.sync();
     }
     prev = c;
+  }
+}
+
+}  // namespace cf
+
+namespace cf {
+
+// ---- cut patches as dense affine maps (v7) ----------------------------------
+// The cut-patch update of eq. (smoother) is affine in (b, x):
+//   z_j = A_j^{-1} (b_I - A_{I,W} x_W) = G_j [b_I ; x_W],
+//   G_j = [A_j^{-1} | -A_j^{-1} A_{I,W}]   (m_j x (m_j + (4p+1)^2), row-major),
+// with W the (4p+1)^2 window of the patch, so it is precomputed at setup --
+// the cut-patch analogue of the Cartesian patch map -- and a colour step is
+// one gather and one small dense matvec per patch.  Column w of the right
+// block is obtained by running the residual phases of the group routine on
+// the unit window e_w (b = 0) and applying A_j^{-1}: the same arithmetic the
+// matrix-free step performs, so G_j [b; x] equals it up to summation order.
+
+// setup: one CTA per (patch, column); column block y = WS^2 copies A_j^{-1}
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) k_cut_map(LevelArgs L, const CutDesc* desc, const double* ecut,
+                                                const double* inv, double* G) {
+  using S = CutGroup6<P>;
+  constexpr int NB = S::NB, WS = S::WS, MM = S::MM, PP = S::PP, WW = WS * WS;
+  __shared__ SmTab T;
+  extern __shared__ __align__(128) unsigned char smm[];
+  const int tid = threadIdx.x, k = blockIdx.x, w = blockIdx.y;
+  load_smtab<P>(T);
+  cut6_prologue<P, NT>(desc, k, ecut, inv, smm, tid, 0);
+  const CutDesc& d = *(const CutDesc*)smm;
+  double* Wp = (double*)(smm + 128);
+  double* Rr = Wp + WW + 12 * PP + 4 * NB;
+  double* Ai = Rr + MM;
+  short* Lc = (short*)(Ai + MM * MM + 4 * NB * NB);
+  unsigned* gmask = (unsigned*)(Lc + MM + (MM & 1));
+  const int m = mask_count(d), K = m + WW;
+  double* Gj = G + d.map_off;
+  if (tid == 0) *gmask = 0u;
+  for (int e = tid; e < WW; e += NT) Wp[e] = e == w ? 1.0 : 0.0;
+  for (int loc = tid; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if ((word >> (loc & 63)) & 1ull) {
+      const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+      Lc[i] = (short)loc;
+      Rr[i] = 0.0;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (w == WW) {   // A_j^{-1} (stored [q][i], symmetric)
+    for (int e = tid; e < m * m; e += NT) Gj[(size_t)(e / m) * K + e % m] = Ai[(e % m) * m + e / m];
+    return;
+  }
+  cut6_resid<P, NT>(L, T, smm, tid, 0);
+  for (int i = tid; i < m; i += NT) {
+    double z = 0.0;
+    for (int q = 0; q < m; ++q) z = fma(Ai[q * m + i], Rr[q], z);
+    Gj[(size_t)i * K + m + w] = z;
+  }
+}
+
+template <int P>
+struct CutMapSmem {
+  static constexpr int BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, WW = WS * WS;
+  static constexpr int maxK = MM + WW;
+  // descriptor | v[maxK] | G_j[MM x maxK] | Lc[MM] shorts | window mask
+  static constexpr size_t gs_off = 64 + (((size_t)maxK * 8 + 15) & ~(size_t)15);
+  static constexpr size_t bytes = gs_off + (size_t)MM * maxK * 8 + 2 * MM + WW + 16;
+  static constexpr int tpr_max = 4;
+};
+
+// hot path: one cut colour step with the precomputed maps (ping-pong as k_cut_step6)
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* desc, int np, const double* G,
+                                                  const double* R, double* W, const double* b, const int32_t* copy,
+                                                  int ncopy) {
+  using S = CutMapSmem<P>;
+  constexpr int BS = S::BS, WS = S::WS, MM = S::MM, WW = S::WW;
+  extern __shared__ __align__(128) unsigned char sm7[];
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  if ((int)blockIdx.x >= np) {
+    const int e = (blockIdx.x - np) * NT + tid;
+    if (e < ncopy) {
+      const int32_t node = copy[e];
+      pdl_wait();
+      W[node] = R[node];
+    }
+    return;
+  }
+  CutDesc& d = *(CutDesc*)sm7;
+  double* v = (double*)(sm7 + 64);
+  double* Gs = (double*)(sm7 + S::gs_off);
+  short* Lc = (short*)(Gs + (size_t)MM * S::maxK);
+  uint8_t* wm = (uint8_t*)(Lc + MM);
+  if (tid < 4) ((int4*)&d)[tid] = ((const int4*)(desc + blockIdx.x))[tid];
+  __syncthreads();
+  const int m = mask_count(d), K = m + WW;
+  // setup data before the wait: the map, interior locations, window DoF mask
+  const double* Gj = G + d.map_off;
+  for (int e = tid; e < m * K; e += NT) cp_async8(Gs + e, Gj + e);
+  for (int loc = tid; loc < MM; loc += NT) {
+    const unsigned long long word = d.mask[loc >> 6];
+    if ((word >> (loc & 63)) & 1ull)
+      Lc[(loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull))] = (short)loc;
+  }
+  const int a0 = P * (d.I - 2), b0 = P * (d.J - 2);
+  for (int e = tid; e < WW; e += NT) {
+    const int a = a0 + e % WS, bb = b0 + e / WS;
+    wm[e] = (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) ? L.mask[(size_t)bb * L.ld + a] : 0;
+  }
+  __syncthreads();
+  pdl_wait();
+  for (int i = tid; i < m; i += NT) {
+    const int loc = Lc[i];
+    v[i] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
+  }
+  for (int e = tid; e < WW; e += NT)
+    v[m + e] = wm[e] ? R[(size_t)(b0 + e / WS) * L.ld + a0 + e % WS] : 0.0;
+  cp_async_wait_all();
+  __syncthreads();
+  // z = G_j v: TPR threads per row (power of two), shuffle-reduced
+  const int tpr = m * 4 <= NT ? 4 : (m * 2 <= NT ? 2 : 1);
+  for (int r0 = 0; r0 < m; r0 += NT / tpr) {
+    const int i = r0 + tid / tpr, h = tid % tpr;
+    double a0c = 0.0, a1c = 0.0;
+    if (i < m) {
+      const double* g = Gs + (size_t)i * K;
+      int c = h;
+      for (; c + tpr < K; c += 2 * tpr) {
+        a0c = fma(g[c], v[c], a0c);
+        a1c = fma(g[c + tpr], v[c + tpr], a1c);
+      }
+      if (c < K) a0c = fma(g[c], v[c], a0c);
+    }
+    double z = a0c + a1c;
+    for (int o = tpr >> 1; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (i < m && h == 0) {
+      const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
+      W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = v[m + (P + rb) * WS + P + ra] + z;
+    }
   }
 }
 

@@ -1,2 +1,2 @@
-python scripts/level_times.py 2>&1 | tail -9
-CUTFEM_CLUSTER_MAX=100000 python scripts/level_times.py 2>&1 | tail -9
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -15 gpurun_out/gputests.log
+timeout 900 python scripts/ab.py variants/base.so variants/base.so:CUTFEM_CUTMAP=0
