@@ -215,20 +215,25 @@ def main():
     cut_ms = sweeps_ms / n_cut_launch
     # per cut step (one colour): 8 m^2 (inverse) + 8 (2p+1)^2 (x block) + 8 m (b) + 16 m (x read, x write)
     # per patch, + 8 ((p+1)^2)^2 per cut cell (element matrix); averaged over the colours
-    cut_bytes = (float(np.sum(8 * m_all * m_all + 8 * (2 * p + 1) ** 2 + 24 * m_all)) +
-                 8.0 * nb * nb * info.n_cut) / 4.0 / world
+    if sum(info.cut_step_bytes[:4]):
+        # k_cut_step7 (precomputed patch maps): per patch descriptor + map block + gathered
+        # x (nonzero exterior columns) and b + written x, from the library (cut_step_bytes)
+        cut_bytes = float(sum(info.cut_step_bytes[:4])) / 4.0 / world
+    else:
+        cut_bytes = (float(np.sum(8 * m_all * m_all + 8 * (2 * p + 1) ** 2 + 24 * m_all)) +
+                     8.0 * nb * nb * info.n_cut) / 4.0 / world
     per_step = {"cart_sweep": cart_ms, "cut_sweeps": sweeps_ms}
     kernels = {
         "k_cart_fused_tma (4 Cartesian colours, one launch)": {
             "launches_per_step": 1, "avg_launch_ms": cart_ms, "bytes_per_launch": cart_bytes,
             "achieved_gbs": cart_bytes / (cart_ms * 1e-3) / 1e9},
-        "k_cut_step (one cut colour)": {
+        "k_cut_step7 (one cut colour)": {
             "launches_per_step": n_cut_launch, "avg_launch_ms": cut_ms, "bytes_per_launch": cut_bytes,
             "achieved_gbs": cut_bytes / (cut_ms * 1e-3) / 1e9}}
     if per_step["cart_sweep"] >= per_step["cut_sweeps"]:
         dom, d_bytes, d_ms = "k_cart_fused_tma<P=%d> (fused Cartesian sweep)" % p, cart_bytes, cart_ms
     else:
-        dom, d_bytes, d_ms = "k_cut_step<P=%d> (cut colour step)" % p, cut_bytes, cut_ms
+        dom, d_bytes, d_ms = ("k_cut_step7<P=%d> (cut colour step, patch maps)" % p if sum(info.cut_step_bytes[:4]) else "k_cut_step6<P=%d> (cut colour step)" % p), cut_bytes, cut_ms
     achieved = d_bytes / (d_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")

@@ -81,6 +81,9 @@ typedef struct {
   int n_cutp[8];        /* cut patches per colour */
   int64_t n_vol_qp, n_surf_qp; /* cut-cell quadrature points (R6) */
   double h;
+  int64_t cut_step_bytes[8];   /* algorithmic bytes of one cut colour step per colour with the
+                                  precomputed patch maps (descriptor, map, gathered x and b,
+                                  written x per patch); 0 without maps */
 } cutfem_level_info;
 
 /* ---- setup ------------------------------------------------------------ */

@@ -127,6 +127,7 @@ int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out) 
       out->n_cart[c] = D.n_cart[c];
       out->n_cutp[c] = D.n_cutp[c];
     }
+    for (int c = 0; c < 8; ++c) out->cut_step_bytes[c] = D.gmap ? D.cut_bytes[c] : 0;
     out->n_vol_qp = D.n_vq;
     out->n_surf_qp = D.n_sq;
     out->h = D.a.h;

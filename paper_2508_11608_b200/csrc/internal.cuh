@@ -130,6 +130,7 @@ struct LevelData {
   double* ecut = nullptr;            // cut-cell element matrices
   double* gmap = nullptr;            // dense cut-patch maps G_j (k_cut_map), CutDesc::map_off
   int64_t n_gmap = 0;
+  int64_t cut_bytes[8] = {};         // algorithmic bytes of one cut colour step (k_cut_step7) per colour
   void* desc = nullptr;              // CutDesc per cut patch (smoother2.cuh)
   double* xs = nullptr;              // shadow lattice vector for the ping-pong cut steps
   int32_t* copy_lists = nullptr;     // node lists: [prev][cur] = N_prev \ N_cur (prev = 4: read band)

@@ -576,25 +576,55 @@ struct Problem {
     const int p = prm.p, WS = 4 * p + 1, WW = WS * WS;
     std::vector<CutDesc> hd(ncp);
     CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
-    int64_t off = 0;
-    for (auto& d : hd) {
-      const int m = __builtin_popcountll(d.mask[0]) + __builtin_popcountll(d.mask[1]);
-      d.map_off = off;
-      off += (int64_t)m * (m + WW);
+    // dense maps first (k_cut_map), then the compressed blocks
+    std::vector<int64_t> dense(ncp + 1, 0);
+    std::vector<int> hm(ncp);
+    for (int k = 0; k < ncp; ++k) {
+      hm[k] = __builtin_popcountll(hd[k].mask[0]) + __builtin_popcountll(hd[k].mask[1]);
+      hd[k].map_off = dense[k];
+      dense[k + 1] = dense[k] + (int64_t)hm[k] * (hm[k] + WW);
     }
     CF_CUDA(cudaMemcpy(D.desc, hd.data(), sizeof(CutDesc) * ncp, cudaMemcpyHostToDevice));
-    D.gmap = alloc<double>(off);
-    D.n_gmap = off;
+    double* Gd = alloc<double>(dense[ncp]);
+    int64_t* doff = alloc<int64_t>(ncp + 1);
+    int* nnz = alloc<int>(ncp);
+    CF_CUDA(cudaMemcpy(doff, dense.data(), sizeof(int64_t) * (ncp + 1), cudaMemcpyHostToDevice));
+    std::vector<int> hn(ncp);
     CF_DISPATCH(p, {
       if constexpr (P <= 3) {
         const size_t smb = CutGroup6<P>::bytes;
         CF_CUDA(cudaFuncSetAttribute(k_cut_map<P, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
         k_cut_map<P, 64><<<dim3(ncp, WW + 1), 64, smb, st>>>(D.a, (const CutDesc*)D.desc, (const double*)D.ecut,
-                                                              (const double*)D.inv, D.gmap);
+                                                              (const double*)D.inv, Gd);
+        CF_LAUNCHED();
+        k_map_nnz<P><<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, doff, Gd, nnz);
+        CF_LAUNCHED();
+        CF_CUDA(cudaMemcpyAsync(hn.data(), nnz, sizeof(int) * ncp, cudaMemcpyDeviceToHost, st));
+        sync();
+        int64_t off = 0;
+        for (int c = 0; c < 8; ++c) D.cut_bytes[c] = 0;
+        for (int k = 0; k < ncp; ++k) {
+          hd[k].map_off = off;
+          const int64_t blk = 1 + (hn[k] + 7) / 8 + (int64_t)hm[k] * (hm[k] + hn[k]);
+          off += blk;
+          // algorithmic bytes of the patch in its colour step: descriptor, map block,
+          // gathered window and b values, written interior values
+          int c = 0;
+          while (c < 3 && k >= D.cutp_off[c + 1]) ++c;
+          D.cut_bytes[c] += 64 + 8 * blk + 8 * (int64_t)hn[k] + 16 * (int64_t)hm[k];
+        }
+        CF_CUDA(cudaMemcpy(D.desc, hd.data(), sizeof(CutDesc) * ncp, cudaMemcpyHostToDevice));
+        D.gmap = alloc<double>(off);
+        D.n_gmap = off;
+        k_map_compact<P><<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, doff, Gd, D.gmap);
         CF_LAUNCHED();
       }
     });
     sync();
+    for (void* q : {(void*)Gd, (void*)doff, (void*)nnz}) {
+      cudaFree(q);
+      allocs.erase(std::remove(allocs.begin(), allocs.end(), q), allocs.end());
+    }
   }
 
   // (ent_node, col_off[0..4]: the interior nodes of the swept patches per

@@ -2027,17 +2027,90 @@ __global__ void __launch_bounds__(NT) k_cut_map(LevelArgs L, const CutDesc* desc
   }
 }
 
+// Compression of the maps: the interior columns of -A_j^{-1} A_{I,W} are -I
+// (A_{I,I} = A_j), so x_I^new = x_I + z_j = A_j^{-1} (b_I - A_{I,E} x_E) over
+// the exterior window nodes E; of those only the columns with a nonzero entry
+// (nodes coupled to the interior through a patch cell or a ghost face) are
+// kept.  Compressed block of patch j at map_off:
+//   [int32 nnz, pad][nnz uint8 window indices, padded to 8 bytes]
+//   [m_j x (m_j + nnz) rows: A_j^{-1} | -A_j^{-1} A_{I,E'}]
+template <int P>
+__device__ __forceinline__ bool window_interior(const CutDesc& d, int w) {
+  constexpr int WS = 4 * P + 1, BS = 2 * P + 1;
+  const int r = w / WS - P, c = w % WS - P;
+  if (r < 0 || c < 0 || r >= BS || c >= BS) return false;
+  const int loc = r * BS + c;
+  return (d.mask[loc >> 6] >> (loc & 63)) & 1ull;
+}
+
+// nonzero exterior columns of the dense map (one CTA per patch)
+template <int P>
+__global__ void k_map_nnz(const CutDesc* desc, const int64_t* dense_off, const double* Gd, int* nnz) {
+  constexpr int WW = (4 * P + 1) * (4 * P + 1);
+  const CutDesc d = desc[blockIdx.x];
+  const int m = mask_count(d), K = m + WW;
+  const double* g = Gd + dense_off[blockIdx.x];
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int w = threadIdx.x; w < WW; w += blockDim.x) {
+    if (window_interior<P>(d, w)) continue;
+    bool nz = false;
+    for (int i = 0; i < m && !nz; ++i) nz = g[(size_t)i * K + m + w] != 0.0;
+    if (nz) atomicAdd(&cnt, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) nnz[blockIdx.x] = cnt;
+}
+
+template <int P>
+__global__ void k_map_compact(const CutDesc* desc, const int64_t* dense_off, const double* Gd, double* Gc) {
+  constexpr int WW = (4 * P + 1) * (4 * P + 1);
+  const CutDesc d = desc[blockIdx.x];
+  const int m = mask_count(d), K = m + WW;
+  const double* g = Gd + dense_off[blockIdx.x];
+  double* out = Gc + d.map_off;
+  __shared__ uint8_t keep[WW];
+  __shared__ uint8_t idx[WW];
+  __shared__ int nnz;
+  for (int w = threadIdx.x; w < WW; w += blockDim.x) {
+    bool nz = false;
+    if (!window_interior<P>(d, w))
+      for (int i = 0; i < m && !nz; ++i) nz = g[(size_t)i * K + m + w] != 0.0;
+    keep[w] = nz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int w = 0; w < WW; ++w)
+      if (keep[w]) idx[c++] = (uint8_t)w;
+    nnz = c;
+    ((int*)out)[0] = c;
+    ((int*)out)[1] = 0;
+    uint8_t* ob = (uint8_t*)(out + 1);
+    for (int q = 0; q < ((c + 7) & ~7); ++q) ob[q] = q < c ? idx[q] : 0;
+  }
+  __syncthreads();
+  const int Kc = m + nnz;
+  double* rows = out + 1 + (nnz + 7) / 8;
+  for (int e = threadIdx.x; e < m * Kc; e += blockDim.x) {
+    const int i = e / Kc, c = e - i * Kc;
+    rows[e] = c < m ? g[(size_t)i * K + c] : g[(size_t)i * K + m + idx[c - m]];
+  }
+}
+
 template <int P>
 struct CutMapSmem {
   static constexpr int BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, WW = WS * WS;
   static constexpr int maxK = MM + WW;
-  // descriptor | v[maxK] | G_j[MM x maxK] | Lc[MM] shorts | window mask
+  // descriptor | v[maxK] | G_j rows [MM x maxK] | Lc[MM] shorts | exterior indices, window mask
   static constexpr size_t gs_off = 64 + (((size_t)maxK * 8 + 15) & ~(size_t)15);
-  static constexpr size_t bytes = gs_off + (size_t)MM * maxK * 8 + 2 * MM + WW + 16;
-  static constexpr int tpr_max = 4;
+  static constexpr size_t bytes = gs_off + (size_t)MM * maxK * 8 + 2 * MM + 2 * WW + 16;
 };
 
-// hot path: one cut colour step with the precomputed maps (ping-pong as k_cut_step6)
+// hot path: one cut colour step with the precomputed maps (ping-pong as
+// k_cut_step6): x_I^new = G_j [b_I ; x_E'] gathered after the wait, the map,
+// interior locations, exterior indices and DoF mask fetched before it
 template <int P, int NT>
 __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* desc, int np, const double* G,
                                                   const double* R, double* W, const double* b, const int32_t* copy,
@@ -2060,22 +2133,26 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
   double* v = (double*)(sm7 + 64);
   double* Gs = (double*)(sm7 + S::gs_off);
   short* Lc = (short*)(Gs + (size_t)MM * S::maxK);
-  uint8_t* wm = (uint8_t*)(Lc + MM);
+  uint8_t* ix = (uint8_t*)(Lc + MM);
+  uint8_t* wm = ix + WW;
   if (tid < 4) ((int4*)&d)[tid] = ((const int4*)(desc + blockIdx.x))[tid];
   __syncthreads();
-  const int m = mask_count(d), K = m + WW;
-  // setup data before the wait: the map, interior locations, window DoF mask
-  const double* Gj = G + d.map_off;
-  for (int e = tid; e < m * K; e += NT) cp_async8(Gs + e, Gj + e);
+  const int m = mask_count(d);
+  const double* blk = G + d.map_off;
+  const int nnz = ((const int*)blk)[0], K = m + nnz;
+  const double* rows = blk + 1 + (nnz + 7) / 8;
+  for (int e = tid; e < m * K; e += NT) cp_async8(Gs + e, rows + e);
   for (int loc = tid; loc < MM; loc += NT) {
     const unsigned long long word = d.mask[loc >> 6];
     if ((word >> (loc & 63)) & 1ull)
       Lc[(loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull))] = (short)loc;
   }
   const int a0 = P * (d.I - 2), b0 = P * (d.J - 2);
-  for (int e = tid; e < WW; e += NT) {
-    const int a = a0 + e % WS, bb = b0 + e / WS;
-    wm[e] = (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) ? L.mask[(size_t)bb * L.ld + a] : 0;
+  for (int j = tid; j < nnz; j += NT) {
+    const int w = ((const uint8_t*)(blk + 1))[j];
+    const int a = a0 + w % WS, bb = b0 + w / WS;
+    ix[j] = (uint8_t)w;
+    wm[j] = (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) ? L.mask[(size_t)bb * L.ld + a] : 0;
   }
   __syncthreads();
   pdl_wait();
@@ -2083,11 +2160,13 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
     const int loc = Lc[i];
     v[i] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
   }
-  for (int e = tid; e < WW; e += NT)
-    v[m + e] = wm[e] ? R[(size_t)(b0 + e / WS) * L.ld + a0 + e % WS] : 0.0;
+  for (int j = tid; j < nnz; j += NT) {
+    const int w = ix[j];
+    v[m + j] = wm[j] ? R[(size_t)(b0 + w / WS) * L.ld + a0 + w % WS] : 0.0;
+  }
   cp_async_wait_all();
   __syncthreads();
-  // z = G_j v: TPR threads per row (power of two), shuffle-reduced
+  // x_I^new = G_j v: TPR threads per row (power of two), shuffle-reduced
   const int tpr = m * 4 <= NT ? 4 : (m * 2 <= NT ? 2 : 1);
   for (int r0 = 0; r0 < m; r0 += NT / tpr) {
     const int i = r0 + tid / tpr, h = tid % tpr;
@@ -2104,8 +2183,8 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
     double z = a0c + a1c;
     for (int o = tpr >> 1; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
     if (i < m && h == 0) {
-      const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
-      W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = v[m + (P + rb) * WS + P + ra] + z;
+      const int loc = Lc[i];
+      W[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS] = z;
     }
   }
 }
