@@ -604,7 +604,7 @@ struct Problem {
         int64_t off = 0;
         for (int c = 0; c < 8; ++c) D.cut_bytes[c] = 0;
         for (int k = 0; k < ncp; ++k) {
-          hd[k].map_off = off;
+          hd[k].map_off = off | ((int64_t)hn[k] << 48);
           const int64_t blk = 1 + (hn[k] + 7) / 8 + (int64_t)hm[k] * (hm[k] + hn[k]);
           off += blk;
           // algorithmic bytes of the patch in its colour step: descriptor, map block,
@@ -614,6 +614,7 @@ struct Problem {
           D.cut_bytes[c] += 64 + 8 * blk + 8 * (int64_t)hn[k] + 16 * (int64_t)hm[k];
         }
         CF_CUDA(cudaMemcpy(D.desc, hd.data(), sizeof(CutDesc) * ncp, cudaMemcpyHostToDevice));
+        require(off < (1ll << 48), ERR_SIZE, "cut-patch maps exceed 2^48 doubles");
         D.gmap = alloc<double>(off);
         D.n_gmap = off;
         k_map_compact<P><<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, doff, Gd, D.gmap);

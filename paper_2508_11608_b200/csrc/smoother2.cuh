@@ -46,7 +46,7 @@ struct __align__(16) CutDesc {
   int cid[4];              // cut-cell ids of the patch cells (dx + 2 dy), -1 if not cut
   long long inv_off;       // offset of A_j^{-1}
   unsigned long long mask[2];  // interior set as bits over the (2p+1)^2 block, row-major
-  long long map_off;       // offset of the dense patch map G_j (k_cut_map), -1 if none
+  long long map_off;       // patch map G_j: offset (bits 0-47) | exterior columns nnz << 48; -1 if none
 };
 static_assert(sizeof(CutDesc) == 64, "CutDesc is one 64-byte line");
 
@@ -2069,7 +2069,7 @@ __global__ void k_map_compact(const CutDesc* desc, const int64_t* dense_off, con
   const CutDesc d = desc[blockIdx.x];
   const int m = mask_count(d), K = m + WW;
   const double* g = Gd + dense_off[blockIdx.x];
-  double* out = Gc + d.map_off;
+  double* out = Gc + (d.map_off & ((1ll << 48) - 1));
   __shared__ uint8_t keep[WW];
   __shared__ uint8_t idx[WW];
   __shared__ int nnz;
@@ -2134,12 +2134,14 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
   double* Gs = (double*)(sm7 + S::gs_off);
   short* Lc = (short*)(Gs + (size_t)MM * S::maxK);
   uint8_t* ix = (uint8_t*)(Lc + MM);
-  uint8_t* wm = ix + WW;
   if (tid < 4) ((int4*)&d)[tid] = ((const int4*)(desc + blockIdx.x))[tid];
   __syncthreads();
   const int m = mask_count(d);
-  const double* blk = G + d.map_off;
-  const int nnz = ((const int*)blk)[0], K = m + nnz;
+  // the kept exterior columns are DoF nodes inside the lattice (a column is
+  // nonzero only if its node shares an active cell or a ghost face with the
+  // interior), so the gather needs no mask
+  const double* blk = G + (d.map_off & ((1ll << 48) - 1));
+  const int nnz = (int)(d.map_off >> 48), K = m + nnz;
   const double* rows = blk + 1 + (nnz + 7) / 8;
   for (int e = tid; e < m * K; e += NT) cp_async8(Gs + e, rows + e);
   for (int loc = tid; loc < MM; loc += NT) {
@@ -2148,12 +2150,7 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
       Lc[(loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull))] = (short)loc;
   }
   const int a0 = P * (d.I - 2), b0 = P * (d.J - 2);
-  for (int j = tid; j < nnz; j += NT) {
-    const int w = ((const uint8_t*)(blk + 1))[j];
-    const int a = a0 + w % WS, bb = b0 + w / WS;
-    ix[j] = (uint8_t)w;
-    wm[j] = (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) ? L.mask[(size_t)bb * L.ld + a] : 0;
-  }
+  for (int j = tid; j < nnz; j += NT) ix[j] = ((const uint8_t*)(blk + 1))[j];
   __syncthreads();
   pdl_wait();
   for (int i = tid; i < m; i += NT) {
@@ -2162,7 +2159,7 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
   }
   for (int j = tid; j < nnz; j += NT) {
     const int w = ix[j];
-    v[m + j] = wm[j] ? R[(size_t)(b0 + w / WS) * L.ld + a0 + w % WS] : 0.0;
+    v[m + j] = R[(size_t)(b0 + w / WS) * L.ld + a0 + w % WS];
   }
   cp_async_wait_all();
   __syncthreads();
