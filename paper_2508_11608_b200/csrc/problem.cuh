@@ -22,6 +22,7 @@
 #include "dim3.cuh"
 #include "tables.cuh"
 #include "comm.cuh"
+#include "vcycle_cluster.cuh"
 
 namespace cf {
 
@@ -78,6 +79,13 @@ struct Problem {
   bool cart_split = false;  // force the two-launch Cartesian sweep through xs (env CUTFEM_CART_SPLIT=1)
   bool wide_halo = true;    // partition: wide-halo cut sweeps where the slabs are thick enough (env CUTFEM_WIDE_HALO=0)
   bool cut_map = true;      // cut steps through the precomputed dense patch maps, p <= 3 (env CUTFEM_CUTMAP=0)
+  // V-cycle levels with n <= this run in one cluster launch (env
+  // CUTFEM_VC_MAX_N; 0 = off).  Off by default: measured 1014 us (n <= 64) and
+  // 903 us (n <= 32) per config1 V-cycle vs 722 us with one PDL launch per
+  // step -- the cluster phases expose the dependent loads of the patch maps
+  // that the launch path issues before griddepcontrol.wait
+  int vc_max_n = 0;
+  int vc_cluster = 16;      // CTAs of that cluster (non-portable 16; falls back to 8)
   // all cut sweeps of a smoothing step in one cooperative launch with grid
   // barriers (env CUTFEM_CUT_GRID=1).  Off: measured 57.5 us vs 43.2 us for
   // one PDL launch per step at config1 (a grid barrier costs more than a
@@ -251,6 +259,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_CART_SPLIT")) cart_split = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_WIDE_HALO")) wide_halo = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUTMAP")) cut_map = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_VC_MAX_N")) vc_max_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_CUT_GRID")) cut_grid = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT_GRID_MIN_N")) cut_grid_min_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
@@ -566,6 +575,7 @@ struct Problem {
     for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
     sync();
     built = true;
+    if (prm.dim == 2) prepare_vc();
   }
 
   // ping-pong copy lists (see k_cut_step): [prev][cur] = N_prev \ N_cur for
@@ -776,6 +786,7 @@ struct Problem {
     require(prm.dim == 2, ERR_ARG, "the slab partition is implemented for 2D problems");
     require(built, ERR_STATE, "cutfem_build_patches has not been called");
     require(comm == nullptr, ERR_STATE, "the problem is already partitioned");
+    vc_built_top = -1;
     require(c->world >= 1 && c->rank >= 0 && c->rank < c->world, ERR_ARG, "bad rank / world");
     const int W = c->world, R = c->rank, p = prm.p;
     fused = true;
@@ -787,7 +798,9 @@ struct Problem {
     for (int l = prm.n_levels - 1; l >= 1; --l) {
       LevelData& D = lv[l];
       const int n = D.a.n, nl = D.a.nl, ld = D.a.ld, s = n / W, TC = D.tc;
-      const bool ok = finer && n % W == 0 && s % TC == 0 && s >= HALO + 1;
+      // (levels the cluster V-cycle covers stay replicated: one launch, no exchanges)
+      const bool vc_level = vc_max_n > 0 && prm.cut_mode == 0 && p <= 3 && cut_map && n <= vc_max_n;
+      const bool ok = finer && n % W == 0 && s % TC == 0 && s >= HALO + 1 && !vc_level;
       finer = ok;
       if (!ok) continue;
       D.part = 1;
@@ -874,6 +887,7 @@ struct Problem {
       D.at1 = std::min(nt, ceil_div(D.c1 + 2, 16));
     }
     comm = c;
+    prepare_vc();
   }
 
   void build_coarse() {
@@ -1458,10 +1472,95 @@ struct Problem {
     CF_LAUNCHED();
   }
 
+  // coarse end of the V-cycle in one cluster launch (vcycle_cluster.cuh):
+  // the highest level it covers (0 = not used)
+  int vc_top() {
+    if (vc_max_n <= 0 || prm.dim != 2 || prm.cut_mode != 0 || prm.p > 3 || !cut_map) return 0;
+    int top = 0;
+    for (int l = 1; l < prm.n_levels; ++l) {
+      const LevelData& D = lv[l];
+      if (D.a.n > vc_max_n || D.part || (D.act_off[4] > 0 && !D.gmap)) break;
+      top = l;
+    }
+    return top;
+  }
+  CoarseLevel* vc_levels = nullptr;
+  int vc_built_top = -1;
+  // per-level arguments of the cluster V-cycle (built outside any graph capture:
+  // at the end of build_patches and of partition)
+  void prepare_vc() {
+    const int top = vc_top();
+    if (top > 0) {
+      std::vector<CoarseLevel> h(top + 1);
+      for (int l = 0; l <= top; ++l) {
+        const LevelData& D = lv[l];
+        CoarseLevel& V = h[l];
+        std::memset(&V, 0, sizeof(V));
+        V.L = D.a;
+        V.cart_list = D.cart_list;
+        for (int c = 0; c < 5; ++c) {
+          V.cart_off[c] = D.cart_off[c];
+          V.cut_off[c] = D.act_off[c];
+        }
+        V.desc = (const CutDesc*)D.act_desc;
+        V.gmap = D.gmap;
+        V.copy = D.copy_lists;
+        for (int i = 0; i < 5; ++i)
+          for (int c = 0; c < 4; ++c) {
+            V.copy_off[i][c] = D.copy_off[i][c];
+            V.copy_n[i][c] = D.copy_n[i][c];
+          }
+        V.x = D.x;
+        V.b = D.b;
+        V.r = D.r;
+        V.xs = D.xs;
+      }
+      if (!vc_levels) vc_levels = alloc<CoarseLevel>(VC_MAXL);
+      require(top < VC_MAXL, ERR_SIZE, "too many cluster V-cycle levels");
+      CF_CUDA(cudaMemcpy(vc_levels, h.data(), sizeof(CoarseLevel) * (top + 1), cudaMemcpyHostToDevice));
+    }
+    vc_built_top = top;
+  }
+  void vcycle_cluster(int top, double* x, const double* b) {
+    require(vc_built_top == top, ERR_STATE, "cluster V-cycle arguments not prepared");
+    CoarseArgs A;
+    A.lv = vc_levels;
+    A.lmax = top;
+    A.n_c = prm.n_c;
+    A.symmetric = prm.symmetric;
+    A.Gc = host::cart_map(prm.p);
+    A.c_inv = c_inv;
+    A.c_nodes = c_nodes;
+    A.n0 = n0;
+    A.x = x;
+    A.b = b;
+    CF_DISPATCH(prm.p, {
+      if constexpr (P <= 3) {
+        static bool attr = false;
+        if (!attr) {
+          CF_CUDA(cudaFuncSetAttribute(k_vcycle_cluster<P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          attr = true;
+        }
+        cudaError_t e = launch_cluster(k_vcycle_cluster<P>, vc_cluster, dim3(256), 0, A);
+        if (e != cudaSuccess) {
+          (void)cudaGetLastError();
+          require(vc_cluster > 8, ERR_CUDA, "cluster launch of the coarse V-cycle failed");
+          vc_cluster = 8;
+          CF_CUDA(launch_cluster(k_vcycle_cluster<P>, vc_cluster, dim3(256), 0, A));
+        }
+        CF_LAUNCHED();
+      }
+    });
+  }
+
   // V-cycle on level l with initial guess x (P l.124, l.217)
   void vcycle(int l, double* x, const double* b) {
     if (l == 0) {
       coarse_solve(b, x);
+      return;
+    }
+    if (const int top = vc_top(); top > 0 && l == top) {
+      vcycle_cluster(top, x, b);
       return;
     }
     LevelData& D = lv[l];
@@ -1786,6 +1885,7 @@ struct Problem {
     for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
     sync();
     built = true;
+    if (prm.dim == 2) prepare_vc();
   }
 
   void apply3(int l, const double* x, double* y, const double* b) {

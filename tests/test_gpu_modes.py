@@ -52,10 +52,10 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
                                  {"CUTFEM_CUT2": "5", "CUTFEM_CLUSTER_MAX": "0"}, {"CUTFEM_CLUSTER_MAX": "512"},
                                  {"CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CART_SPLIT": "1", "CUTFEM_TMA": "0"},
                                  {"CUTFEM_CART_SPLIT": "1", "CUTFEM_MMA": "0"}, {"CUTFEM_TC32_MIN_N": "32"},
-                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CUT_GRID": "1"}, {"CUTFEM_CUTMAP": "0"}],
+                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CUT_GRID": "1"}, {"CUTFEM_CUTMAP": "0"}, {"CUTFEM_VC_MAX_N": "0"}],
                          ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply",
                               "cut-step-v4", "cut-step-v5", "cluster-cut-sweeps", "cart-split-tma",
-                              "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split", "cut-sweeps-one-grid-launch", "cut-step-matrix-free"])
+                              "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split", "cut-sweeps-one-grid-launch", "cut-step-matrix-free", "vcycle-launch-per-step"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
@@ -132,3 +132,28 @@ def test_cart_split_equals_inplace_fullsize():
         outs.append(g.to_host(x))
         g.close()
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("vc_max_n", ["0", "16", "64", "100000"], ids=["launches", "n<=16", "n<=64", "all-levels"])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_vcycle_cluster_levels(vc_max_n, p):
+    """coarse end of the V-cycle in one cluster launch (vcycle_cluster.cuh) for
+    0 / some / all levels: V-cycle vs the oracle's, identical CG iterations"""
+    from paper_2508_11608_b200 import cutfem
+    w = workloads.paper_level(p, 7 if p > 1 else 6)
+    os.environ["CUTFEM_VC_MAX_N"] = vc_max_n
+    try:
+        g = cutfem.Problem.from_workload(w)
+    finally:
+        os.environ.pop("CUTFEM_VC_MAX_N", None)
+    o = from_workload(w)
+    lf = o.fine.lv
+    bl = lattice_random(w, 77, None)
+    x = g.zeros()
+    g.vcycle(x, g.to_device(bl))
+    assert rel_err(compact(lf, g.to_host(x)), o.precondition(compact(lf, bl))) < 10 * TOL
+    xs = g.zeros()
+    it, rel = g.solve_cg_mg(xs, g.to_device(bl), tol=1e-8, max_it=200)
+    xo, ito, _ = o.solve_cg(compact(lf, bl), 1e-8, 200)
+    assert it == ito and rel <= 1e-8
+    assert rel_err(compact(lf, g.to_host(xs)), xo) < 1e-7
