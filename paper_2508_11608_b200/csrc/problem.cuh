@@ -46,6 +46,9 @@ int64_t g_launches = 0;
 
 template <int P> constexpr int cart_tp() { return P == 1 ? 16 : (P == 2 ? 8 : (P == 3 ? 7 : 6)); }
 constexpr int CUT_WPB = 4;
+#ifndef CF_CART_NT32
+#define CF_CART_NT32 256   // threads of the fused Cartesian CTA with 32-cell tiles (512 measured slower)
+#endif
 // fused Cartesian tile (cells per side); p = 2 uses 32-cell tiles on large
 // levels of the TMA/tensor-core sweep (Problem::tc_big_n) and 16 otherwise
 template <int P> constexpr int fused_tc() { return P == 1 ? 32 : (P <= 3 ? 16 : 8); }
@@ -214,11 +217,11 @@ struct Problem {
   }
   // CTAs of `kern` (256 threads, smem bytes) that fit on the device at once
   template <typename K>
-  int coresident(K kern, size_t smem) {
+  int coresident(K kern, size_t smem, int threads = 256) {
     int nsm = 0, dev = 0, per = 0;
     CF_CUDA(cudaGetDevice(&dev));
     CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem));
     return per * nsm;
   }
 
@@ -1081,22 +1084,23 @@ struct Problem {
   template <int P, int TC>
   void cart_fused_tma(int l, double* x, const double* b, int reverse) {
     LevelData& D = lv[l];
+    constexpr int NT = TC >= 32 ? CF_CART_NT32 : 256;
     const double* G = host::cart_map(P);
     using S = CartTmaSmem<P, TC>;
     const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
     const CUtensorMap tmb = host::lattice_tmap(b, D.a.nl, D.a.ld, S::RWP, S::RW);
     static int cap = -1;
     if (cap < 0) {
-      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
-      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      cap = coresident(k_cart_fused_tma<P, TC>, S::bytes);
+      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      cap = coresident(k_cart_fused_tma<P, TC, NT>, S::bytes, NT);
     }
     if (verbose) {
       std::fprintf(stderr, "[cutfem] level %d: %d fused tiles (%d ext), %d co-resident -> %s\n", l,
                    D.n_fused_tiles, D.n_fused_ext, cap, (!cart_split && D.n_fused_tiles <= cap) ? "in place" : "split");
     }
     if (!cart_split && D.n_fused_tiles <= cap) {
-      launch_ex(true, k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tmx, tmb, D.a,
+      launch_ex(true, k_cart_fused_tma<P, TC, NT>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
                 (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, 1);
       CF_LAUNCHED();
       cart_done(l, x, reverse);
@@ -1104,11 +1108,11 @@ struct Problem {
     }
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
     if (D.n_fused_ext)
-      launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_ext), dim3(256), S::bytes, tmx, tmb, D.a,
+      launch(k_cart_fused_tma<P, TC, NT>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
              (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, 0);
     CF_LAUNCHED();
     halo_n(l, D.xs);
-    launch(k_cart_fused_tma<P, TC>, dim3(D.n_fused_tiles), dim3(256), S::bytes, tms, tmb, D.a,
+    launch(k_cart_fused_tma<P, TC, NT>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
            (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, 0);
     CF_LAUNCHED();
     cart_done(l, x, reverse);

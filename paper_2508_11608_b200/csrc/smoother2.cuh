@@ -1058,8 +1058,8 @@ struct CartTmaSmem {
 // cooperative launch: the grid barrier before the write keeps every CTA's
 // apron load ahead of its neighbours' writes.  Otherwise the sweep is split
 // into two launches through the shadow buffer (passes 0-1 x -> xs, 2-3 xs -> x).
-template <int P, int TC>
-__global__ void __launch_bounds__(256, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
+template <int P, int TC, int NT = 256>
+__global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* xout, int reverse, int s0, int s1, int gsync) {
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__(256, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused
     // compact the Cartesian patches of this pass
     if (tid == 0) *pcount = 0;
     __syncthreads();
-    for (int q = tid; q < nvx * nvy; q += 256) {
+    for (int q = tid; q < nvx * nvy; q += NT) {
       const int pj = q / nvx, pi = q - pj * nvx;
       const int I = ilo + 2 * pi, J = jlo + 2 * pj;
       if (I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART)
@@ -1123,7 +1123,7 @@ __global__ void __launch_bounds__(256, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused
     if (s == s0) mbar_wait(bar, 0);
     __syncthreads();
     const int np = *pcount, ng = (np + 7) / 8;
-    for (int g = warp; g < ng; g += 8) {
+    for (int g = warp; g < ng; g += NT / 32) {
       const int pq = 8 * g + (lane >> 2);
       const int base = pq < np ? plist[pq] : -1;
       double acc[MF > 0 ? MF : 1][2][2];
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(256, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused
   if (gsync) cooperative_groups::this_grid().sync();
   // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
   const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
-  for (int bb = P * cj0 + warp; bb < bhi; bb += 8) {
+  for (int bb = P * cj0 + warp; bb < bhi; bb += NT / 32) {
     const double* src = Xs + (bb - b0) * RWP - a0;
     double* dst = xout + (size_t)bb * L.ld;
     for (int a = P * ci0 + lane; a < ahi; a += 32) dst[a] = src[a];
