@@ -582,7 +582,8 @@ __global__ void k_prolongate_add(LevelArgs Lf, LevelArgs Lc, const double* xc, d
 // b_c = P^T r_f: one thread per coarse node gathers the fine nodes of the
 // support of its basis function with weights phi^c(x_f) (tensor of 1D).
 template <int P>
-__global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double* bc, int row0, int row1) {
+__global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double* bc, int row0, int row1,
+                           double* xz /* optional: zeroed at the same entries (the coarse initial guess) */) {
   __shared__ double tw[P][4 * P + 1];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   if (tid < P * (4 * P + 1)) tw[tid / (4 * P + 1)][tid % (4 * P + 1)] = c_tab[P].tw[tid / (4 * P + 1)][tid % (4 * P + 1)];
@@ -590,6 +591,7 @@ __global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double*
   const int A = blockIdx.x * blockDim.x + threadIdx.x, B = row0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (A >= Lc.ld || B >= row1) return;
   const size_t o = (size_t)B * Lc.ld + A;
+  if (xz) xz[o] = 0.0;
   if (A >= Lc.nl || !Lc.mask[o]) {
     bc[o] = 0.0;
     return;

@@ -1443,7 +1443,7 @@ struct Problem {
     }
   }
 
-  void restrict_(int l, const double* rf, double* bc) {
+  void restrict_(int l, const double* rf, double* bc, double* xz = nullptr) {
     const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
     if (prm.dim == 3) {
       const int64_t nv = (int64_t)Lc.nl * Lc.nl * Lc.ld;
@@ -1454,7 +1454,7 @@ struct Problem {
     const LevelData& F = lv[l];
     const int row0 = F.part ? F.rc0 : 0, row1 = F.part ? F.rc1 : Lc.nl;
     CF_DISPATCH(prm.p, (k_restrict<P><<<dim3(ceil_div(Lc.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
-                           Lf, Lc, rf, bc, row0, row1)));
+                           Lf, Lc, rf, bc, row0, row1, xz)));
     CF_LAUNCHED();
   }
   void prolongate_add(int l, const double* xc, double* xf) {
@@ -1571,12 +1571,15 @@ struct Problem {
     LevelData& C = lv[l - 1];
     smooth(l, x, b, 0);
     apply(l, x, D.r, b);
-    restrict_(l, D.r, C.b);
+    // the restriction also zeroes the coarse initial guess (no memset node
+    // between the kernels, which would break the programmatic launch chain)
+    const bool zero_in_restrict = !D.part && prm.dim == 2;
+    restrict_(l, D.r, C.b, zero_in_restrict ? C.x : nullptr);
     if (D.part) {
       if (C.part) halo(l - 1, C.b);
       else replicate(l - 1, C.b, D.rc0, D.rc1);   // the coarse levels run on every rank
     }
-    CF_CUDA(cudaMemsetAsync(C.x, 0, vsize(l - 1) * 8, st));
+    if (!zero_in_restrict) CF_CUDA(cudaMemsetAsync(C.x, 0, vsize(l - 1) * 8, st));
     vcycle(l - 1, C.x, C.b);
     prolongate_add(l, C.x, x);
     smooth(l, x, b, prm.symmetric ? 1 : 0);
