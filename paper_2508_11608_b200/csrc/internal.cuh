@@ -44,6 +44,13 @@ __device__ Tab g_tab[CF_MAXP + 1];   // global-memory copy for lane-varying (coa
 __constant__ double c_gx[CF_MAXNQ + 1][CF_MAXNQ];  // Gauss-Legendre points on [0,1], c_gx[n][i]
 __constant__ double c_gw[CF_MAXNQ + 1][CF_MAXNQ];
 
+// PDL: wait until the preceding kernel in the stream has completed (no-op
+// when launched without the programmatic-serialization attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// PDL: allow the next kernel in the stream to be scheduled (its own wait
+// still orders it after this kernel's completion)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // Per-level arguments passed by value to every kernel.
 struct LevelArgs {
   int n, p, nl, ld;

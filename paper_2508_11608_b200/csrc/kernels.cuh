@@ -476,6 +476,8 @@ __global__ void __launch_bounds__(128) k_band(LevelArgs L, const double* x, Band
   __shared__ double sX[4][NB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw0 = blockIdx.x * 4 + w;
+  pdl_trigger();
+  pdl_wait();
   if (gw0 < R.cut_n) {
     const int gw = R.cut_lo + gw0;
     const int c = L.cut_list[gw], i = c % L.n, j = c / L.n;
@@ -520,8 +522,10 @@ __global__ void __launch_bounds__(256) k_node_apply(LevelArgs L, const double* x
                                                     int row1) {
   constexpr int NB = (P + 1) * (P + 1);
   __shared__ SmTab T;
+  pdl_trigger();
   load_smtab<P>(T);
   __syncthreads();
+  pdl_wait();
   const int a = blockIdx.x * blockDim.x + threadIdx.x, bb = row0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (a >= L.ld || bb >= row1) return;
   const size_t o = (size_t)bb * L.ld + a;
@@ -560,8 +564,10 @@ template <int P>
 __global__ void k_prolongate_add(LevelArgs Lf, LevelArgs Lc, const double* xc, double* xf, int row0, int row1) {
   __shared__ double pw[2 * P + 1][P + 1];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  pdl_trigger();
   if (tid < (2 * P + 1) * (P + 1)) pw[tid / (P + 1)][tid % (P + 1)] = c_tab[P].pw[tid / (P + 1)][tid % (P + 1)];
   __syncthreads();
+  pdl_wait();
   const int a = blockIdx.x * blockDim.x + threadIdx.x, bb = row0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (a >= Lf.nl || bb >= row1) return;
   const size_t o = (size_t)bb * Lf.ld + a;
@@ -586,8 +592,10 @@ __global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double*
                            double* xz /* optional: zeroed at the same entries (the coarse initial guess) */) {
   __shared__ double tw[P][4 * P + 1];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  pdl_trigger();
   if (tid < P * (4 * P + 1)) tw[tid / (4 * P + 1)][tid % (4 * P + 1)] = c_tab[P].tw[tid / (4 * P + 1)][tid % (4 * P + 1)];
   __syncthreads();
+  pdl_wait();
   const int A = blockIdx.x * blockDim.x + threadIdx.x, B = row0 + blockIdx.y * blockDim.y + threadIdx.y;
   if (A >= Lc.ld || B >= row1) return;
   const size_t o = (size_t)B * Lc.ld + A;

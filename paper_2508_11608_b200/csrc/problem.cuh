@@ -942,9 +942,9 @@ struct Problem {
     const int warps = R.cut_n + ceil_div(R.g_n0 + R.g_n1, 32);
     if (warps) {
       if (prm.cut_mode == 0) {
-        CF_DISPATCH(p, (k_band<P, false><<<ceil_div(warps, 4), 128, 0, st>>>(L, x, R)));
+        CF_DISPATCH(p, launch(k_band<P, false>, dim3(ceil_div(warps, 4)), dim3(128), 0, L, x, R));
       } else {
-        CF_DISPATCH(p, (k_band<P, true><<<ceil_div(warps, 4), 128, 0, st>>>(L, x, R)));
+        CF_DISPATCH(p, launch(k_band<P, true>, dim3(ceil_div(warps, 4)), dim3(128), 0, L, x, R));
       }
       CF_LAUNCHED();
     }
@@ -968,8 +968,8 @@ struct Problem {
       return;
     }
     const int row0 = D.part ? std::max(0, (D.c0 - 2) * p) : 0, row1 = D.part ? std::min(L.nl, (D.c1 + 2) * p + 1) : L.nl;
-    CF_DISPATCH(p, (k_node_apply<P><<<dim3(ceil_div(L.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
-                       L, x, b, y, row0, row1)));
+    CF_DISPATCH(p, launch(k_node_apply<P>, dim3(ceil_div(L.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, L, x, b,
+                          y, row0, row1));
     CF_LAUNCHED();
   }
 
@@ -1453,8 +1453,8 @@ struct Problem {
     }
     const LevelData& F = lv[l];
     const int row0 = F.part ? F.rc0 : 0, row1 = F.part ? F.rc1 : Lc.nl;
-    CF_DISPATCH(prm.p, (k_restrict<P><<<dim3(ceil_div(Lc.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
-                           Lf, Lc, rf, bc, row0, row1, xz)));
+    CF_DISPATCH(prm.p, launch(k_restrict<P>, dim3(ceil_div(Lc.ld, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, Lf,
+                              Lc, rf, bc, row0, row1, xz));
     CF_LAUNCHED();
   }
   void prolongate_add(int l, const double* xc, double* xf) {
@@ -1467,8 +1467,8 @@ struct Problem {
     }
     const LevelData& F = lv[l];
     const int row0 = F.part ? F.v0n : 0, row1 = F.part ? F.v1n : Lf.nl;
-    CF_DISPATCH(prm.p, (k_prolongate_add<P><<<dim3(ceil_div(Lf.nl, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0, st>>>(
-                           Lf, Lc, xc, xf, row0, row1)));
+    CF_DISPATCH(prm.p, launch(k_prolongate_add<P>, dim3(ceil_div(Lf.nl, 32), ceil_div(row1 - row0, 8)), dim3(32, 8), 0,
+                              Lf, Lc, xc, xf, row0, row1));
     CF_LAUNCHED();
   }
   void coarse_solve(const double* b, double* x) {

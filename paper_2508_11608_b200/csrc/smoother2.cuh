@@ -56,12 +56,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// PDL: wait until the preceding kernel in the stream has completed (no-op
-// when launched without the programmatic-serialization attribute)
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-// PDL: allow the next kernel in the stream to be scheduled (its own wait
-// still orders it after this kernel's completion)
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 __device__ __forceinline__ int desc_kind(const CutDesc& d, int wx, int wy) {
   return (d.kinds >> (2 * (wy * 4 + wx))) & 3;
