@@ -803,7 +803,13 @@ struct Problem {
       const int n = D.a.n, nl = D.a.nl, ld = D.a.ld, s = n / W, TC = D.tc;
       // (levels the cluster V-cycle covers stay replicated: one launch, no exchanges)
       const bool vc_level = vc_max_n > 0 && prm.cut_mode == 0 && p <= 3 && cut_map && n <= vc_max_n;
-      const bool ok = finer && n % W == 0 && s % TC == 0 && s >= HALO + 1 && !vc_level;
+      // With the wide halo (default) only slabs thick enough for it are
+      // partitioned: a thinner level would need an exchange per cut step
+      // (4 n_c + 1 per smoothing step), which costs more than computing the
+      // whole (small) level on every rank; CUTFEM_WIDE_HALO=0 partitions every
+      // level of >= HALO + 1 rows with the narrow halo instead.
+      const int S = 4 * prm.n_c, HW = 3 * S;   // wide halo: 3 cells per cut step (see build_wide)
+      const bool ok = finer && n % W == 0 && s % TC == 0 && s >= (wide_halo ? HW : HALO) + 1 && !vc_level;
       finer = ok;
       if (!ok) continue;
       D.part = 1;
@@ -811,8 +817,7 @@ struct Problem {
       D.c1 = D.c0 + s;
       D.r0 = D.c0 * p;
       D.r1 = R == W - 1 ? nl : D.c1 * p;
-      const int S = 4 * prm.n_c, HW = 3 * S;   // wide halo: 3 cells per cut step (see build_wide)
-      D.wide = wide_halo && s >= HW + 1;
+      D.wide = wide_halo;
       D.hw = D.wide ? HW : HALO;
       D.v0n = std::max(0, D.r0 - HALO * p);
       D.v1n = std::min(nl, D.r1 + HALO * p + 1);

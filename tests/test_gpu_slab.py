@@ -112,8 +112,8 @@ def test_partition_layout(w, world):
                 assert a["r1"] == b["r0"]
             s = (infos[0]["r1"] - infos[0]["r0"]) // w.p       # slab thickness in cells
             for i in infos:
-                # wide halo (12 n_c cells) where the slab is thick enough, else 4 cells
-                assert i["halo"] == (12 * w.n_c if s >= 12 * w.n_c + 1 else 4)
+                # only slabs thick enough for the wide halo (12 n_c cells) are partitioned
+                assert i["halo"] == 12 * w.n_c and s >= 12 * w.n_c + 1
                 h = i["halo"]
                 assert i["v0"] == max(0, i["r0"] - h * w.p) and i["v1"] == min(nl, i["r1"] + h * w.p + 1)
         else:
