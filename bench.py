@@ -103,14 +103,16 @@ def oracle_sample(steps):
     b = workloads.lattice_vector(w, 2)[lv.dof_nodes]
     x = workloads.lattice_vector(w, 1)[lv.dof_nodes]
     times = []
-    for _ in range(max(1, steps)):
-        t0 = time.perf_counter()
-        ld.smooth(x, b, w.n_c)
-        times.append(time.perf_counter() - t0)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):   # one core: the `cores` the line reports
+        for _ in range(max(1, steps)):
+            t0 = time.perf_counter()
+            ld.smooth(x, b, w.n_c)
+            times.append(time.perf_counter() - t0)
     sec = float(np.mean(times))
     return {"value": lv.n_dofs / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"oracle smoothing step on level {ORACLE_SAMPLE_LEVEL} ({lv.n}x{lv.n} cells, {lv.n_dofs} DoFs) "
-                      f"of the {WORKLOAD.name} hierarchy, mean of {len(times)} steps, numpy/scipy single process"}, sec
+                      f"of the {WORKLOAD.name} hierarchy, mean of {len(times)} steps, numpy/scipy, one process, BLAS limited to 1 thread"}, sec
 
 
 def run_reference(args, rank, world):
