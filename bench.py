@@ -158,7 +158,6 @@ def main():
     g = cutfem.Problem.from_workload(w)
     if world > 1:   # slab partition of the mesh over the ranks (NCCL halo exchanges inside the library)
         g.partition(cutfem.Comm.nccl_from_torch(dist))
-        args.no_3d = True
     L = w.n_levels - 1
     info = g.level_info(L)
     nl, ld = info.nl, info.ld
@@ -284,13 +283,15 @@ def main():
         g.close()
         w3 = workloads.CONFIG2
         g3 = cutfem.Problem.from_workload(w3)
+        if world > 1:   # z-slabs over the ranks
+            g3.partition(cutfem.Comm.nccl_from_torch(dist))
         L3 = w3.n_levels - 1
         i3 = g3.level_info(L3)
         x3 = g3.to_device(workloads.lattice_vector(w3, 1))
         b3 = g3.to_device(workloads.lattice_vector(w3, 2))
-        ms3 = timed(lambda: g3.smooth(L3, x3, b3), 10, 3)
+        ms3 = max_over_ranks(float(np.mean(timed(lambda: g3.smooth(L3, x3, b3), 10, 3))), dist, "cuda")
         z3 = g3.zeros()
-        v3 = timed(lambda: (z3.zero_(), g3.vcycle(z3, b3)), 3, 1)
+        v3 = max_over_ranks(float(np.median(timed(lambda: (z3.zero_(), g3.vcycle(z3, b3)), 3, 1))), dist, "cuda")
         xs3 = g3.zeros()
         g3.solve_cg_mg(xs3, b3, tol=w3.tol)
         torch.cuda.synchronize()
@@ -299,16 +300,19 @@ def main():
         it3, rel3 = g3.solve_cg_mg(xs3, b3, tol=w3.tol)
         c1.record(stream)
         torch.cuda.synchronize()
-        cart3 = float(np.mean(timed(lambda: g3.colour_step(L3, 0, 0, x3, b3), 10, 2)))
-        # Cartesian colour step: x read over the colour's blocks (~ all active nodes),
-        # b read and x written on the colour's interiors (~ 1/8 of the nodes each)
-        cart3_bytes = 8.0 * i3.n_dofs * (1.0 + 2.0 / 8.0)
+        cg3 = max_over_ranks(c0.elapsed_time(c1), dist, "cuda")
         cfg3 = {"workload": w3.name, "n_dofs": int(i3.n_dofs), "cells_per_side": i3.n, "degree": w3.p,
-                "smoothing_dofs_per_s": i3.n_dofs / (float(np.mean(ms3)) * 1e-3),
-                "ms_per_step": float(np.mean(ms3)), "vcycle_ms": float(np.median(v3)),
-                "cg_mg": {"time_to_solution_ms": c0.elapsed_time(c1), "iterations": it3, "rel_residual": rel3},
-                "cart_colour_ms": cart3, "cart_colour_achieved_gbs": cart3_bytes / (cart3 * 1e-3) / 1e9,
-                "l2": "flushed before every timed step (vectors 142 MB > L2)"}
+                "smoothing_dofs_per_s": i3.n_dofs / (ms3 * 1e-3), "ms_per_step": ms3, "vcycle_ms": v3,
+                "cg_mg": {"time_to_solution_ms": cg3, "iterations": it3, "rel_residual": rel3},
+                "parallelism": f"z-slabs over {world} GPUs (NCCL halo exchange per colour step)" if world > 1
+                else "single GPU", "l2": "flushed before every timed step (vectors 142 MB > L2)"}
+        if world == 1:
+            cart3 = float(np.mean(timed(lambda: g3.colour_step(L3, 0, 0, x3, b3), 10, 2)))
+            # Cartesian colour step: x read over the colour's blocks (~ all active nodes),
+            # b read and x written on the colour's interiors (~ 1/8 of the nodes each)
+            cart3_bytes = 8.0 * i3.n_dofs * (1.0 + 2.0 / 8.0)
+            cfg3["cart_colour_ms"] = cart3
+            cfg3["cart_colour_achieved_gbs"] = cart3_bytes / (cart3 * 1e-3) / 1e9
         g3.close()
 
     if rank == 0:

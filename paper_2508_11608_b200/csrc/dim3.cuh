@@ -729,14 +729,21 @@ __global__ void __launch_bounds__(128) k_cart_colour3(LevelArgs L, const int* pl
 }
 
 // ---- operator: band (cut cells + ghost faces) and node gather ---------------
+// R: cut cells [cut_lo, cut_lo + cut_n) and ghost faces of the three axes
+// [g_lo[a], g_lo[a] + g_n[a]) (a rank's planes under the slab partition)
+struct BandRange3 {
+  int cut_lo, cut_n, g_lo[3], g_n[3];
+};
+
 template <int P>
-__global__ void __launch_bounds__(128) k_band3(LevelArgs L, const double* x) {
+__global__ void __launch_bounds__(128) k_band3(LevelArgs L, const double* x, BandRange3 R) {
   constexpr int N1 = P + 1, NB = N1 * N1 * N1;
   __shared__ double sX[4][NB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * 4 + w;
+  const int gw0 = blockIdx.x * 4 + w;
   const int n = L.n, nl = L.nl, ld = L.ld;
-  if (gw < L.n_cut) {
+  if (gw0 < R.cut_n) {
+    const int gw = R.cut_lo + gw0;
     const int64_t c = L.cut_list[gw];
     const int i = c % n, j = (c / n) % n, k = c / ((int64_t)n * n);
     for (int t = lane; t < NB; t += 32)
@@ -750,8 +757,12 @@ __global__ void __launch_bounds__(128) k_band3(LevelArgs L, const double* x) {
     }
     return;
   }
-  const int g = (gw - L.n_cut) * 32 + lane;
-  if (g >= L.n_ghost) return;
+  int kk = (gw0 - R.cut_n) * 32 + lane, g = -1;
+  for (int a = 0; a < 3 && g < 0; ++a) {
+    if (kk < R.g_n[a]) g = R.g_lo[a] + kk;
+    else kk -= R.g_n[a];
+  }
+  if (g < 0) return;
   const int64_t n3 = (int64_t)n * n * n, f = L.ghost_list[g];
   const int axis = (int)(f / n3);
   const int64_t c = f - axis * n3;
@@ -762,14 +773,15 @@ __global__ void __launch_bounds__(128) k_band3(LevelArgs L, const double* x) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(256) k_node_apply3(LevelArgs L, const double* x, const double* b, double* y) {
+__global__ void __launch_bounds__(256) k_node_apply3(LevelArgs L, const double* x, const double* b, double* y,
+                                                     int64_t o0, int64_t o1) {
   constexpr int N1 = P + 1, NB = N1 * N1 * N1;
   __shared__ SmTab T;
   load_smtab<P>(T);
   __syncthreads();
-  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t o = o0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int nl = L.nl, ld = L.ld, n = L.n;
-  if (o >= (int64_t)nl * nl * ld) return;
+  if (o >= o1) return;
   if (!L.mask[o]) {
     y[o] = 0.0;
     return;
@@ -806,13 +818,13 @@ __global__ void __launch_bounds__(256) k_node_apply3(LevelArgs L, const double* 
 
 // ---- transfer in 3D ---------------------------------------------------------
 template <int P>
-__global__ void k_prolongate_add3(LevelArgs Lf, LevelArgs Lc, const double* xc, double* xf) {
+__global__ void k_prolongate_add3(LevelArgs Lf, LevelArgs Lc, const double* xc, double* xf, int64_t o0, int64_t o1) {
   __shared__ double pw[2 * P + 1][P + 1];
   if (threadIdx.x < (2 * P + 1) * (P + 1)) pw[threadIdx.x / (P + 1)][threadIdx.x % (P + 1)] = g_tab[P].pw[threadIdx.x / (P + 1)][threadIdx.x % (P + 1)];
   __syncthreads();
-  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t o = o0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int nl = Lf.nl, ld = Lf.ld;
-  if (o >= (int64_t)nl * nl * ld) return;
+  if (o >= o1) return;
   if (!Lf.mask[o]) return;
   const int a = o % ld, bb = (o / ld) % nl, cc = o / ((int64_t)ld * nl);
   const int Ia = min(min(a / P, Lf.n - 1) / 2, Lc.n - 1), Ib = min(min(bb / P, Lf.n - 1) / 2, Lc.n - 1),
@@ -833,13 +845,13 @@ __global__ void k_prolongate_add3(LevelArgs Lf, LevelArgs Lc, const double* xc, 
 }
 
 template <int P>
-__global__ void k_restrict3(LevelArgs Lf, LevelArgs Lc, const double* rf, double* bc) {
+__global__ void k_restrict3(LevelArgs Lf, LevelArgs Lc, const double* rf, double* bc, int64_t o0, int64_t o1) {
   __shared__ double tw[P][4 * P + 1];
   if (threadIdx.x < P * (4 * P + 1)) tw[threadIdx.x / (4 * P + 1)][threadIdx.x % (4 * P + 1)] = g_tab[P].tw[threadIdx.x / (4 * P + 1)][threadIdx.x % (4 * P + 1)];
   __syncthreads();
-  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t o = o0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int nl = Lc.nl, ld = Lc.ld;
-  if (o >= (int64_t)nl * nl * ld) return;
+  if (o >= o1) return;
   const int A = o % ld, B = (o / ld) % nl, Cc = o / ((int64_t)ld * nl);
   if (A >= nl || !Lc.mask[o]) {
     bc[o] = 0.0;

@@ -157,7 +157,12 @@ struct LevelData {
   int band[6] = {0, 0, 0, 0, 0, 0};  // k_band range (BandRange): cut cells, two ghost-face ranges
   int at0 = 0, at1 = 0;              // tile rows of the TMA operator (k_apply_tile)
   const void* act_desc = nullptr;    // cut-patch descriptors the sweeps run (this rank's subset)
-  int act_off[5] = {0, 0, 0, 0, 0};
+  int act_off[9] = {};               // ... per colour (4 in 2D, 8 in 3D)
+  const int* act_cart = nullptr;     // 3D: Cartesian patches the colour steps run, per colour at act_cart_off
+  int act_cart_off[9] = {};
+  const int32_t* act_ent = nullptr;  // 3D: interior nodes of the swept cut patches (scatter list), per colour
+  int64_t act_ent_off[9] = {};
+  int band3[8] = {};                 // 3D k_band ranges (BandRange3)
   std::vector<Xfer> halo;            // transfers of one halo exchange (hw cells)
   std::vector<Xfer> halo_n;          // ... of the narrow halo
   const void* wdesc = nullptr;       // wide-halo cut sweeps: descriptors of step s of direction d

@@ -785,9 +785,124 @@ struct Problem {
   // the slab boundary are computed by both neighbours, identically), cut cells
   // and ghost faces within HALO cells.  Lattice vectors are full-size; the
   // rows [v0, v1) = owned rows + HALO cells are valid after a halo exchange.
+  // doubles per lattice row of the partitioned direction (a row in 2D, a plane in 3D)
+  int64_t rowsz(int l) const {
+    const LevelArgs& L = lv[l].a;
+    return (int64_t)L.ld * (prm.dim == 3 ? L.nl : 1);
+  }
+
+  // 3D: slabs of z-planes; narrow halo, one exchange per colour step; the
+  // rank runs the Cartesian and cut patches with vertex planes [c0 - 1, c1]
+  // (compact descriptor / scatter lists with renumbered zbuf offsets)
+  void partition3(Comm* c) {
+    const int W = c->world, R = c->rank, p = prm.p;
+    bool finer = true;
+    for (int l = prm.n_levels - 1; l >= 1; --l) {
+      LevelData& D = lv[l];
+      const int n = D.a.n, nl = D.a.nl, s = n / W, nv = n + 1;
+      const int64_t ps = rowsz(l);
+      const bool ok = finer && n % W == 0 && s >= HALO + 1;
+      finer = ok;
+      if (!ok) continue;
+      D.part = 1;
+      D.c0 = R * s;
+      D.c1 = D.c0 + s;
+      D.r0 = D.c0 * p;
+      D.r1 = R == W - 1 ? nl : D.c1 * p;
+      D.wide = 0;
+      D.hw = HALO;
+      D.v0 = D.v0n = std::max(0, D.r0 - HALO * p);
+      D.v1 = D.v1n = std::min(nl, D.r1 + HALO * p + 1);
+      D.rc0 = p * (D.c0 / 2);
+      D.rc1 = R == W - 1 ? lv[l - 1].a.nl : p * (D.c1 / 2);
+      const int64_t hr = (int64_t)HALO * p;
+      D.halo.clear();
+      if (R > 0) D.halo.push_back({R - 1, D.r0 * ps, (hr + 1) * ps, (D.r0 - hr) * ps, hr * ps});
+      if (R < W - 1) D.halo.push_back({R + 1, (D.r1 - hr) * ps, hr * ps, D.r1 * ps, (hr + 1) * ps});
+      D.halo_n = D.halo;
+      auto keepK = [&](int K) { return K >= D.c0 - 1 && K <= D.c1; };
+      // Cartesian patches
+      {
+        const int nc = D.cart_off[8];
+        std::vector<int> h(nc), k;
+        if (nc) CF_CUDA(cudaMemcpy(h.data(), D.cart_list, sizeof(int) * nc, cudaMemcpyDeviceToHost));
+        D.act_cart_off[0] = 0;
+        for (int cc = 0; cc < 8; ++cc) {
+          for (int q = D.cart_off[cc]; q < D.cart_off[cc + 1]; ++q)
+            if (keepK(h[q] / (nv * nv))) k.push_back(h[q]);
+          D.act_cart_off[cc + 1] = (int)k.size();
+        }
+        int* dl = alloc<int>(k.size());
+        if (!k.empty()) CF_CUDA(cudaMemcpy(dl, k.data(), sizeof(int) * k.size(), cudaMemcpyHostToDevice));
+        D.act_cart = dl;
+      }
+      // cut patches: compact descriptors (zbuf offsets renumbered) and scatter list
+      {
+        const int ncp = D.cutp_off[8];
+        std::vector<CutDesc3> hd(ncp), kd;
+        std::vector<int64_t> he(ncp + 1);
+        std::vector<int32_t> hn(D.n_ent), kn;
+        if (ncp) {
+          CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc3) * ncp, cudaMemcpyDeviceToHost));
+          CF_CUDA(cudaMemcpy(he.data(), D.cutp_ent, sizeof(int64_t) * (ncp + 1), cudaMemcpyDeviceToHost));
+        }
+        if (D.n_ent) CF_CUDA(cudaMemcpy(hn.data(), D.ent_node, sizeof(int32_t) * D.n_ent, cudaMemcpyDeviceToHost));
+        D.act_off[0] = 0;
+        D.act_ent_off[0] = 0;
+        for (int cc = 0; cc < 8; ++cc) {
+          for (int k = D.cutp_off[cc]; k < D.cutp_off[cc + 1]; ++k)
+            if (keepK(hd[k].K)) {
+              CutDesc3 d = hd[k];
+              d.e0 = (int)kn.size();
+              kd.push_back(d);
+              kn.insert(kn.end(), hn.begin() + he[k], hn.begin() + he[k + 1]);
+            }
+          D.act_off[cc + 1] = (int)kd.size();
+          D.act_ent_off[cc + 1] = (int64_t)kn.size();
+        }
+        CutDesc3* dd = alloc<CutDesc3>(kd.size());
+        int32_t* dn = alloc<int32_t>(kn.size());
+        if (!kd.empty()) CF_CUDA(cudaMemcpy(dd, kd.data(), sizeof(CutDesc3) * kd.size(), cudaMemcpyHostToDevice));
+        if (!kn.empty()) CF_CUDA(cudaMemcpy(dn, kn.data(), sizeof(int32_t) * kn.size(), cudaMemcpyHostToDevice));
+        D.act_desc = dd;
+        D.act_ent = dn;
+      }
+      // k_band3 ranges: cut cells and x/y-faces of the planes [c0 - HALO, c1 + HALO),
+      // z-faces (k | k+1) with k in [c0 - HALO, c1 + HALO - 1); lists sorted by (k n + j) n + i
+      {
+        const int lo = std::max(0, D.c0 - HALO), hi = std::min(n, D.c1 + HALO);
+        const int zhi = std::max(lo, std::min(n - 1, D.c1 + HALO - 1));
+        const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
+        std::vector<int64_t> hc(D.a.n_cut), hg(D.a.n_ghost);
+        {
+          std::vector<int> t(D.a.n_cut), u(D.a.n_ghost);
+          if (D.a.n_cut) CF_CUDA(cudaMemcpy(t.data(), D.cut_list, sizeof(int) * D.a.n_cut, cudaMemcpyDeviceToHost));
+          if (D.a.n_ghost) CF_CUDA(cudaMemcpy(u.data(), D.ghost_list, sizeof(int) * D.a.n_ghost, cudaMemcpyDeviceToHost));
+          for (size_t q = 0; q < t.size(); ++q) hc[q] = (uint32_t)t[q];
+          for (size_t q = 0; q < u.size(); ++q) hg[q] = (uint32_t)u[q];
+        }
+        auto range = [](const std::vector<int64_t>& v, int64_t a, int64_t b, int& first, int& cnt) {
+          first = (int)(std::lower_bound(v.begin(), v.end(), a) - v.begin());
+          cnt = (int)(std::lower_bound(v.begin(), v.end(), b) - v.begin()) - first;
+        };
+        range(hc, lo * n2, hi * n2, D.band3[0], D.band3[1]);
+        range(hg, 0 * n3 + lo * n2, 0 * n3 + hi * n2, D.band3[2], D.band3[5]);
+        range(hg, 1 * n3 + lo * n2, 1 * n3 + hi * n2, D.band3[3], D.band3[6]);
+        range(hg, 2 * n3 + lo * n2, 2 * n3 + zhi * n2, D.band3[4], D.band3[7]);
+      }
+    }
+    comm = c;
+  }
+
   void partition(Comm* c) {
-    require(prm.dim == 2, ERR_ARG, "the slab partition is implemented for 2D problems");
+    require(prm.dim == 2 || prm.dim == 3, ERR_ARG, "the slab partition needs a 2D or 3D problem");
     require(built, ERR_STATE, "cutfem_build_patches has not been called");
+    if (prm.dim == 3) {
+      require(comm == nullptr, ERR_STATE, "the problem is already partitioned");
+      require(c->world >= 1 && c->rank >= 0 && c->rank < c->world, ERR_ARG, "bad rank / world");
+      partition3(c);
+      return;
+    }
     require(comm == nullptr, ERR_STATE, "the problem is already partitioned");
     vc_built_top = -1;
     require(c->world >= 1 && c->rank >= 0 && c->rank < c->world, ERR_ARG, "bad rank / world");
@@ -1452,7 +1567,10 @@ struct Problem {
     const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
     if (prm.dim == 3) {
       const int64_t nv = (int64_t)Lc.nl * Lc.nl * Lc.ld;
-      CF_DISPATCH3(prm.p, (k_restrict3<P><<<ceil_div(nv, 128), 128, 0, st>>>(Lf, Lc, rf, bc)));
+      const LevelData& F = lv[l];
+      const int64_t ps = (int64_t)Lc.nl * Lc.ld;
+      const int64_t o0 = F.part ? F.rc0 * ps : 0, o1 = F.part ? F.rc1 * ps : nv;
+      CF_DISPATCH3(prm.p, (k_restrict3<P><<<ceil_div(o1 - o0, 128), 128, 0, st>>>(Lf, Lc, rf, bc, o0, o1)));
       CF_LAUNCHED();
       return;
     }
@@ -1466,7 +1584,10 @@ struct Problem {
     const LevelArgs &Lf = lv[l].a, &Lc = lv[l - 1].a;
     if (prm.dim == 3) {
       const int64_t nv = (int64_t)Lf.nl * Lf.nl * Lf.ld;
-      CF_DISPATCH3(prm.p, (k_prolongate_add3<P><<<ceil_div(nv, 128), 128, 0, st>>>(Lf, Lc, xc, xf)));
+      const LevelData& F = lv[l];
+      const int64_t ps = (int64_t)Lf.nl * Lf.ld;
+      const int64_t o0 = F.part ? F.v0n * ps : 0, o1 = F.part ? F.v1n * ps : nv;
+      CF_DISPATCH3(prm.p, (k_prolongate_add3<P><<<ceil_div(o1 - o0, 128), 128, 0, st>>>(Lf, Lc, xc, xf, o0, o1)));
       CF_LAUNCHED();
       return;
     }
@@ -1637,7 +1758,7 @@ struct Problem {
   void dot(const double* a, const double* b, int mode, int slot) {
     const LevelData& F = lv[prm.n_levels - 1];
     if (comm && F.part) {   // owned rows, then the sum over ranks
-      const int64_t o = (int64_t)F.r0 * F.a.ld, n = (int64_t)(F.r1 - F.r0) * F.a.ld;
+      const int64_t rs = rowsz(prm.n_levels - 1), o = F.r0 * rs, n = (F.r1 - F.r0) * rs;
       k_dot_partial<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(a + o, b + o, n, part);
       CF_LAUNCHED();
       k_dot_final<<<1, DOT_THREADS, 0, st>>>(part, sc, 0, 7);
@@ -1656,9 +1777,10 @@ struct Problem {
   // v (a replicated level) <- sum over ranks of the rows [r0, r1) each rank computed
   void replicate(int l, double* v, int r0, int r1) {
     const LevelArgs& L = lv[l].a;
-    if (r0 > 0) CF_CUDA(cudaMemsetAsync(v, 0, (size_t)r0 * L.ld * 8, st));
-    if (r1 < L.nl) CF_CUDA(cudaMemsetAsync(v + (size_t)r1 * L.ld, 0, (size_t)(L.nl - r1) * L.ld * 8, st));
-    comm->allreduce_sum(v, (int64_t)L.nl * L.ld, st);
+    const int64_t rs = rowsz(l);
+    if (r0 > 0) CF_CUDA(cudaMemsetAsync(v, 0, (size_t)(r0 * rs) * 8, st));
+    if (r1 < L.nl) CF_CUDA(cudaMemsetAsync(v + r1 * rs, 0, (size_t)((L.nl - r1) * rs) * 8, st));
+    comm->allreduce_sum(v, vsize(l), st);
   }
 
   // ================================================================ 3D
@@ -1882,6 +2004,14 @@ struct Problem {
                                                                             D.cutp_inv, (CutDesc3*)D.desc)));
         CF_LAUNCHED();
       }
+      D.act_desc = D.desc;
+      D.act_cart = D.cart_list;
+      D.act_ent = D.ent_node;
+      for (int c = 0; c < 9; ++c) {
+        D.act_off[c] = D.cutp_off[c];
+        D.act_cart_off[c] = D.cart_off[c];
+        D.act_ent_off[c] = D.ent_col_off[c];
+      }
       sync();
     }
     build_coarse();
@@ -1901,30 +2031,43 @@ struct Problem {
   }
 
   void apply3(int l, const double* x, double* y, const double* b) {
-    const LevelArgs& L = lv[l].a;
-    const int warps = L.n_cut + ceil_div(L.n_ghost, 32);
+    const LevelData& D = lv[l];
+    const LevelArgs& L = D.a;
+    BandRange3 R;
+    if (D.part) {
+      R = BandRange3{D.band3[0], D.band3[1], {D.band3[2], D.band3[3], D.band3[4]}, {D.band3[5], D.band3[6], D.band3[7]}};
+    } else {
+      // the full ghost list, split by axis is not needed: one range covers it
+      R = BandRange3{0, L.n_cut, {0, 0, 0}, {L.n_ghost, 0, 0}};
+    }
+    const int warps = R.cut_n + ceil_div(R.g_n[0] + R.g_n[1] + R.g_n[2], 32);
     if (warps) {
-      CF_DISPATCH3(prm.p, (k_band3<P><<<ceil_div(warps, 4), 128, 0, st>>>(L, x)));
+      CF_DISPATCH3(prm.p, (k_band3<P><<<ceil_div(warps, 4), 128, 0, st>>>(L, x, R)));
       CF_LAUNCHED();
     }
-    CF_DISPATCH3(prm.p, (k_node_apply3<P><<<ceil_div(vsize(l), 256), 256, 0, st>>>(L, x, b, y)));
+    // under the partition: the lattice planes of the cell planes [c0 - 2, c1 + 2)
+    const int64_t ps = (int64_t)L.nl * L.ld;
+    const int64_t o0 = D.part ? std::max(0, (D.c0 - 2) * L.p) * ps : 0;
+    const int64_t o1 = D.part ? std::min(L.nl, (D.c1 + 2) * L.p + 1) * ps : vsize(l);
+    CF_DISPATCH3(prm.p, (k_node_apply3<P><<<ceil_div(o1 - o0, 256), 256, 0, st>>>(L, x, b, y, o0, o1)));
     CF_LAUNCHED();
   }
 
   void cart_step3(int l, int c, double* x, const double* b) {
     LevelData& D = lv[l];
-    const int np = D.n_cart[c];
+    const int np = D.act_cart_off[c + 1] - D.act_cart_off[c];
     if (!np) return;
     CF_DISPATCH3(prm.p, (launch(k_cart_colour3<P>, dim3(ceil_div(ceil_div(np, 8), 4)), dim3(128), 0, D.a,
-                                (const int*)(D.cart_list + D.cart_off[c]), np, host::cart_map3(P), x, b)));
+                                (const int*)(D.act_cart + D.act_cart_off[c]), np, host::cart_map3(P), x, b)));
     CF_LAUNCHED();
   }
 
   void cut_step3(int l, int c, double* x, const double* b) {
     LevelData& D = lv[l];
-    const int np = D.n_cutp[c];
+    const int np = D.act_off[c + 1] - D.act_off[c];
     if (!np) return;
-    const int base = D.cutp_off[c];
+    const int base = D.act_off[c];
+    require(!D.part || (prm.cut_mode == 0 && cut3_v >= 2), ERR_STATE, "partitioned 3D levels need the descriptor cut kernels");
     if (prm.cut_mode == 0) {
       if (cut3_v >= 3) {
         CF_DISPATCH3(prm.p, {
@@ -1940,10 +2083,10 @@ struct Problem {
           }
           if (tma3)
             launch(k_cut_colour3v3<P, 128, true>, dim3(np), dim3(128), Cut3SmemV3<P, true>::bytes, tm, D.a,
-                   (const CutDesc3*)D.desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
+                   (const CutDesc3*)D.act_desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
           else
             launch(k_cut_colour3v3<P, 128, false>, dim3(np), dim3(128), Cut3SmemV3<P, false>::bytes, tm, D.a,
-                   (const CutDesc3*)D.desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
+                   (const CutDesc3*)D.act_desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
         });
       } else
       CF_DISPATCH3(prm.p, {
@@ -1953,7 +2096,7 @@ struct Problem {
           CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
           attr = true;
         }
-        launch(k_cut_colour3v2<P>, dim3(np), dim3(128), pw, D.a, (const CutDesc3*)D.desc + base, np,
+        launch(k_cut_colour3v2<P>, dim3(np), dim3(128), pw, D.a, (const CutDesc3*)D.act_desc + base, np,
                (const double*)D.inv, (const double*)x, b, D.zbuf);
       });
     } else {
@@ -1963,9 +2106,9 @@ struct Problem {
                                   (const double*)D.inv, (const double*)x, b, D.zbuf, prm.cut_mode)));
     }
     CF_LAUNCHED();
-    const int64_t e0 = D.ent_col_off[c], e1 = D.ent_col_off[c + 1];
+    const int64_t e0 = D.act_ent_off[c], e1 = D.act_ent_off[c + 1];
     if (e1 <= e0) return;
-    launch(k_cut_apply, dim3(ceil_div(e1 - e0, 256)), dim3(256), 0, (const int32_t*)D.ent_node, (const double*)D.zbuf,
+    launch(k_cut_apply, dim3(ceil_div(e1 - e0, 256)), dim3(256), 0, (const int32_t*)D.act_ent, (const double*)D.zbuf,
            e0, e1, x);
     CF_LAUNCHED();
   }
@@ -1979,6 +2122,7 @@ struct Problem {
     for (auto& q : seq) {
       if (q.first == 0) cart_step3(l, q.second, x, b);
       else cut_step3(l, q.second, x, b);
+      halo_n(l, x);   // slab partition: one exchange per colour step
     }
   }
 
@@ -1990,7 +2134,7 @@ struct Problem {
     // vector updates and dot products over the owned rows under the slab
     // partition (the dot products are then summed over the ranks)
     const bool dist = comm && F.part;
-    const int64_t o = dist ? (int64_t)F.r0 * F.a.ld : 0, no = dist ? (int64_t)(F.r1 - F.r0) * F.a.ld : nv;
+    const int64_t o = dist ? F.r0 * rowsz(Lf) : 0, no = dist ? (F.r1 - F.r0) * rowsz(Lf) : nv;
     const int grid = 4 * 148;
     k_masked_copy<<<grid, 256, 0, st>>>(cg_r + o, b + o, F.mask + o, no);
     CF_LAUNCHED();

@@ -1,2 +1,1 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -3 gpurun_out/gputests.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+python -m pytest tests/test_gpu_slab.py -x -q -k "3d" > gpurun_out/s3.log 2>&1; tail -30 gpurun_out/s3.log

@@ -286,3 +286,72 @@ def test_world1_transports(transport):
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1]
     assert np.abs(outs[0][2] - outs[1][2]).max() <= 1e-10 * np.abs(outs[0][2]).max()
+
+
+# ---- 3D: slabs of z-planes (narrow halo, one exchange per colour step) ----
+S3_Q2 = workloads.sphere("sphere-Q2-32", 2, 5, 2)                      # 2 .. 32 cells per side
+S3_Q1 = workloads.sphere("sphere-Q1-32-off", 2, 5, 1, c=(0.031, -0.017, 0.023), r=0.93)
+
+
+def _rows3(g, v, level=-1):
+    """(planes, nl*ld) view of a 3D lattice vector and the rank's owned planes"""
+    info = g.partition_info(level)
+    nl, ld = g.lattice_shape(level)
+    a = v.detach().cpu().numpy().reshape(nl, nl, ld)[:, :, :nl]
+    return a[info["r0"]:info["r1"]], info
+
+
+@pytest.mark.parametrize("w,world", [(S3_Q2, 2), (S3_Q2, 4), (S3_Q1, 2)])
+def test_3d_partition_bitexact(w, world):
+    """3D smoothing steps (forward, reverse), operator and V-cycle on the owned
+    planes bit-exact vs one rank; CG iteration counts identical"""
+    L = w.n_levels - 1
+    x0, b0 = workloads.lattice_vector(w, 61), workloads.lattice_vector(w, 62)
+    g1 = single(w)
+    ref = {}
+    x = g1.to_device(x0)
+    b = g1.to_device(b0)
+    g1.smooth(L, x, b)
+    g1.smooth(L, x, b, reverse=True)
+    ref["smooth"] = x.clone()
+    y = g1.zeros()
+    g1.apply_operator(L, g1.to_device(x0), y)
+    ref["apply"] = y
+    xv = g1.to_device(x0)
+    g1.vcycle(xv, b)
+    ref["vcycle"] = xv
+    xs = g1.zeros()
+    ref["cg"] = g1.solve_cg_mg(xs, b, tol=1e-9)
+    ref["cg_x"] = xs
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        st = s.cuda_stream
+        out = {}
+        x = g.to_device(x0)
+        b = g.to_device(b0)
+        g.smooth(L, x, b, stream=st)
+        g.smooth(L, x, b, reverse=True, stream=st)
+        out["smooth"] = x
+        y = g.zeros()
+        g.apply_operator(L, g.to_device(x0), y, stream=st)
+        out["apply"] = y
+        xv = g.to_device(x0)
+        g.vcycle(xv, b, stream=st)
+        out["vcycle"] = xv
+        xs = g.zeros()
+        out["cg"] = g.solve_cg_mg(xs, b, tol=1e-9, stream=st)
+        out["cg_x"] = xs
+        return out
+
+    outs, gs = run_ranks(w, world, fn)
+    assert gs[0].partition_info(L)["part"] == 1
+    for g, o in zip(gs, outs):
+        for key in ("smooth", "apply", "vcycle"):
+            a, info = _rows3(g, o[key])
+            full = ref[key].cpu().numpy().reshape(a.shape[1], a.shape[1], -1)[:, :, :a.shape[2]]
+            np.testing.assert_array_equal(a, full[info["r0"]:info["r1"]], err_msg=key)
+        assert o["cg"][0] == ref["cg"][0]
+        a, info = _rows3(g, o["cg_x"])
+        r = ref["cg_x"].cpu().numpy().reshape(a.shape[1], a.shape[1], -1)[info["r0"]:info["r1"], :, :a.shape[2]]
+        assert np.abs(a - r).max() <= 1e-10 * np.abs(ref["cg_x"].cpu().numpy()).max()
