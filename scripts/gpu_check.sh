@@ -1,1 +1,2 @@
-python -m pytest tests/test_gpu_slab.py -x -q -k "3d" > gpurun_out/s3.log 2>&1; tail -30 gpurun_out/s3.log
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -3 gpurun_out/gputests.log
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
