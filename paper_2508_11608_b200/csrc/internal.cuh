@@ -118,7 +118,8 @@ struct LevelData {
   int cart_tile_off[5] = {0, 0, 0, 0, 0};
   int* fused_tiles = nullptr;        // TC x TC cell tiles for the fused Cartesian sweep
   int n_fused_tiles = 0;
-  int tc = 16;                       // cells per side of the fused tiles of this level
+  int tc = 16;                       // cells of the fused tiles of this level in y (rows)
+  int tcx = 16;                      // ... and in x
   int* fused_ext = nullptr;          // fused tiles dilated by one tile (split sweep through xs)
   int n_fused_ext = 0;
   int n_cutp[8] = {};

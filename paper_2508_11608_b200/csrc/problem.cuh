@@ -96,6 +96,7 @@ struct Problem {
   bool cut_grid = false;
   int cut_grid_min_n = 0;   // ... on levels with n >= this (env CUTFEM_CUT_GRID_MIN_N)
   int tc_big_n = 512;       // levels with n >= this use 32-cell fused tiles for p = 2 (env CUTFEM_TC32_MIN_N)
+  int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
   // slab partition: comm != nullptr after partition()
   Comm* comm = nullptr;
@@ -267,6 +268,8 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_CUT_GRID_MIN_N")) cut_grid_min_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
+    require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
     if (prm.dim == 3) {
       setup_mesh3();
       return;
@@ -478,15 +481,20 @@ struct Problem {
       {
         int TC = 0;
         CF_DISPATCH(p, TC = fused_tc<P>());
-        if (p == 2 && use_mma && use_tma && n >= tc_big_n) TC = 32;   // (p = 3: 32-cell tiles exceed shared memory)
+        int TCX = TC;
+        if (p == 2 && use_mma && use_tma && n >= tc_big_n) {   // (p = 3: 32-cell tiles exceed shared memory)
+          TC = 32;
+          TCX = tcx_big;
+        }
         D.tc = TC;
-        const int tx = ceil_div(n, TC), nt = tx * tx;
+        D.tcx = TCX;
+        const int tx = ceil_div(n, TCX), ty = ceil_div(n, TC), nt = tx * ty;
         uint8_t* tf = alloc<uint8_t>(nt);
         int* ts = alloc<int>(nt);
-        k_fused_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(n, D.vkind, TC, tx, tf, nt);
+        k_fused_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(n, D.vkind, TCX, TC, tx, tf, nt);
         CF_LAUNCHED();
         uint8_t* tfe = alloc<uint8_t>(nt);
-        k_dilate_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(tx, tf, tfe);
+        k_dilate_tile_flags<<<ceil_div(nt, 128), 128, 0, st>>>(tx, ty, tf, tfe);
         CF_LAUNCHED();
         D.n_fused_tiles = select(tf, nt, ts);
         if (D.n_fused_tiles) {
@@ -1201,26 +1209,26 @@ struct Problem {
   }
 
   // the TMA / tensor-core fused sweep with TC x TC cell tiles (see cart_fused)
-  template <int P, int TC>
+  template <int P, int TC, int TCX = TC>
   void cart_fused_tma(int l, double* x, const double* b, int reverse) {
     LevelData& D = lv[l];
     constexpr int NT = TC >= 32 ? CF_CART_NT32 : 256;
     const double* G = host::cart_map(P);
-    using S = CartTmaSmem<P, TC>;
+    using S = CartTmaSmem<P, TC, TCX>;
     const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
     const CUtensorMap tmb = host::lattice_tmap(b, D.a.nl, D.a.ld, S::RWP, S::RW);
     static int cap = -1;
     if (cap < 0) {
-      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
-      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      cap = coresident(k_cart_fused_tma<P, TC, NT>, S::bytes, NT);
+      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT, TCX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+      CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT, TCX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      cap = coresident(k_cart_fused_tma<P, TC, NT, TCX>, S::bytes, NT);
     }
     if (verbose) {
       std::fprintf(stderr, "[cutfem] level %d: %d fused tiles (%d ext), %d co-resident -> %s\n", l,
                    D.n_fused_tiles, D.n_fused_ext, cap, (!cart_split && D.n_fused_tiles <= cap) ? "in place" : "split");
     }
     if (!cart_split && D.n_fused_tiles <= cap) {
-      launch_ex(true, k_cart_fused_tma<P, TC, NT>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
+      launch_ex(true, k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
                 (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, 1);
       CF_LAUNCHED();
       cart_done(l, x, reverse);
@@ -1228,11 +1236,11 @@ struct Problem {
     }
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
     if (D.n_fused_ext)
-      launch(k_cart_fused_tma<P, TC, NT>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
+      launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
              (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, 0);
     CF_LAUNCHED();
     halo_n(l, D.xs);
-    launch(k_cart_fused_tma<P, TC, NT>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
+    launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
            (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, 0);
     CF_LAUNCHED();
     cart_done(l, x, reverse);
@@ -1253,7 +1261,9 @@ struct Problem {
     CF_DISPATCH(prm.p, {
       if constexpr (P == 2) {
         if (D.tc == 32) {
-          cart_fused_tma<P, 32>(l, x, b, reverse);
+          if (D.tcx == 16) cart_fused_tma<P, 32, 16>(l, x, b, reverse);
+          else if (D.tcx == 24) cart_fused_tma<P, 32, 24>(l, x, b, reverse);
+          else cart_fused_tma<P, 32, 32>(l, x, b, reverse);
           return;
         }
       }

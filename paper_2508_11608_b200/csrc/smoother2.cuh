@@ -622,27 +622,27 @@ __global__ void __launch_bounds__(256) k_cart_fused(LevelArgs L, const int* tile
 
 // tiles within one tile of a flagged tile (the tiles whose owned nodes the
 // split Cartesian sweep must carry through the shadow buffer)
-__global__ void k_dilate_tile_flags(int tx, const uint8_t* in, uint8_t* out) {
+__global__ void k_dilate_tile_flags(int tx, int ty, const uint8_t* in, uint8_t* out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= tx * tx) return;
+  if (t >= tx * ty) return;
   const int ti = t % tx, tj = t / tx;
   uint8_t f = 0;
   for (int dj = -1; dj <= 1; ++dj)
     for (int di = -1; di <= 1; ++di) {
       const int i = ti + di, j = tj + dj;
-      if (i >= 0 && j >= 0 && i < tx && j < tx && in[j * tx + i]) f = 1;
+      if (i >= 0 && j >= 0 && i < tx && j < ty && in[j * tx + i]) f = 1;
     }
   out[t] = f;
 }
 
-// tiles of TC x TC cells whose owned vertex range holds a Cartesian patch
-__global__ void k_fused_tile_flags(int n, const uint8_t* vk, int TC, int tx, uint8_t* flag, int ntiles) {
+// tiles of TCX x TCY cells whose owned vertex range holds a Cartesian patch
+__global__ void k_fused_tile_flags(int n, const uint8_t* vk, int TCX, int TCY, int tx, uint8_t* flag, int ntiles) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
-  const int ci0 = (t % tx) * TC, cj0 = (t / tx) * TC;
+  const int ci0 = (t % tx) * TCX, cj0 = (t / tx) * TCY;
   uint8_t f = 0;
-  for (int J = cj0; J <= min(cj0 + TC, n) && !f; ++J)
-    for (int I = ci0; I <= min(ci0 + TC, n); ++I)
+  for (int J = cj0; J <= min(cj0 + TCY, n) && !f; ++J)
+    for (int I = ci0; I <= min(ci0 + TCX, n); ++I)
       if (vk[J * (n + 1) + I] == V_CART) {
         f = 1;
         break;
@@ -1037,11 +1037,12 @@ __global__ void k_andnot_flags(const uint8_t* a, const uint8_t* b, int64_t n, ui
 namespace cf {
 
 // ---- fused Cartesian sweep, v2: TMA tile loads, hoisted operand offsets ----
-template <int P, int TC>
+template <int P, int TC, int TCX = TC>
 struct CartTmaSmem {
-  static constexpr int H = 4, RC = TC + 2 * H, RW = RC * P + 1, RWP = (RW + 1) & ~1;
+  // TC = cells per tile in y (rows: the partitioned direction), TCX in x
+  static constexpr int H = 4, RW = (TC + 2 * H) * P + 1, RWX = (TCX + 2 * H) * P + 1, RWP = (RWX + 1) & ~1;
   static constexpr int tile_doubles = (RW * RWP + 15) & ~15;   // 128-byte aligned tiles (TMA destination)
-  static constexpr int maxp = ((TC + 7) / 2 + 1) * ((TC + 7) / 2 + 1);
+  static constexpr int maxp = ((TCX + 7) / 2 + 1) * ((TC + 7) / 2 + 1);
   static constexpr int head = ((16 + 4 * maxp) + 127) & ~127;     // mbarrier, count, patch list
   static constexpr size_t bytes = head + 2 * tile_doubles * sizeof(double);
 };
@@ -1052,18 +1053,18 @@ struct CartTmaSmem {
 // cooperative launch: the grid barrier before the write keeps every CTA's
 // apron load ahead of its neighbours' writes.  Otherwise the sweep is split
 // into two launches through the shadow buffer (passes 0-1 x -> xs, 2-3 xs -> x).
-template <int P, int TC, int NT = 256>
+template <int P, int TC, int NT = 256, int TCX = TC>
 __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* xout, int reverse, int s0, int s1, int gsync) {
   using C = CartMMA<P>;
-  using S = CartTmaSmem<P, TC>;
+  using S = CartTmaSmem<P, TC, TCX>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
   constexpr int MF = NINT / 8;                 // full 8-row tiles on the tensor cores
   constexpr int RR = NINT - 8 * MF;            // remainder rows on the FMA pipe (p = 1: 1, p = 2: 1, p = 3: 1)
   constexpr int H = S::H, RW = S::RW, RWP = S::RWP, TD = S::tile_doubles;
-  constexpr int MAXP = ((TC + 7) / 2 + 1) * ((TC + 7) / 2 + 1);   // candidate patches of the widest pass
+  constexpr int MAXP = S::maxp;   // candidate patches of the widest pass
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* bar = (uint64_t*)smraw;
   int* plist = (int*)(smraw + 16);             // compacted Cartesian patches of a pass (block origins)
@@ -1091,7 +1092,7 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
 #pragma unroll
     for (int s = 0; s < KS; ++s) gr[rr][s] = G[(8 * MF + rr) * C::COLS + 4 * s + (lane & 3)];
   const int tile = tiles[blockIdx.x];
-  const int ci0 = (tile & 0xffff) * TC, cj0 = (tile >> 16) * TC;
+  const int ci0 = (tile & 0xffff) * TCX, cj0 = (tile >> 16) * TC;
   const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
@@ -1104,7 +1105,7 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
   for (int s = s0; s < s1; ++s) {
     const int c = reverse ? 3 - s : s, rad = s1 - 1 - s;
     const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
-    const int nvx = (ci0 + TC + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
+    const int nvx = (ci0 + TCX + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
     // compact the Cartesian patches of this pass
     if (tid == 0) *pcount = 0;
     __syncthreads();
@@ -1156,7 +1157,7 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
   if (s1 == s0) mbar_wait(bar, 0);
   if (gsync) cooperative_groups::this_grid().sync();
   // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
-  const int ahi = (ci0 + TC >= n) ? L.nl : P * (ci0 + TC), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
+  const int ahi = (ci0 + TCX >= n) ? L.nl : P * (ci0 + TCX), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   for (int bb = P * cj0 + warp; bb < bhi; bb += NT / 32) {
     const double* src = Xs + (bb - b0) * RWP - a0;
     double* dst = xout + (size_t)bb * L.ld;
