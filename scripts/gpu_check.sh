@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -3 gpurun_out/gputests.log
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
+python -m pytest tests/test_gpu_3d.py tests/test_gpu_slab.py -x -q -k "3d" > gpurun_out/t3.log 2>&1; tail -3 gpurun_out/t3.log
+timeout 900 python scripts/ab.py --w CONFIG2 variants/v18.so variants/v19.so
