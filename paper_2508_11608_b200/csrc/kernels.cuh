@@ -606,17 +606,22 @@ __global__ void k_restrict(LevelArgs Lf, LevelArgs Lc, const double* rf, double*
   }
   const int mA = A % P, IA = A / P, mB = B % P, IB = B / P;
   const int dalo = mA == 0 ? -2 * P : 0, dblo = mB == 0 ? -2 * P : 0;
+  // fully unrolled with predicated (zero-weight) terms so that all (4p+1)^2
+  // loads are in flight at once; a zero-weight term adds fma(0, v, t) = t
+  // (v is finite: residual entries of non-DoF nodes are 0)
   double s = 0.0;
-  for (int db = dblo; db <= 2 * P; ++db) {
+#pragma unroll
+  for (int db = -2 * P; db <= 2 * P; ++db) {
     const int fb = 2 * P * IB + db;
-    if (fb < 0 || fb >= Lf.nl) continue;
-    const double wb = tw[mB][db + 2 * P];
-    if (wb == 0.0) continue;
+    const bool rb = db >= dblo && fb >= 0 && fb < Lf.nl;
+    const double wb = rb ? tw[mB][db + 2 * P] : 0.0;
     double t = 0.0;
-    for (int da = dalo; da <= 2 * P; ++da) {
+#pragma unroll
+    for (int da = -2 * P; da <= 2 * P; ++da) {
       const int fa = 2 * P * IA + da;
-      if (fa < 0 || fa >= Lf.nl) continue;
-      t = fma(tw[mA][da + 2 * P], rf[(size_t)fb * Lf.ld + fa], t);
+      const bool ok = rb && wb != 0.0 && da >= dalo && fa >= 0 && fa < Lf.nl;
+      const double v = ok ? rf[(size_t)fb * Lf.ld + fa] : 0.0;
+      t = fma(ok ? tw[mA][da + 2 * P] : 0.0, v, t);
     }
     s = fma(wb, t, s);
   }

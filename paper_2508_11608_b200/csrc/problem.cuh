@@ -96,6 +96,7 @@ struct Problem {
   bool cut_grid = false;
   int cut_grid_min_n = 0;   // ... on levels with n >= this (env CUTFEM_CUT_GRID_MIN_N)
   int tc_big_n = 512;       // levels with n >= this use 32-cell fused tiles for p = 2 (env CUTFEM_TC32_MIN_N)
+  int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
   // slab partition: comm != nullptr after partition()
@@ -269,6 +270,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
     require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
     if (prm.dim == 3) {
       setup_mesh3();
@@ -1076,8 +1078,11 @@ struct Problem {
       }
       CF_LAUNCHED();
     }
+    // TMA tiles of 16 x 16 cells where the level has enough of them to fill the
+    // GPU; small levels use one thread per node (shorter per-thread chains)
     bool tile_ok = false;
-    CF_DISPATCH(p, tile_ok = L.nl >= ApplySmem<P, 16>::RW && L.ld >= ApplySmem<P, 16>::RWP);
+    CF_DISPATCH(p, tile_ok = L.nl >= ApplySmem<P, 16>::RW && L.ld >= ApplySmem<P, 16>::RWP &&
+                             (int64_t)ceil_div(L.n, 16) * ceil_div(L.n, 16) >= tile_apply_min_tiles);
     if (tile_apply && tile_ok) {   // the TMA box must fit inside the lattice
       CF_DISPATCH(p, {
         constexpr int TX = 16;

@@ -1,2 +1,2 @@
-python -m pytest tests/test_gpu_3d.py tests/test_gpu_slab.py -x -q -k "3d" > gpurun_out/t3.log 2>&1; tail -3 gpurun_out/t3.log
-timeout 900 python scripts/ab.py --w CONFIG2 variants/v18.so variants/v19.so
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -3 gpurun_out/gputests.log
+timeout 900 python scripts/ab.py variants/v18.so variants/v20.so variants/v20.so:CUTFEM_TILEAPPLY_MIN=1 variants/v20.so:CUTFEM_TILEAPPLY_MIN=100000
