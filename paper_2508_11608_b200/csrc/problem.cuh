@@ -96,6 +96,11 @@ struct Problem {
   bool cut_grid = false;
   int cut_grid_min_n = 0;   // ... on levels with n >= this (env CUTFEM_CUT_GRID_MIN_N)
   int tc_big_n = 512;       // levels with n >= this use 32-cell fused tiles for p = 2 (env CUTFEM_TC32_MIN_N)
+  // levels whose colours have <= this many cut patches: cut sweeps in one
+  // cluster launch with the patch maps (env CUTFEM_CLUSTER7_MAX).  Off:
+  // measured slower than PDL launches (V-cycle 727 us with <= 64, 1030 us
+  // with <= 400, vs 679 us)
+  int cluster7_max = 0;
   int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
@@ -271,6 +276,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_CLUSTER7_MAX")) cluster7_max = std::atoi(e);
     require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
     if (prm.dim == 3) {
       setup_mesh3();
@@ -1450,6 +1456,48 @@ struct Problem {
     return ok;
   }
 
+  // all cut sweeps of a small level in one cluster launch with the patch maps
+  void cut_sweeps_cluster7(int l, double* x, const double* b, int reverse) {
+    LevelData& D = lv[l];
+    CutSweepArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.L = D.a;
+    A.desc = (const CutDesc*)D.act_desc;
+    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.act_off[c];
+    A.copy = D.copy_lists;
+    for (int i = 0; i < 5; ++i)
+      for (int c = 0; c < 4; ++c) {
+        A.copy_off[i][c] = D.copy_off[i][c];
+        A.copy_n[i][c] = D.copy_n[i][c];
+      }
+    A.x = x;
+    A.xs = D.xs;
+    A.b = b;
+    A.n_c = prm.n_c;
+    A.reverse = reverse;
+    A.gmap = D.gmap;
+    CF_DISPATCH(prm.p, {
+      if constexpr (P <= 3) {
+        constexpr int G = P <= 2 ? 4 : 2;
+        const size_t smb = (size_t)G * ((CutMapSmem<P>::bytes + 127) & ~(size_t)127);
+        static bool attr = false;
+        if (!attr) {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster7<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+          CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster7<P, G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          attr = true;
+        }
+        cudaError_t e = launch_cluster(k_cut_sweeps_cluster7<P, G>, cluster_size, dim3(64 * G), smb, A);
+        if (e != cudaSuccess) {
+          (void)cudaGetLastError();
+          require(cluster_size > 8, ERR_CUDA, "cluster launch of the cut sweeps failed");
+          cluster_size = 8;
+          CF_CUDA(launch_cluster(k_cut_sweeps_cluster7<P, G>, cluster_size, dim3(64 * G), smb, A));
+        }
+        CF_LAUNCHED();
+      }
+    });
+  }
+
   // all cut sweeps of a smoothing step in one cooperative launch over the GPU
   bool cut_sweeps_grid(int l, double* x, const double* b, int reverse) {
     LevelData& D = lv[l];
@@ -1492,6 +1540,14 @@ struct Problem {
   }
 
   void cut_sweeps(int l, double* x, const double* b, int reverse) {
+    if (cluster7_max > 0 && !lv[l].part && lv[l].gmap && cut_map && prm.cut_mode == 0 && cta_cut && prm.p <= 3) {
+      int npmax = 0;
+      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].act_off[c + 1] - lv[l].act_off[c]);
+      if (npmax <= cluster7_max) {
+        cut_sweeps_cluster7(l, x, b, reverse);
+        return;
+      }
+    }
     if (cut_grid && !lv[l].part && prm.cut_mode == 0 && cta_cut && (prm.n_c * 4) % 2 == 0 &&
         lv[l].a.n >= cut_grid_min_n) {
       cut_sweeps_grid(l, x, b, reverse);

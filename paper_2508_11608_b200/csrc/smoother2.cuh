@@ -1826,6 +1826,7 @@ struct CutSweepArgs {
   double* xs;
   const double* b;
   int n_c, reverse;
+  const double* gmap;       // cut-patch maps (k_cut_sweeps_cluster7)
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -2103,34 +2104,23 @@ struct CutMapSmem {
   static constexpr size_t bytes = gs_off + (size_t)MM * maxK * 8 + 2 * MM + 2 * WW + 16;
 };
 
-// hot path: one cut colour step with the precomputed maps (ping-pong as
-// k_cut_step6): x_I^new = G_j [b_I ; x_E'] gathered after the wait, the map,
-// interior locations, exterior indices and DoF mask fetched before it
+// the cut-step-7 routine for a group of NT threads with named barrier `bar`:
+// prologue (setup data only: descriptor, map block by cp.async, interior
+// locations, exterior window indices), then main (after the previous step's
+// writes are visible): gather b_I and x_E, x_I^new = G_j [b_I ; x_E], store.
+// LDCG: read x through L2 only (previous step written by other SMs of the
+// same launch).
 template <int P, int NT>
-__global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* desc, int np, const double* G,
-                                                  const double* R, double* W, const double* b, const int32_t* copy,
-                                                  int ncopy) {
+__device__ __forceinline__ void cut7_prologue(const CutDesc* desc, int k, const double* G, unsigned char* gsm, int gt,
+                                              int bar) {
   using S = CutMapSmem<P>;
-  constexpr int BS = S::BS, WS = S::WS, MM = S::MM, WW = S::WW;
-  extern __shared__ __align__(128) unsigned char sm7[];
-  const int tid = threadIdx.x;
-  pdl_trigger();
-  if ((int)blockIdx.x >= np) {
-    const int e = (blockIdx.x - np) * NT + tid;
-    if (e < ncopy) {
-      const int32_t node = copy[e];
-      pdl_wait();
-      W[node] = R[node];
-    }
-    return;
-  }
-  CutDesc& d = *(CutDesc*)sm7;
-  double* v = (double*)(sm7 + 64);
-  double* Gs = (double*)(sm7 + S::gs_off);
+  constexpr int MM = S::MM;
+  CutDesc& d = *(CutDesc*)gsm;
+  double* Gs = (double*)(gsm + S::gs_off);
   short* Lc = (short*)(Gs + (size_t)MM * S::maxK);
   uint8_t* ix = (uint8_t*)(Lc + MM);
-  if (tid < 4) ((int4*)&d)[tid] = ((const int4*)(desc + blockIdx.x))[tid];
-  __syncthreads();
+  if (gt < 4) ((int4*)&d)[gt] = ((const int4*)(desc + k))[gt];
+  group_sync(bar, NT);
   const int m = mask_count(d);
   // the kept exterior columns are DoF nodes inside the lattice (a column is
   // nonzero only if its node shares an active cell or a ghost face with the
@@ -2138,30 +2128,43 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
   const double* blk = G + (d.map_off & ((1ll << 48) - 1));
   const int nnz = (int)(d.map_off >> 48), K = m + nnz;
   const double* rows = blk + 1 + (nnz + 7) / 8;
-  for (int e = tid; e < m * K; e += NT) cp_async8(Gs + e, rows + e);
-  for (int loc = tid; loc < MM; loc += NT) {
+  for (int e = gt; e < m * K; e += NT) cp_async8(Gs + e, rows + e);
+  for (int loc = gt; loc < MM; loc += NT) {
     const unsigned long long word = d.mask[loc >> 6];
     if ((word >> (loc & 63)) & 1ull)
       Lc[(loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull))] = (short)loc;
   }
+  for (int j = gt; j < nnz; j += NT) ix[j] = ((const uint8_t*)(blk + 1))[j];
+  group_sync(bar, NT);   // Lc, ix visible (in k_cut_step7: before griddepcontrol.wait)
+}
+
+template <int P, int NT, bool LDCG>
+__device__ __forceinline__ void cut7_main(const LevelArgs& L, const double* R, double* W, const double* b,
+                                          unsigned char* gsm, int gt, int bar) {
+  using S = CutMapSmem<P>;
+  constexpr int BS = S::BS, WS = S::WS, MM = S::MM;
+  const CutDesc& d = *(const CutDesc*)gsm;
+  double* v = (double*)(gsm + 64);
+  double* Gs = (double*)(gsm + S::gs_off);
+  short* Lc = (short*)(Gs + (size_t)MM * S::maxK);
+  uint8_t* ix = (uint8_t*)(Lc + MM);
+  const int m = mask_count(d), nnz = (int)(d.map_off >> 48), K = m + nnz;
   const int a0 = P * (d.I - 2), b0 = P * (d.J - 2);
-  for (int j = tid; j < nnz; j += NT) ix[j] = ((const uint8_t*)(blk + 1))[j];
-  __syncthreads();
-  pdl_wait();
-  for (int i = tid; i < m; i += NT) {
+  for (int i = gt; i < m; i += NT) {
     const int loc = Lc[i];
     v[i] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
   }
-  for (int j = tid; j < nnz; j += NT) {
+  for (int j = gt; j < nnz; j += NT) {
     const int w = ix[j];
-    v[m + j] = R[(size_t)(b0 + w / WS) * L.ld + a0 + w % WS];
+    const double* src = R + (size_t)(b0 + w / WS) * L.ld + a0 + w % WS;
+    v[m + j] = LDCG ? __ldcg(src) : *src;
   }
   cp_async_wait_all();
-  __syncthreads();
+  group_sync(bar, NT);
   // x_I^new = G_j v: TPR threads per row (power of two), shuffle-reduced
   const int tpr = m * 4 <= NT ? 4 : (m * 2 <= NT ? 2 : 1);
   for (int r0 = 0; r0 < m; r0 += NT / tpr) {
-    const int i = r0 + tid / tpr, h = tid % tpr;
+    const int i = r0 + gt / tpr, h = gt % tpr;
     double a0c = 0.0, a1c = 0.0;
     if (i < m) {
       const double* g = Gs + (size_t)i * K;
@@ -2178,6 +2181,79 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
       const int loc = Lc[i];
       W[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS] = z;
     }
+  }
+}
+
+// hot path: one cut colour step with the precomputed maps (ping-pong as
+// k_cut_step6): the prologue before griddepcontrol.wait, the main part after
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* desc, int np, const double* G,
+                                                  const double* R, double* W, const double* b, const int32_t* copy,
+                                                  int ncopy) {
+  extern __shared__ __align__(128) unsigned char sm7[];
+  const int tid = threadIdx.x;
+  pdl_trigger();
+  if ((int)blockIdx.x >= np) {
+    const int e = (blockIdx.x - np) * NT + tid;
+    if (e < ncopy) {
+      const int32_t node = copy[e];
+      pdl_wait();
+      W[node] = R[node];
+    }
+    return;
+  }
+  cut7_prologue<P, NT>(desc, blockIdx.x, G, sm7, tid, 0);
+  pdl_wait();
+  cut7_main<P, NT, false>(L, R, W, b, sm7, tid, 0);
+}
+
+// all n_c x 4 cut steps of a smoothing step in ONE launch of one
+// thread-block cluster (CTAs of G groups of 64 threads, the step-7 routine,
+// cluster barriers between the ping-pong steps; the next step's prologue is
+// issued before the barrier).  For small levels, where a launch per step
+// costs more than the step.
+template <int P, int G>
+__global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster7(CutSweepArgs A) {
+  using S = CutMapSmem<P>;
+  extern __shared__ __align__(128) unsigned char smc7[];
+  const int tid = threadIdx.x, grp = tid >> 6, gt = tid & 63;
+  const int cr = (int)cluster_rank(), cs = (int)cluster_nctas();
+  unsigned char* gsm = smc7 + (size_t)grp * ((S::bytes + 127) & ~(size_t)127);
+  pdl_trigger();
+  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
+  const int k0 = cr * G + grp;
+  {
+    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c];
+    if (k0 < np) cut7_prologue<P, 64>(A.desc, A.cut_off[c] + k0, A.gmap, gsm, gt, 1 + grp);
+  }
+  pdl_wait();
+  cluster_sync_all();
+  double* bufs[2] = {A.x, A.xs};
+  int prev = 4;
+  const int nsteps = A.n_c * 4;
+  for (int s = 0; s < nsteps; ++s) {
+    const int c = step_colour(s);
+    const double* R = bufs[s & 1];
+    double* W = bufs[(s + 1) & 1];
+    const int nco = A.copy_n[prev][c];
+    const int32_t* cl = A.copy + A.copy_off[prev][c];
+    for (int e = cr * 64 * G + tid; e < nco; e += cs * 64 * G) W[cl[e]] = __ldcg(R + cl[e]);
+    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
+    const int rounds = (np + cs * G - 1) / (cs * G);
+    for (int r = 0; r < rounds; ++r) {
+      const int k = (r * cs + cr) * G + grp;
+      if (k < np) {
+        if (r > 0) cut7_prologue<P, 64>(A.desc, p0 + k, A.gmap, gsm, gt, 1 + grp);
+        cut7_main<P, 64, true>(A.L, R, W, A.b, gsm, gt, 1 + grp);
+        group_sync(1 + grp, 64);
+      }
+    }
+    if (s + 1 < nsteps) {
+      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn];
+      if (k0 < npn) cut7_prologue<P, 64>(A.desc, A.cut_off[cn] + k0, A.gmap, gsm, gt, 1 + grp);
+    }
+    prev = c;
+    cluster_sync_all();
   }
 }
 
