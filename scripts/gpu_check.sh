@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -2 gpurun_out/gputests.log
-timeout 900 python scripts/ab.py variants/v20.so variants/v22.so
+python -m pytest tests/test_gpu_modes.py tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log
+timeout 900 python scripts/ab.py variants/v23_nosort.so variants/v23.so
