@@ -22,8 +22,11 @@
  *    (a, b) = x-index a, y-index b, at position
  *    x0 + (a div p + xi_{a mod p}) h (xi = Gauss-Lobatto nodes on [0,1]).
  *    Entries of nodes that carry no DoF (P l.121: no DoFs on exterior cells)
- *    and the padding columns a >= NL are ignored on input and written as 0 on
- *    output.  Vectors are owned by the caller; the library never frees them.
+ *    and the padding columns a >= NL are ignored on input (they may hold any
+ *    value, NaN included); output vectors (y of cutfem_apply_operator, x of
+ *    cutfem_solve_cg_mg) are 0 there, vectors updated in place (x of
+ *    cutfem_smooth / cutfem_vcycle) keep their non-DoF entries unchanged.
+ *    Vectors are owned by the caller; the library never frees them.
  *  - The problem handle owns all device memory it allocates (mesh data,
  *    patch data, local inverses, workspaces); cutfem_destroy releases it.
  *  - A handle is not thread-safe; calls on one handle must be serialised.

@@ -1,3 +1,1 @@
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_v15.csv python scripts/profile_step.py --steps 2 --vcycle > /dev/null 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+python -m pytest tests/test_gpu_parity.py -x -q -k "non_dof" > gpurun_out/t.log 2>&1; tail -25 gpurun_out/t.log

@@ -188,3 +188,38 @@ def test_runtime_quadrature_mode_parity(w, torch_cuda):
     xo = compact(ld.lv, xl).copy()
     ld.smooth(xo, compact(ld.lv, bl), w.n_c)
     assert rel_err(compact(ld.lv, g.to_host(x, l)), xo) < TOL
+
+
+@pytest.mark.parametrize("w", [workloads.paper_level(2, 8), workloads.CONFIG0], ids=["paper-Q2-L8", "config0"])
+def test_non_dof_entries_ignored(w, torch_cuda):
+    """include/cutfem_mg.h: entries of nodes without a DoF are ignored on input
+    (NaN there must not reach any DoF: operator, smoothing steps, V-cycle,
+    CG), written as 0 by the output vectors (operator, CG) and left untouched
+    by the in-place updates (smoothing step, V-cycle)"""
+    g = gpu(w)
+    mask = g.dof_mask().ravel()
+    xl, bl = lattice_random(w, 91, None), lattice_random(w, 92, None)
+    xn, bn = xl.copy(), bl.copy()
+    xn[~mask] = np.nan
+    bn[~mask] = np.nan
+    L = w.n_levels - 1
+    outs = []
+    for xv, bv in ((xl, bl), (xn, bn)):
+        x = g.to_device(xv)
+        b = g.to_device(bv)
+        y = g.zeros()
+        g.apply_operator(L, x, y)
+        g.smooth(L, x, b)
+        g.smooth(L, x, b, True)
+        g.vcycle(x, b)
+        xs = g.zeros()
+        it, _ = g.solve_cg_mg(xs, b, tol=1e-8)
+        outs.append((g.to_host(y), g.to_host(x), g.to_host(xs), it))
+    for k, (a, b_) in enumerate(zip(outs[0][:3], outs[1][:3])):
+        assert np.all(np.isfinite(b_[mask]))
+        np.testing.assert_array_equal(a[mask], b_[mask])
+        if k == 1:   # in place: untouched
+            assert np.all(np.isnan(b_[~mask]))
+        else:
+            assert np.all(b_[~mask] == 0.0)
+    assert outs[0][3] == outs[1][3]
