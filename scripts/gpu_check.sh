@@ -1,1 +1,1 @@
-python -m pytest tests/test_gpu_parity.py -x -q -k "non_dof" > gpurun_out/t.log 2>&1; tail -25 gpurun_out/t.log
+timeout 900 python scripts/ab.py --w CONFIG2 variants/v24.so variants/v24_ilp4.so
