@@ -1345,7 +1345,10 @@ struct Problem {
     if (D.gmap && cut_map && prm.cut_mode == 0 && cta_cut) {
       CF_DISPATCH(prm.p, {
         if constexpr (P <= 3) {
-          constexpr int NT = P <= 2 ? 64 : 128;
+#ifndef CF_CUT7_NT
+#define CF_CUT7_NT 128   // threads per cut patch (p <= 2); 64: V-cycle 671 vs 660 us
+#endif
+          constexpr int NT = P <= 2 ? CF_CUT7_NT : 128;
           const size_t smb = CutMapSmem<P>::bytes;
           static bool attr7 = false;
           if (!attr7) {

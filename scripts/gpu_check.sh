@@ -1,1 +1,1 @@
-timeout 900 python scripts/ab.py --w CONFIG2 variants/v24.so variants/v24_ilp4.so
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -2 gpurun_out/gputests.log
