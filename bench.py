@@ -241,6 +241,19 @@ def main():
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(dom.split("<")[0])
 
+    # fp64 tensor-core roofline of the fused Cartesian sweep (a dense contraction:
+    # x_int = G [b_int; x_block] per patch, G of (2p-1)^2 x ((2p-1)^2 + (2p+1)^2)),
+    # algorithmic flops without the temporal-blocking redundancy
+    ni, ne = (2 * p - 1) ** 2, (2 * p + 1) ** 2
+    cart_flops = 2.0 * ni * (ni + ne) * float(sum(info.n_cart[:4])) / world
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    fp64_peak = 40.0 * float(mp.get("bf16_tflops", 2250.0)) / 2250.0   # nominal 40 TF fp64 x measured/nominal bf16
+    roof_fp64 = {"bound": "tensor", "kernel": "k_cart_fused_tma (DMMA fp64)", "achieved": cart_flops / (cart_ms * 1e-3) / 1e12,
+                 "peak": fp64_peak, "unit": "TFLOP/s", "frac": cart_flops / (cart_ms * 1e-3) / 1e12 / fp64_peak,
+                 "peak_source": "nominal 40 TFLOP/s fp64 (B200) x measured/nominal bf16 (MEASURED_PEAKS.json / 2250)",
+                 "flops_per_launch": cart_flops}
+
     # ---- V-cycle and CG+MG time to solution
     z = g.zeros()
     vms = timed(lambda: (z.zero_(), g.vcycle(z, b)), 20, 3)
@@ -337,6 +350,7 @@ def main():
                          "algorithmic_bytes_per_launch": d_bytes, "avg_launch_ms": d_ms,
                          "step_share_ms": per_step},
             "kernels": kernels,
+            "roofline_fp64_cartesian": roof_fp64,
             "vcycle": {"ms": v_ms, "dofs_per_s": n_dofs / (v_ms * 1e-3)},
             "cg_mg": {"time_to_solution_ms": cg_ms, "iterations": it, "rel_residual": rel, "tol": w.tol,
                       "dofs_per_s": n_dofs / (cg_ms * 1e-3)},
