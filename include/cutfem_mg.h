@@ -197,6 +197,14 @@ int cutfem_partition(cutfem_problem pb, cutfem_comm comm);
  * cells, or 12 n_c cells on levels whose slabs are thick enough for the
  * wide-halo cut sweeps (one exchange per sweep instead of one per step) */
 int cutfem_partition_info(cutfem_problem pb, int level, int* out);
+/* The slab plan the partition uses for one level (host only, no device):
+ * out[17] = {c0, c1, r0, r1, v0, v1, n_xfers, then 2 x (peer, send_off,
+ * send_n, recv_off, recv_n)} -- owned cell rows [c0, c1), owned lattice rows
+ * [r0, r1), valid rows [v0, v1) after an exchange of `halo_cells` cells, and
+ * the row bands exchanged with the neighbours (offsets / counts in lattice
+ * rows; peer = -1 for an unused slot).  ERR_ARG unless n_cells % world == 0
+ * and n_cells / world >= halo_cells + 1. */
+int cutfem_slab_plan(int n_cells, int degree, int world, int rank, int halo_cells, int64_t* out);
 /* exchange the halo rows of a lattice vector of `level` with the neighbours */
 int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream);
 

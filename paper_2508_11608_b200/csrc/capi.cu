@@ -243,6 +243,27 @@ int cutfem_partition_info(cutfem_problem pb, int level, int* out) {
   });
 }
 
+int cutfem_slab_plan(int n_cells, int degree, int world, int rank, int halo_cells, int64_t* out) {
+  return guarded([&]() {
+    cf::require(out != nullptr, cf::ERR_ARG, "null output");
+    cf::require(n_cells >= 1 && degree >= 1 && world >= 1 && rank >= 0 && rank < world && halo_cells >= 0, cf::ERR_ARG,
+                "bad slab plan arguments");
+    cf::require(n_cells % world == 0 && n_cells / world >= halo_cells + 1, cf::ERR_ARG,
+                "slabs must be whole and thicker than the halo");
+    const cf::SlabPlan s = cf::slab_plan(n_cells, degree, world, rank, halo_cells, 1);
+    const int64_t head[7] = {s.c0, s.c1, s.r0, s.r1, s.v0, s.v1, (int64_t)s.xf.size()};
+    for (int i = 0; i < 7; ++i) out[i] = head[i];
+    for (int i = 0; i < 2; ++i) {
+      const bool has = i < (int)s.xf.size();
+      out[7 + 5 * i + 0] = has ? s.xf[i].peer : -1;
+      out[7 + 5 * i + 1] = has ? s.xf[i].send_off : 0;
+      out[7 + 5 * i + 2] = has ? s.xf[i].send_n : 0;
+      out[7 + 5 * i + 3] = has ? s.xf[i].recv_off : 0;
+      out[7 + 5 * i + 4] = has ? s.xf[i].recv_n : 0;
+    }
+  });
+}
+
 int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream) {
   return guarded([&]() {
     check_level(pb, level);

@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <mutex>
 #include <vector>
@@ -26,6 +27,35 @@
 #include "internal.cuh"
 
 namespace cf {
+
+// Slab plan of one level (host-only, also exported as cutfem_slab_plan):
+// rank R of W owns the cell rows [c0, c1) = [R n/W, (R+1) n/W), lattice rows
+// [r0, r1) = [p c0, p c1) (the last rank also owns the top line nl - 1); with
+// a halo of hc cells the rows [v0, v1) = owned +- hc p (+1 above) are valid
+// after the exchange, whose transfers move contiguous row bands: to R-1 the
+// rows [r0, r0 + hc p], from R-1 the rows [r0 - hc p, r0), to R+1 the rows
+// [r1 - hc p, r1), from R+1 the rows [r1, r1 + hc p] -- so a band sent by one
+// rank is exactly the band its neighbour receives.  Offsets in units of
+// `rowsz` doubles (a row in 2D, a plane in 3D).
+struct SlabPlan {
+  int c0 = 0, c1 = 0, r0 = 0, r1 = 0, v0 = 0, v1 = 0;
+  std::vector<Xfer> xf;
+};
+
+inline SlabPlan slab_plan(int n, int p, int W, int R, int hc, int64_t rowsz) {
+  SlabPlan s;
+  const int nl = n * p + 1, per = n / W;
+  s.c0 = R * per;
+  s.c1 = s.c0 + per;
+  s.r0 = s.c0 * p;
+  s.r1 = R == W - 1 ? nl : s.c1 * p;
+  s.v0 = std::max(0, s.r0 - hc * p);
+  s.v1 = std::min(nl, s.r1 + hc * p + 1);
+  const int64_t hr = (int64_t)hc * p;
+  if (R > 0) s.xf.push_back({R - 1, s.r0 * rowsz, (hr + 1) * rowsz, (s.r0 - hr) * rowsz, hr * rowsz});
+  if (R < W - 1) s.xf.push_back({R + 1, (s.r1 - hr) * rowsz, hr * rowsz, s.r1 * rowsz, (hr + 1) * rowsz});
+  return s;
+}
 
 struct Comm {
   int rank = 0, world = 1;

@@ -821,21 +821,19 @@ struct Problem {
       finer = ok;
       if (!ok) continue;
       D.part = 1;
-      D.c0 = R * s;
-      D.c1 = D.c0 + s;
-      D.r0 = D.c0 * p;
-      D.r1 = R == W - 1 ? nl : D.c1 * p;
+      const SlabPlan sp = slab_plan(n, p, W, R, HALO, ps);
+      D.c0 = sp.c0;
+      D.c1 = sp.c1;
+      D.r0 = sp.r0;
+      D.r1 = sp.r1;
       D.wide = 0;
       D.hw = HALO;
-      D.v0 = D.v0n = std::max(0, D.r0 - HALO * p);
-      D.v1 = D.v1n = std::min(nl, D.r1 + HALO * p + 1);
+      D.v0 = D.v0n = sp.v0;
+      D.v1 = D.v1n = sp.v1;
       D.rc0 = p * (D.c0 / 2);
       D.rc1 = R == W - 1 ? lv[l - 1].a.nl : p * (D.c1 / 2);
-      const int64_t hr = (int64_t)HALO * p;
-      D.halo.clear();
-      if (R > 0) D.halo.push_back({R - 1, D.r0 * ps, (hr + 1) * ps, (D.r0 - hr) * ps, hr * ps});
-      if (R < W - 1) D.halo.push_back({R + 1, (D.r1 - hr) * ps, hr * ps, D.r1 * ps, (hr + 1) * ps});
-      D.halo_n = D.halo;
+      D.halo = sp.xf;
+      D.halo_n = sp.xf;
       auto keepK = [&](int K) { return K >= D.c0 - 1 && K <= D.c1; };
       // Cartesian patches
       {
@@ -944,27 +942,21 @@ struct Problem {
       finer = ok;
       if (!ok) continue;
       D.part = 1;
-      D.c0 = R * s;
-      D.c1 = D.c0 + s;
-      D.r0 = D.c0 * p;
-      D.r1 = R == W - 1 ? nl : D.c1 * p;
       D.wide = wide_halo;
       D.hw = D.wide ? HW : HALO;
-      D.v0n = std::max(0, D.r0 - HALO * p);
-      D.v1n = std::min(nl, D.r1 + HALO * p + 1);
-      D.v0 = std::max(0, D.r0 - D.hw * p);
-      D.v1 = std::min(nl, D.r1 + D.hw * p + 1);
+      const SlabPlan sw = slab_plan(n, p, W, R, D.hw, ld), sn = slab_plan(n, p, W, R, HALO, ld);
+      D.c0 = sw.c0;
+      D.c1 = sw.c1;
+      D.r0 = sw.r0;
+      D.r1 = sw.r1;
+      D.v0n = sn.v0;
+      D.v1n = sn.v1;
+      D.v0 = sw.v0;
+      D.v1 = sw.v1;
       D.rc0 = p * (D.c0 / 2);
       D.rc1 = R == W - 1 ? lv[l - 1].a.nl : p * (D.c1 / 2);
-      auto halo_list = [&](int hc) {
-        std::vector<Xfer> v;
-        const int64_t hr = (int64_t)hc * p;
-        if (R > 0) v.push_back({R - 1, (int64_t)D.r0 * ld, (hr + 1) * ld, (D.r0 - hr) * ld, hr * ld});
-        if (R < W - 1) v.push_back({R + 1, (D.r1 - hr) * ld, hr * ld, (int64_t)D.r1 * ld, (hr + 1) * ld});
-        return v;
-      };
-      D.halo = halo_list(D.hw);
-      D.halo_n = halo_list(HALO);
+      D.halo = sw.xf;
+      D.halo_n = sn.xf;
       // fused tiles (packed ti | tj << 16) of the owned rows
       auto own_tiles = [&](int*& list, int& cnt) {
         std::vector<int> h(cnt), keep;

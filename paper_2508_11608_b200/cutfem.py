@@ -76,6 +76,8 @@ _sig = {
     "cutfem_partition": [_P, _P],
     "cutfem_partition_info": [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
     "cutfem_halo_exchange": [_P, ctypes.c_int, _D, _P],
+    "cutfem_slab_plan": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                         ctypes.POINTER(ctypes.c_int64)],
 }
 for _name, _args in _sig.items():
     getattr(_lib, _name).argtypes = _args
@@ -119,6 +121,17 @@ def make_params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D=0
 
 
 NCCL_ID_BYTES = 128
+
+
+def slab_plan(n_cells, degree, world, rank, halo_cells):
+    """The partition's slab plan of one level (host only): owned / valid
+    lattice rows and the row bands exchanged with the neighbours."""
+    out = (ctypes.c_int64 * 17)()
+    _check(_lib.cutfem_slab_plan(n_cells, degree, world, rank, halo_cells, out))
+    v = list(out)
+    xf = [dict(zip(("peer", "send_off", "send_n", "recv_off", "recv_n"), v[7 + 5 * i:12 + 5 * i]))
+          for i in range(v[6])]
+    return dict(c0=v[0], c1=v[1], r0=v[2], r1=v[3], v0=v[4], v1=v[5], xfers=xf)
 
 
 class Comm:
