@@ -355,3 +355,46 @@ def test_3d_partition_bitexact(w, world):
         a, info = _rows3(g, o["cg_x"])
         r = ref["cg_x"].cpu().numpy().reshape(a.shape[1], a.shape[1], -1)[info["r0"]:info["r1"], :, :a.shape[2]]
         assert np.abs(a - r).max() <= 1e-10 * np.abs(ref["cg_x"].cpu().numpy()).max()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fullsize_config1_partition(world):
+    """config1 (512^2, Q2: 24 x 32-cell Cartesian tiles, wide-halo cut sweeps,
+    the bench's launch configuration) split into `world` slabs: the smoothing
+    step pair and a V-cycle bit-exact on every rank's rows, CG iterations equal"""
+    w = workloads.CONFIG1
+    L = w.n_levels - 1
+    x0, b0 = workloads.lattice_vector(w, 1), workloads.lattice_vector(w, 2)
+    g1 = single(w)
+    x = g1.to_device(x0)
+    b = g1.to_device(b0)
+    g1.smooth(L, x, b)
+    g1.smooth(L, x, b, reverse=True)
+    g1.vcycle(x, b)
+    xs = g1.zeros()
+    it1, _ = g1.solve_cg_mg(xs, b, tol=1e-8)
+    torch.cuda.synchronize()
+    nl, ld = g1.lattice_shape(L)
+    ref = x.cpu().numpy().reshape(nl, ld)[:, :nl]
+    refcg = xs.cpu().numpy().reshape(nl, ld)[:, :nl]
+    g1.close()
+
+    def fn(r, g, s):
+        st = s.cuda_stream
+        x = g.to_device(x0)
+        b = g.to_device(b0)
+        g.smooth(L, x, b, stream=st)
+        g.smooth(L, x, b, reverse=True, stream=st)
+        g.vcycle(x, b, stream=st)
+        xs = g.zeros()
+        it, _ = g.solve_cg_mg(xs, b, tol=1e-8, stream=st)
+        return x, xs, it
+
+    res, gs = run_ranks(w, world, fn, timeout=600)
+    assert gs[0].partition_info(L)["halo"] == 24
+    for g, (x, xs, it) in zip(gs, res):
+        r0, r1, a = owned(g, x, L)
+        np.testing.assert_array_equal(a, ref[r0:r1])
+        assert it == it1
+        _, _, c = owned(g, xs, L)
+        assert np.abs(c - refcg[r0:r1]).max() <= 1e-10 * np.abs(refcg).max()
