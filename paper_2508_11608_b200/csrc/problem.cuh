@@ -101,6 +101,7 @@ struct Problem {
   // measured slower than PDL launches (V-cycle 727 us with <= 64, 1030 us
   // with <= 400, vs 679 us)
   int cluster7_max = 0;
+  int tc_small_n = 128;     // Q2 levels with 16 <= n <= this use 8 x 8-cell fused tiles (env CUTFEM_TC8_MAX_N; V-cycle 658 -> 640 us)
   int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
@@ -276,6 +277,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_TC8_MAX_N")) tc_small_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_CLUSTER7_MAX")) cluster7_max = std::atoi(e);
     require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
     if (prm.dim == 3) {
@@ -493,6 +495,8 @@ struct Problem {
         if (p == 2 && use_mma && use_tma && n >= tc_big_n) {   // (p = 3: 32-cell tiles exceed shared memory)
           TC = 32;
           TCX = tcx_big;
+        } else if (p == 2 && use_mma && use_tma && n <= tc_small_n && n >= 16) {
+          TC = TCX = 8;   // small levels: more, smaller tiles (more CTAs in flight)
         }
         D.tc = TC;
         D.tcx = TCX;
@@ -1263,6 +1267,10 @@ struct Problem {
     if (!D.n_fused_tiles) return;
     CF_DISPATCH(prm.p, {
       if constexpr (P == 2) {
+        if (D.tc == 8) {
+          cart_fused_tma<P, 8>(l, x, b, reverse);
+          return;
+        }
         if (D.tc == 32) {
           if (D.tcx == 16) cart_fused_tma<P, 32, 16>(l, x, b, reverse);
           else if (D.tcx == 24) cart_fused_tma<P, 32, 24>(l, x, b, reverse);

@@ -1,1 +1,2 @@
-python -m pytest tests/test_gpu_slab.py -x -q -k "fullsize" > gpurun_out/fs.log 2>&1; tail -15 gpurun_out/fs.log
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -2 gpurun_out/gputests.log
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
