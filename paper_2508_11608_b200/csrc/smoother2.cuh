@@ -1118,37 +1118,52 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
     if (s == s0) mbar_wait(bar, 0);
     __syncthreads();
     const int np = *pcount, ng = (np + 7) / 8;
-    for (int g = warp; g < ng; g += NT / 32) {
-      const int pq = 8 * g + (lane >> 2);
-      const int base = pq < np ? plist[pq] : -1;
-      double acc[MF > 0 ? MF : 1][2][2];
-      double rs[RR > 0 ? RR : 1];
+#ifndef CF_CART_GPW
+#define CF_CART_GPW 1   // groups of 8 patches per warp iteration (2: measured no faster, spills at 16-cell tiles)
+#endif
+    constexpr int GW = CF_CART_GPW;
+    for (int g = warp; g < ng; g += GW * (NT / 32)) {
+      int base[GW];
+      double acc[GW][MF > 0 ? MF : 1][2][2];
+      double rs[GW][RR > 0 ? RR : 1];
 #pragma unroll
-      for (int mt = 0; mt < MF; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
+      for (int u = 0; u < GW; ++u) {
+        const int gu = g + u * (NT / 32), pq = 8 * gu + (lane >> 2);
+        base[u] = (gu < ng && pq < np) ? plist[pq] : -1;
 #pragma unroll
-      for (int rr = 0; rr < RR; ++rr) rs[rr] = 0.0;
+        for (int mt = 0; mt < MF; ++mt) acc[u][mt][0][0] = acc[u][mt][0][1] = acc[u][mt][1][0] = acc[u][mt][1][1] = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) rs[u][rr] = 0.0;
+      }
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
-        const double v = (base >= 0 && ko[ks] >= 0) ? Xs[base + ko[ks]] : 0.0;
 #pragma unroll
-        for (int mt = 0; mt < MF; ++mt) dmma(af[mt][ks], v, acc[mt][ks & 1][0], acc[mt][ks & 1][1]);
+        for (int u = 0; u < GW; ++u) {
+          const double v = (base[u] >= 0 && ko[ks] >= 0) ? Xs[base[u] + ko[ks]] : 0.0;
 #pragma unroll
-        for (int rr = 0; rr < RR; ++rr) rs[rr] = fma(gr[rr][ks], v, rs[rr]);
+          for (int mt = 0; mt < MF; ++mt) dmma(af[mt][ks], v, acc[u][mt][ks & 1][0], acc[u][mt][ks & 1][1]);
+#pragma unroll
+          for (int rr = 0; rr < RR; ++rr) rs[u][rr] = fma(gr[rr][ks], v, rs[u][rr]);
+        }
       }
 #pragma unroll
-      for (int rr = 0; rr < RR; ++rr) {
-        rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], 1);
-        rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], 2);
-        const int r = 8 * MF + rr;
-        if ((lane & 3) == 0 && base >= 0) Xs[base + (r / NI + 1) * RWP + r % NI + 1] = rs[rr];
-      }
+      for (int u = 0; u < GW; ++u) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int bo = __shfl_sync(0xffffffffu, base, 4 * (2 * (lane & 3) + i));
+        for (int rr = 0; rr < RR; ++rr) {
+          double t = rs[u][rr];
+          t += __shfl_xor_sync(0xffffffffu, t, 1);
+          t += __shfl_xor_sync(0xffffffffu, t, 2);
+          const int r = 8 * MF + rr;
+          if ((lane & 3) == 0 && base[u] >= 0) Xs[base[u] + (r / NI + 1) * RWP + r % NI + 1] = t;
+        }
 #pragma unroll
-        for (int mt = 0; mt < MF; ++mt) {
-          const int r = 8 * mt + (lane >> 2);
-          if (bo >= 0) Xs[bo + (r / NI + 1) * RWP + r % NI + 1] = acc[mt][0][i] + acc[mt][1][i];
+        for (int i = 0; i < 2; ++i) {
+          const int bo = __shfl_sync(0xffffffffu, base[u], 4 * (2 * (lane & 3) + i));
+#pragma unroll
+          for (int mt = 0; mt < MF; ++mt) {
+            const int r = 8 * mt + (lane >> 2);
+            if (bo >= 0) Xs[bo + (r / NI + 1) * RWP + r % NI + 1] = acc[u][mt][0][i] + acc[u][mt][1][i];
+          }
         }
       }
     }

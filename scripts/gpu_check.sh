@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -2 gpurun_out/gputests.log
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
+python -m pytest tests/test_gpu_modes.py tests/test_gpu_fullsize.py -x -q > gpurun_out/t.log 2>&1; tail -2 gpurun_out/t.log
+timeout 900 python scripts/ab.py variants/v27_g1.so variants/v27.so
