@@ -190,6 +190,9 @@ int cutfem_comm_nccl_unique_id(unsigned char* id_out);
 int cutfem_comm_nccl_create(const unsigned char* id, int rank, int world, cutfem_comm* out);
 /* destroys an endpoint that was not attached to a problem */
 int cutfem_comm_destroy(cutfem_comm comm);
+/* On failure the endpoint stays with the caller; a partition that failed
+ * half-way leaves the problem unusable (every later call returns
+ * CUTFEM_ERR_STATE; destroy it). */
 int cutfem_partition(cutfem_problem pb, cutfem_comm comm);
 /* out[8] = {partitioned, r0, r1, v0, v1, rank, world, halo}: owned lattice
  * rows [r0, r1) and valid rows [v0, v1) = owned rows +- `halo` cells of

@@ -31,11 +31,13 @@ static int guarded(F&& f) {
 
 static void check_level(cutfem_problem pb, int level) {
   cf::require(pb != nullptr, cf::ERR_ARG, "null problem handle");
+  cf::require(!pb->p.broken, cf::ERR_STATE, "a failed cutfem_partition left this problem unusable; destroy it");
   cf::require(level >= 0 && level < (int)pb->p.lv.size(), cf::ERR_ARG, "level out of range");
 }
 static void check_built(cutfem_problem pb) {
   cf::require(pb != nullptr, cf::ERR_ARG, "null problem handle");
   cf::require(pb->p.built, cf::ERR_STATE, "cutfem_build_patches has not been called");
+  cf::require(!pb->p.broken, cf::ERR_STATE, "a failed cutfem_partition left this problem unusable; destroy it");
 }
 static void use_stream(cutfem_problem pb, void* stream) { pb->p.st = (cudaStream_t)stream; }
 
@@ -220,7 +222,13 @@ int cutfem_partition(cutfem_problem pb, cutfem_comm comm) {
   return guarded([&]() {
     check_built(pb);
     cf::require(comm != nullptr && comm->c != nullptr, cf::ERR_ARG, "null or already attached comm");
-    pb->p.partition(comm->c);
+    try {
+      pb->p.partition(comm->c);
+    } catch (...) {
+      // some levels may already hold rank-restricted work lists: refuse further use
+      if (pb->p.comm == nullptr) pb->p.broken = true;
+      throw;
+    }
     comm->c = nullptr;   // owned by the problem now
     delete comm;
   });

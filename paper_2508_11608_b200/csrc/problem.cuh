@@ -64,6 +64,7 @@ struct Problem {
   cudaStream_t st = nullptr;
   cudaStream_t cap_st = nullptr;
   bool built = false;
+  bool broken = false;      // a partition failed half-way (capi refuses further hot-path calls)
   bool persistent = false;  // one cooperative launch per smoothing step (env CUTFEM_PERSISTENT=1)
   bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
   int persistent_below = 0; // levels with n <= this use the cooperative one-launch smoothing step (env)
