@@ -398,3 +398,24 @@ def test_fullsize_config1_partition(world):
         assert it == it1
         _, _, c = owned(g, xs, L)
         assert np.abs(c - refcg[r0:r1]).max() <= 1e-10 * np.abs(refcg).max()
+
+
+def test_partition_errors():
+    """a second partition is refused (ERR_STATE) and leaves the problem usable;
+    slab plans that do not divide are refused (ERR_ARG)"""
+    cutfem = _cutfem()
+    w = W_Q2
+    g = cutfem.Problem.from_workload(w)
+    g.partition(cutfem.Comm.local(1)[0])
+    extra = cutfem.Comm.local(1)[0]
+    with pytest.raises(cutfem.CutfemError, match="already partitioned"):
+        g.partition(extra)
+    x = g.to_device(workloads.lattice_vector(w, 3))
+    b = g.to_device(workloads.lattice_vector(w, 4))
+    g.smooth(-1, x, b)
+    torch.cuda.synchronize()
+    assert np.all(np.isfinite(g.to_host(x)))
+    with pytest.raises(cutfem.CutfemError):
+        cutfem.slab_plan(100, 2, 3, 0, 4)
+    with pytest.raises(cutfem.CutfemError):
+        cutfem.slab_plan(16, 2, 4, 0, 4)
