@@ -495,7 +495,10 @@ struct Problem {
         int TCX = TC;
         if (p == 2 && use_mma && use_tma && n >= tc_big_n) {   // (p = 3: 32-cell tiles exceed shared memory)
           TC = 32;
-          TCX = tcx_big;
+          // 24 x 32 balances the single co-resident wave at 512^2; on larger
+          // levels (several waves through the split sweep) 32 x 32 has less
+          // apron overhead: 4096^2 sweep 662 vs 746 us
+          TCX = n >= 1024 ? 32 : tcx_big;
         } else if (p == 2 && use_mma && use_tma && n <= tc_small_n && n >= 16) {
           TC = TCX = 8;   // small levels: more, smaller tiles (more CTAs in flight)
         }

@@ -32,9 +32,12 @@ for nlev in (10, 11, 12):
         return float(np.median(ts))
     ms = t(lambda: g.smooth(L, x, b))
     cart = t(lambda: g.colour_step(L, 2, 0, x, b))
-    cut = t(lambda: g.colour_step(L, 1, 0, x, b))
+    cut = t(lambda: g.colour_step(L, 3, 0, x, b)) / (4 * w.n_c)   # one cut step of the ping-pong sweeps
+    z = g.zeros()
+    vc = t(lambda: (z.zero_(), g.vcycle(z, b)), 5)
     cart_bytes = 24.0 * 4 * info.n_inside
+    cut_bytes = sum(info.cut_step_bytes[:4]) / 4.0
     print(f"n={info.n} dofs={info.n_dofs} step={ms*1e3:.1f}us ({info.n_dofs/ms/1e6:.3g} DoF/s) "
           f"cart_sweep={cart*1e3:.1f}us ({cart_bytes/cart/1e6:.0f} GB/s) cut_step={cut*1e3:.1f}us "
-          f"cut patches/colour={list(info.n_cutp)}", flush=True)
+          f"({cut_bytes/cut/1e6:.0f} GB/s) vcycle={vc:.2f}ms cut patches/colour={list(info.n_cutp)[:4]}", flush=True)
     g.close()
