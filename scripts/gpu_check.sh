@@ -1,2 +1,3 @@
-timeout 900 python scripts/large_size.py 2>&1 | tail -3
-python -m pytest tests/test_gpu_modes.py tests/test_gpu_fullsize.py -x -q > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; tail -1 gpurun_out/gputests.log
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
