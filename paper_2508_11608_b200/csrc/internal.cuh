@@ -121,6 +121,7 @@ struct LevelData {
   int tc = 16;                       // cells of the fused tiles of this level in y (rows)
   int tcx = 16;                      // ... and in x
   int* fused_ext = nullptr;          // fused tiles dilated by one tile (split sweep through xs)
+  unsigned long long* gbar = nullptr; // grid-barrier counter of the in-place fused sweep
   int n_fused_ext = 0;
   int n_cutp[8] = {};
   int cutp_off[9] = {};

@@ -525,6 +525,8 @@ struct Problem {
           CF_LAUNCHED();
         }
         D.fused_ext = te;
+        D.gbar = alloc<unsigned long long>(1);
+        CF_CUDA(cudaMemsetAsync(D.gbar, 0, sizeof(unsigned long long), st));
       }
       D.cart_tiles = alloc<int>(tiles.size());
       if (!tiles.empty())
@@ -1240,7 +1242,7 @@ struct Problem {
     }
     if (!cart_split && D.n_fused_tiles <= cap) {
       launch_ex(true, k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
-                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, 1);
+                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, D.gbar);
       CF_LAUNCHED();
       cart_done(l, x, reverse);
       return;
@@ -1248,11 +1250,11 @@ struct Problem {
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
     if (D.n_fused_ext)
       launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
-             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, 0);
+             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned long long*)nullptr);
     CF_LAUNCHED();
     halo_n(l, D.xs);
     launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
-           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, 0);
+           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, (unsigned long long*)nullptr);
     CF_LAUNCHED();
     cart_done(l, x, reverse);
     return;

@@ -1037,6 +1037,21 @@ __global__ void k_andnot_flags(const uint8_t* a, const uint8_t* b, int64_t n, ui
 namespace cf {
 
 // ---- fused Cartesian sweep, v2: TMA tile loads, hoisted operand offsets ----
+// grid-wide barrier of a cooperative (co-resident) launch: one arrival per
+// CTA on a monotonic 64-bit counter owned by the caller (one per launch
+// configuration, never reset: the target is the next multiple of the grid
+// size).  Control only -- the CTAs' region loads have completed (TMA
+// mbarrier) before they arrive, which is all the in-place sweep needs.
+__device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long nb = gridDim.x, t = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (t / nb + 1) * nb;
+    while (*(volatile unsigned long long*)ctr < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
 template <int P, int TC, int TCX = TC>
 struct CartTmaSmem {
   // TC = cells per tile in y (rows: the partitioned direction), TCX in x
@@ -1057,7 +1072,8 @@ template <int P, int TC, int NT = 256, int TCX = TC>
 __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
-                                                        double* xout, int reverse, int s0, int s1, int gsync) {
+                                                        double* xout, int reverse, int s0, int s1,
+                                                        unsigned long long* gbar) {
   using C = CartMMA<P>;
   using S = CartTmaSmem<P, TC, TCX>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
@@ -1170,7 +1186,7 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
     __syncthreads();
   }
   if (s1 == s0) mbar_wait(bar, 0);
-  if (gsync) cooperative_groups::this_grid().sync();
+  if (gbar) grid_barrier(gbar);
   // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
   const int ahi = (ci0 + TCX >= n) ? L.nl : P * (ci0 + TCX), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   for (int bb = P * cj0 + warp; bb < bhi; bb += NT / 32) {
