@@ -102,6 +102,10 @@ struct Problem {
   // measured slower than PDL launches (V-cycle 727 us with <= 64, 1030 us
   // with <= 400, vs 679 us)
   int cluster7_max = 0;
+  bool cut_grid7 = false;   // cut sweeps of large levels in one cooperative launch (env CUTFEM_CUT_GRID7;
+                            // measured slower: 51.6 vs 27.6 us per config1 sweep set, the grid barrier costs more than a PDL launch gap)
+  int cut_grid7_min_np = 256;  // ... when a colour has at least this many cut patches (CUTFEM_CUT_GRID7_MIN_NP)
+  unsigned long long* cut_gbar = nullptr;  // grid-barrier counters of k_cut_sweeps_grid7, one per level
   int tc_small_n = 128;     // Q2 levels with 16 <= n <= this use 8 x 8-cell fused tiles (env CUTFEM_TC8_MAX_N; V-cycle 658 -> 640 us)
   int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
@@ -280,7 +284,11 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TC8_MAX_N")) tc_small_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_CLUSTER7_MAX")) cluster7_max = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_CUT_GRID7")) cut_grid7 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_CUT_GRID7_MIN_NP")) cut_grid7_min_np = std::atoi(e);
     require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
+    cut_gbar = alloc<unsigned long long>(std::max(1, prm.n_levels));
+    CF_CUDA(cudaMemset(cut_gbar, 0, sizeof(unsigned long long) * std::max(1, prm.n_levels)));
     if (prm.dim == 3) {
       setup_mesh3();
       return;
@@ -1548,7 +1556,64 @@ struct Problem {
     return true;
   }
 
+  // all cut sweeps of a large level in one cooperative launch with the patch
+  // maps (k_cut_sweeps_grid7); false if the grid does not fit co-resident
+  bool cut_sweeps_grid7(int l, double* x, const double* b, int reverse, int npmax) {
+    LevelData& D = lv[l];
+    CutSweepArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.L = D.a;
+    A.desc = (const CutDesc*)D.act_desc;
+    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.act_off[c];
+    A.copy = D.copy_lists;
+    for (int i = 0; i < 5; ++i)
+      for (int c = 0; c < 4; ++c) {
+        A.copy_off[i][c] = D.copy_off[i][c];
+        A.copy_n[i][c] = D.copy_n[i][c];
+      }
+    A.x = x;
+    A.xs = D.xs;
+    A.b = b;
+    A.n_c = prm.n_c;
+    A.reverse = reverse;
+    A.gmap = D.gmap;
+    bool ok = false;
+    CF_DISPATCH(prm.p, {
+      if constexpr (P <= 3) {
+#ifndef CF_GRID7_G
+#define CF_GRID7_G 1     // patches per CTA of k_cut_sweeps_grid7
+#endif
+        constexpr int G = CF_GRID7_G, NTG = 128;
+        const size_t smb = (size_t)G * ((CutMapSmem<P>::bytes + 127) & ~(size_t)127);
+        static int cap = -1;
+        if (cap < 0) {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_grid7<P, G, NTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+          int nsm = 0, dev = 0, per = 0;
+          CF_CUDA(cudaGetDevice(&dev));
+          CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+          CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cut_sweeps_grid7<P, G, NTG>, NTG * G, smb));
+          cap = per * nsm;
+        }
+        const int grid = std::min(cap, ceil_div(npmax, G));
+        if (grid > 0) {
+          launch_ex(true, k_cut_sweeps_grid7<P, G, NTG>, dim3(grid), dim3(NTG * G), smb, A, cut_gbar + l);
+          CF_LAUNCHED();
+          ok = true;
+        }
+      }
+    });
+    return ok;
+  }
+
   void cut_sweeps(int l, double* x, const double* b, int reverse) {
+    if (cut_grid7 && cut_gbar && !lv[l].part && lv[l].gmap && cut_map && prm.cut_mode == 0 && cta_cut &&
+        prm.p <= 3 && (prm.n_c * 4) % 2 == 0) {
+      int npmax = 0;
+      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].act_off[c + 1] - lv[l].act_off[c]);
+      if (npmax >= cut_grid7_min_np && (cluster7_max <= 0 || npmax > cluster7_max) &&
+          cut_sweeps_grid7(l, x, b, reverse, npmax))
+        return;
+    }
     if (cluster7_max > 0 && !lv[l].part && lv[l].gmap && cut_map && prm.cut_mode == 0 && cta_cut && prm.p <= 3) {
       int npmax = 0;
       for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].act_off[c + 1] - lv[l].act_off[c]);

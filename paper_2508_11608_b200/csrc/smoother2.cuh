@@ -2288,4 +2288,67 @@ __global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster7(CutSweepArgs A) 
   }
 }
 
+// grid-wide barrier with release/acquire: the CTAs' global writes before the
+// barrier are visible to every CTA after it (the cut steps read the previous
+// step's W through L2).  Counter as grid_barrier(): monotonic, one per level.
+__device__ __forceinline__ void grid_barrier_mem(unsigned long long* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long nb = gridDim.x, t = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (t / nb + 1) * nb;
+    while (*(volatile unsigned long long*)ctr < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// all n_c x 4 cut steps of a smoothing step in ONE cooperative launch over the
+// GPU (k_cut_sweeps_cluster7 with blockIdx / gridDim for the cluster rank /
+// size and a grid barrier between the ping-pong steps): removes the launch
+// gap of each of the 8 cut colour steps on large levels.
+template <int P, int G, int NTG>
+__global__ void __launch_bounds__(NTG * G) k_cut_sweeps_grid7(CutSweepArgs A, unsigned long long* gbar) {
+  using S = CutMapSmem<P>;
+  extern __shared__ __align__(128) unsigned char smg7[];
+  const int tid = threadIdx.x, grp = tid / NTG, gt = tid % NTG;
+  const int cr = (int)blockIdx.x, cs = (int)gridDim.x;
+  unsigned char* gsm = smg7 + (size_t)grp * ((S::bytes + 127) & ~(size_t)127);
+  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
+  const int k0 = cr * G + grp;
+  {
+    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c];
+    if (k0 < np) cut7_prologue<P, NTG>(A.desc, A.cut_off[c] + k0, A.gmap, gsm, gt, 1 + grp);
+  }
+  pdl_wait();
+  double* bufs[2] = {A.x, A.xs};
+  int prev = 4;
+  const int nsteps = A.n_c * 4;
+  for (int s = 0; s < nsteps; ++s) {
+    const int c = step_colour(s);
+    const double* R = bufs[s & 1];
+    double* W = bufs[(s + 1) & 1];
+    const int nco = A.copy_n[prev][c];
+    const int32_t* cl = A.copy + A.copy_off[prev][c];
+    for (int e = cr * NTG * G + tid; e < nco; e += cs * NTG * G) W[cl[e]] = __ldcg(R + cl[e]);
+    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
+    const int rounds = (np + cs * G - 1) / (cs * G);
+    for (int r = 0; r < rounds; ++r) {
+      const int k = (r * cs + cr) * G + grp;
+      if (k < np) {
+        if (r > 0) cut7_prologue<P, NTG>(A.desc, p0 + k, A.gmap, gsm, gt, 1 + grp);
+        cut7_main<P, NTG, true>(A.L, R, W, A.b, gsm, gt, 1 + grp);
+        group_sync(1 + grp, NTG);
+      }
+    }
+    if (s + 1 < nsteps) {
+      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn];
+      if (k0 < npn) cut7_prologue<P, NTG>(A.desc, A.cut_off[cn] + k0, A.gmap, gsm, gt, 1 + grp);
+    }
+    prev = c;
+    grid_barrier_mem(gbar);
+    if (s == 0) pdl_trigger();   // every CTA is resident: dependents may be scheduled
+  }
+}
+
 }  // namespace cf

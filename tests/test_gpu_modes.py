@@ -54,10 +54,12 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
                                  {"CUTFEM_CART_SPLIT": "1", "CUTFEM_MMA": "0"}, {"CUTFEM_TC32_MIN_N": "32"},
                                  {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CUT_GRID": "1"}, {"CUTFEM_CUTMAP": "0"}, {"CUTFEM_VC_MAX_N": "0"}, {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_TCX": "24"},
                                  {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_TCX": "16", "CUTFEM_CART_SPLIT": "1"},
-                                 {"CUTFEM_CLUSTER7_MAX": "100000"}],
+                                 {"CUTFEM_CLUSTER7_MAX": "100000"}, {"CUTFEM_CUT_GRID7": "0"},
+                                 {"CUTFEM_CUT_GRID7": "1", "CUTFEM_CUT_GRID7_MIN_NP": "1"}],
                          ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply",
                               "cut-step-v4", "cut-step-v5", "cluster-cut-sweeps", "cart-split-tma",
-                              "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split", "cut-sweeps-one-grid-launch", "cut-step-matrix-free", "vcycle-launch-per-step", "tile24x32", "tile16x32-split", "cluster-cut-sweeps-maps"])
+                              "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split", "cut-sweeps-one-grid-launch", "cut-step-matrix-free", "vcycle-launch-per-step", "tile24x32", "tile16x32-split", "cluster-cut-sweeps-maps",
+                              "cut-step-launch-per-colour", "cut-sweeps-grid7-all-levels"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
