@@ -103,7 +103,7 @@ struct Problem {
   // with <= 400, vs 679 us)
   int cluster7_max = 0;
   bool cut_grid7 = false;   // cut sweeps of large levels in one cooperative launch (env CUTFEM_CUT_GRID7;
-                            // measured slower: 51.6 vs 27.6 us per config1 sweep set, the grid barrier costs more than a PDL launch gap)
+                            // measured slower: 48.2 vs 27.6 us per config1 sweep set, the grid barrier costs more than a PDL launch gap)
   int cut_grid7_min_np = 256;  // ... when a colour has at least this many cut patches (CUTFEM_CUT_GRID7_MIN_NP)
   unsigned long long* cut_gbar = nullptr;  // grid-barrier counters of k_cut_sweeps_grid7, one per level
   int tc_small_n = 128;     // Q2 levels with 16 <= n <= this use 8 x 8-cell fused tiles (env CUTFEM_TC8_MAX_N; V-cycle 658 -> 640 us)

@@ -2294,11 +2294,13 @@ __global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster7(CutSweepArgs A) 
 __device__ __forceinline__ void grid_barrier_mem(unsigned long long* ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long nb = gridDim.x, t = atomicAdd(ctr, 1ull);
+    const unsigned long long nb = gridDim.x;
+    unsigned long long t, v;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(t) : "l"(ctr) : "memory");
     const unsigned long long target = (t / nb + 1) * nb;
-    while (*(volatile unsigned long long*)ctr < target) __nanosleep(32);
-    __threadfence();
+    do {
+      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
