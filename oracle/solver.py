@@ -23,26 +23,88 @@ from .geometry import CARTESIAN, CUTPATCH, Circle, build_patches, hierarchy
 from .transfer import prolongation_matrix
 
 
+LOCAL_READINGS = ("principal", "patch", "patch_matrix", "no_ghost")
+
+
+def _boundary_ghost_rows(lv, prm, patches):
+    """Per patch: the rows (at the interior set I) of the ghost-face terms on
+    faces F(T1, T2) with exactly one of T1, T2 in the patch -- the coupling
+    "through ghost penalties between neighboring vertex patches" of PAPER.md
+    l.181 -- as a sparse (|I| x n_dofs) matrix.  Only for the sensitivity
+    study of the local-solver readings (R9 / "Q2/Q3 iteration
+    counts"); the default reading does not use it."""
+    import scipy.sparse as sp
+    from .assemble import ghost_face_matrix
+    from .geometry import ghost_faces
+    prm = prm.resolved(lv.p)
+    by_cell = {}
+    faces = []
+    for axis, i, j in ghost_faces(lv):
+        c2 = (i + 1, j) if axis == 0 else (i, j + 1)
+        d, M = ghost_face_matrix(lv, axis, i, j, prm)
+        faces.append(((i, j), c2, d, M))
+        by_cell.setdefault((i, j), []).append(len(faces) - 1)
+        by_cell.setdefault(c2, []).append(len(faces) - 1)
+    out = []
+    for pt in patches:
+        cells = set(pt.cells)
+        fids = {f for c in cells for f in by_cell.get(c, ())}
+        pos = {int(g): r for r, g in enumerate(pt.interior)}
+        rows, cols, vals = [], [], []
+        for f in fids:
+            c1, c2, d, M = faces[f]
+            if (c1 in cells) == (c2 in cells):
+                continue                      # interior face of the patch (or none)
+            for a, ga in enumerate(d):
+                r = pos.get(int(ga))
+                if r is None:
+                    continue
+                rows.extend([r] * d.size); cols.extend(d.tolist()); vals.extend(M[a].tolist())
+        out.append(sp.csr_matrix((vals, (rows, cols)), shape=(pt.interior.size, lv.n_dofs)))
+    return out
+
+
 class LevelData:
-    def __init__(self, lv, prm, vertices="active"):
+    """One level with A_l, its vertex patches and local solvers.
+
+    `local` selects the reading of the local problem of PAPER.md l.156-164 /
+    l.181 (R9, R10): "principal" (default) -- A_j = rows/columns of
+    A_l at the interior set and the residual of the global A_l;
+    "patch" -- A_j and the residual rows both from the patch-local operator
+    (patch cells and the ghost faces between two patch cells; the ghost faces
+    on the patch boundary are dropped); "patch_matrix" -- only A_j patch-local;
+    "no_ghost" -- A_j without any ghost term.  The non-default readings exist
+    for the iteration-count sensitivity study (scripts/oracle_sensitivity.py)
+    and are 2D only."""
+
+    def __init__(self, lv, prm, vertices="active", local="principal"):
         self.lv = lv
+        if local not in LOCAL_READINGS:
+            raise ValueError(local)
+        self.local = local
         if getattr(lv, "dim", 2) == 3:
             from .dim3 import assemble_matrix3, build_patches3
             self.A = assemble_matrix3(lv, prm)
             self.patches = build_patches3(lv)
+            if local != "principal":
+                raise ValueError("local readings other than 'principal' are 2D only")
         else:
             self.A = assemble_matrix(lv, prm)
             self.patches = build_patches(lv, vertices)
         self.nc = lv.n_colours
         self.groups = {(k, c): [] for k in (CARTESIAN, CUTPATCH) for c in range(self.nc)}
         self.inv = []
+        self.bnd = _boundary_ghost_rows(lv, prm, self.patches) if local in ("patch", "patch_matrix") else None
+        A_ng = assemble_matrix(lv, prm, with_ghost=False) if local == "no_ghost" else None
         for idx, pt in enumerate(self.patches):
             self.groups[(pt.kind, pt.colour)].append(idx)
             I = pt.interior
             if I.size == 0:
                 self.inv.append(np.zeros((0, 0)))
                 continue
-            Aj = self.A[I][:, I].toarray()
+            Aj = (A_ng if A_ng is not None else self.A)[I][:, I].toarray()
+            if self.bnd is not None:
+                Aj = Aj - self.bnd[idx][:, I].toarray()
             self.inv.append(np.linalg.inv(Aj))
 
     def colour_step(self, x, b, kind, colour):
@@ -53,7 +115,10 @@ class LevelData:
         for idx in self.groups[(kind, colour)]:
             I = self.patches[idx].interior
             if I.size:
-                x[I] += self.inv[idx] @ r[I]
+                rI = r[I]
+                if self.local == "patch":
+                    rI = rI + self.bnd[idx] @ x
+                x[I] += self.inv[idx] @ rI
 
     def smooth(self, x, b, n_c, reverse=False):
         """S(x, b) of eq. (smoother-split): Cartesian
@@ -72,14 +137,14 @@ class Hierarchy:
     """Levels 0..L of PAPER.md l.65-69 with operators, patches and transfers."""
 
     def __init__(self, x0, y0, length, n0, n_levels, circle, p, prm=None, n_c=2, symmetric=True, vertices="active",
-                 levels=None):
+                 levels=None, local="principal"):
         self.prm = prm if prm is not None else Params()
         self.p = p
         self.n_c = n_c
         self.symmetric = symmetric
         if levels is None:
             levels = hierarchy(x0, y0, length, n0, n_levels, circle, p)
-        self.levels = [LevelData(lv, self.prm, vertices) for lv in levels]
+        self.levels = [LevelData(lv, self.prm, vertices, local) for lv in levels]
         if getattr(levels[0], "dim", 2) == 3:
             from .dim3 import prolongation_matrix3 as prolong
         else:
@@ -142,26 +207,34 @@ class Hierarchy:
             rho = rho_new
         return x, it, hist
 
-    def solve_gmres(self, b, tol=1e-9, max_it=500):
-        """Full (non-restarted) right-preconditioned GMRES with modified
-        Gram-Schmidt (Table 1 caption: "Multigrid preconditioner for
-        GMRES solver, iteration counts to reduce residual by 10^-9")."""
+    def solve_gmres(self, b, tol=1e-9, max_it=500, left=False):
+        """Full (non-restarted) GMRES with modified Gram-Schmidt (PAPER.md
+        Table 1 caption: "Multigrid preconditioner for GMRES solver, iteration
+        counts to reduce residual by 10^-9").  Right preconditioning (the
+        default) measures the true residual ||b - A x||; left=True solves
+        M A x = M b and measures the preconditioned residual ||M (b - A x)||
+        (the paper does not say which; sensitivity study only)."""
         A = self.fine.A
         n = b.size
-        beta = np.linalg.norm(b)
+        r0 = self.precondition(b) if left else b
+        beta = np.linalg.norm(r0)
         hist = [beta]
         if beta == 0.0:
             return np.zeros(n), 0, hist
-        V = [b / beta]
+        V = [r0 / beta]
         Z = []
         H = np.zeros((max_it + 1, max_it))
         g = np.zeros(max_it + 1); g[0] = beta
         cs, sn = np.zeros(max_it), np.zeros(max_it)
         it = 0
         for k in range(max_it):
-            z = self.precondition(V[k])
+            if left:
+                z = V[k]
+                w = self.precondition(A @ z)
+            else:
+                z = self.precondition(V[k])
+                w = A @ z
             Z.append(z)
-            w = A @ z
             for i in range(k + 1):
                 H[i, k] = w @ V[i]
                 w = w - H[i, k] * V[i]

@@ -94,6 +94,37 @@ def test_ghost_single_line_kink_closed_form(sigma):
     assert abs(u @ (G @ u) - expect) < 1e-12 * expect
 
 
+@pytest.mark.parametrize("sigma", [-1, 1])
+@pytest.mark.parametrize("axis", [0, 1])
+@pytest.mark.parametrize("p,k", [(2, 1), (2, 2), (3, 1), (3, 2), (3, 3)])
+def test_ghost_kink_closed_form_each_order(p, k, axis, sigma):
+    # u = s^(k-1)|s|, s = x - x_F (or y - y_F), is piecewise a polynomial of
+    # degree k <= p on each side of the mesh line x = x_F (exact in Q_p), C^(k-1)
+    # across it, and its k-th normal derivative jumps by 2 k!.  So only the
+    # order-k term of g_l sees it:
+    #   g(u,u) = gamma_k h^(2k+sigma)/(k!)^2 (2 k!)^2 |F| = 4 gamma_k h^(2k+sigma) h
+    # per ghost face on that line.  Distinct gamma_1..gamma_p catch an index
+    # slip; both sigma catch a wrong h power; k = 2, 3 catch (k!)^2 vs k!.
+    lv = paper_level(16, p)
+    gam = [0.1, 0.23, 0.37][:p]
+    G = assemble_matrix(lv, Params(gamma_k=gam, sigma=sigma), with_cells=False)
+    line = 6
+    if axis == 0:
+        xF = lv.x0 + line * lv.h
+        u = interp(lv, lambda x, y: (x - xF) ** (k - 1) * np.abs(x - xF))
+    else:
+        yF = lv.y0 + line * lv.h
+        u = interp(lv, lambda x, y: (y - yF) ** (k - 1) * np.abs(y - yF))
+    nf = sum(1 for (ax, i, j) in ghost_faces(lv) if ax == axis and (i if axis == 0 else j) == line - 1)
+    assert nf > 0
+    expect = nf * 4.0 * gam[k - 1] * lv.h ** (2 * k + sigma) * lv.h
+    # rounding: the face terms away from the line cancel in G u; bound by the
+    # absolute quadratic form (|u|^T |G| |u| is ~1e3 x expect at k = 3)
+    scale = np.abs(u) @ (abs(G) @ np.abs(u))
+    assert abs(u @ (G @ u) - expect) < 1e-13 * scale + 1e-12 * expect, (u @ (G @ u), expect, scale)
+    assert abs(u @ (G @ u) - expect) < 1e-6 * expect
+
+
 @pytest.mark.parametrize("p,ns", [(1, (16, 32, 64)), (2, (8, 16, 32)), (3, (8, 16, 32))])
 def test_manufactured_solution_rate(p, ns):
     # optimal O(h^(p+1)) L2 convergence (BASELINE.json north_star) for

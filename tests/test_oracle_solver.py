@@ -145,23 +145,59 @@ def test_q1_gmres_counts_match_paper(row):
 
 
 @pytest.mark.parametrize("L", [6, 7])
-def test_q1_vcycle_counts_bounded_by_paper(L):
-    # Table 3 (stationary V-cycle, Q1): converges, no more iterations than the
-    # paper, more than GMRES, and n_c = 2 beats n_c = 1 (l.269-270)
+def test_q1_vcycle_counts_band(L):
+    # Table 3 (stationary V-cycle, Q1, l.271-290): two-sided band
+    # paper/2 <= oracle <= paper; more iterations than GMRES; n_c = 2 beats
+    # n_c = 1 (l.269-270)
     paper = {(r[1], r[2], r[3]): r[4] for r in tables() if r[0] == "T3"}
     it1, it2 = run("T3", L, 1, 1), run("T3", L, 1, 2)
-    assert 0 < it2 < it1 <= paper[(L, 1, 1)]
-    assert it2 <= paper[(L, 1, 2)]
+    assert paper[(L, 1, 1)] // 2 <= it1 <= paper[(L, 1, 1)]
+    assert paper[(L, 1, 2)] // 2 <= it2 <= paper[(L, 1, 2)]
+    assert it2 < it1
     assert it2 >= run("T2", L, 1, 2)
 
 
 @pytest.mark.parametrize("L", [6, 7])
-def test_q2_q3_no_worse_than_paper_and_nc_helps_q3(L):
-    # Tables 2: Q2/Q3 GMRES counts; our smoother (patches at every vertex of
-    # Omega_l, R3) is at least as strong; a second cut sweep helps Q3
-    # ("a second smoothing step on the cut cells is crucial", l.268).
+def test_q2_q3_gmres_band_nc2_and_nc_helps_q3(L):
+    # Table 2, n_c = 2 columns (= Table 1 circle block): two-sided band
+    # paper/3 <= oracle <= paper for Q2 and Q3 (the oracle's smoother is
+    # stronger than the paper's at Q2/Q3; DESIGN.md "Q2/Q3 iteration counts:
+    # sensitivity study" lists the readings tried), and a second cut sweep
+    # helps Q3 ("a second smoothing step on the cut cells is crucial", l.268)
     paper = {(r[1], r[2], r[3]): r[4] for r in tables() if r[0] == "T2"}
     for p in (2, 3):
-        for nc in (1, 2):
-            assert run("T2", L, p, nc) <= paper[(L, p, nc)]
+        got = run("T2", L, p, 2)
+        assert paper[(L, p, 2)] / 3.0 <= got <= paper[(L, p, 2)], (p, got)
     assert run("T2", L, 3, 2) < run("T2", L, 3, 1)
+    assert run("T2", L, 2, 1) <= paper[(L, 2, 1)]
+
+
+@pytest.mark.xfail(strict=True, reason="known gap, DESIGN.md 'Q2/Q3 iteration counts: sensitivity study': no reading "
+                   "tried reproduces Table 2's Q3 n_c=1 blow-up (132 GMRES iterations at L=6)")
+def test_q3_nc1_gmres_blowup_table2():
+    paper = {(r[1], r[2], r[3]): r[4] for r in tables() if r[0] == "T2"}
+    assert run("T2", 6, 3, 1) >= paper[(6, 3, 1)] / 2
+
+
+@pytest.mark.xfail(strict=True, reason="known gap, DESIGN.md 'Q2/Q3 iteration counts: sensitivity study': the oracle's "
+                   "stationary V-cycle converges for Q3 n_c=1 where Table 3 prints divergence")
+def test_q3_nc1_vcycle_divergence_table3():
+    assert run("T3", 6, 3, 1) == -1
+
+
+@pytest.mark.parametrize("L,paper_row", [(6, (5.4, 5.7, 5.8)), (7, (5.0, 5.3, 5.5))])
+def test_table4_fractional_iterations_band(L, paper_row):
+    # Table 4 (l.295-313): Q1 GMRES fractional iteration counts
+    # n_frac = n_it (-8) / log10(||r_n|| / ||r_0||) (l.350-353) at
+    # gamma_1 = 0.05, 0.10, 0.15 (n_c = 2 as in Table 1): within 1.0 of the
+    # printed values and non-decreasing in gamma_1 over that window, as printed
+    got = []
+    for g1 in (0.05, 0.10, 0.15):
+        w = workloads.paper_level(1, L, n_c=2)
+        h = from_workload(w, prm=Params(gamma_k=[g1]), symmetric=False)
+        b = np.random.default_rng(7).standard_normal(h.fine.lv.n_dofs)
+        _, it, hist = h.solve_gmres(b, 1e-9, 300)
+        got.append(fractional_iterations(it, hist[-1], hist[0]))
+    for g, p in zip(got, paper_row):
+        assert abs(g - p) <= 1.0, (got, paper_row)
+    assert got[0] <= got[1] + 0.02 and got[1] <= got[2] + 0.02, got
