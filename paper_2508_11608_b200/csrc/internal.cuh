@@ -142,6 +142,17 @@ struct LevelData {
   int64_t cut_bytes[8] = {};         // algorithmic bytes of one cut colour step (k_cut_step7) per colour
   void* desc = nullptr;              // CutDesc per cut patch (smoother2.cuh)
   double* xs = nullptr;              // shadow lattice vector for the ping-pong cut steps
+  // dataflow cut sweep (cutdf.cuh): segment blobs, dependencies, step flags
+  int df_nseg = 0;
+  size_t df_smem = 0;
+  unsigned char* df_blob = nullptr;
+  long long* df_seg_off = nullptr;
+  int* df_dep_off = nullptr;
+  int* df_deps = nullptr;
+  unsigned* df_flags = nullptr;
+  int df_max_dep = 0;
+  long long df_map_bytes = 0;        // G_j bytes of one launch (read once, applied n_c times)
+  long long cut_method_bytes[8] = {};  // method bytes of one cut colour step per colour
   int32_t* copy_lists = nullptr;     // node lists: [prev][cur] = N_prev \ N_cur (prev = 4: read band)
   int copy_off[5][4] = {};           // offsets into copy_lists
   int copy_n[5][4] = {};

@@ -23,6 +23,7 @@
 #include "tables.cuh"
 #include "comm.cuh"
 #include "vcycle_cluster.cuh"
+#include "cutdf.cuh"
 
 namespace cf {
 
@@ -110,6 +111,14 @@ struct Problem {
   int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
+  // all cut steps of a smoothing step in one dataflow launch (cutdf.cuh) on
+  // unpartitioned levels (env CUTFEM_DF=0: one PDL launch per step)
+  bool use_df = true;
+  int df_budget = 0;            // shared-memory bytes per segment (env CUTFEM_DF_BUDGET; 0 = most CTAs per SM that fit)
+  int df_tile = 4;              // Morton tile of the segment packing, in vertices (env CUTFEM_DF_TILE)
+  size_t df_smem_max = 0;       // largest dynamic shared memory of any level's k_cut_df launch
+  int df_spin_ns = 0;           // __nanosleep back-off of the flag polls (env CUTFEM_DF_SPIN)
+  bool df_coop = false;         // cooperative launch attribute on k_cut_df (env CUTFEM_DF_COOP=1)
   // slab partition: comm != nullptr after partition()
   Comm* comm = nullptr;
   static constexpr int HALO = 4;   // halo width in cells (the fused Cartesian apron)
@@ -286,6 +295,12 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_CLUSTER7_MAX")) cluster7_max = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_CUT_GRID7")) cut_grid7 = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT_GRID7_MIN_NP")) cut_grid7_min_np = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_DF")) use_df = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_DF_BUDGET")) df_budget = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_DF_TILE")) df_tile = std::atoi(e);
+    if (const char* e = std::getenv("CUTFEM_DF_COOP")) df_coop = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_DF_SPIN")) df_spin_ns = std::atoi(e);
+    require(df_tile >= 1, ERR_ARG, "CUTFEM_DF_TILE must be >= 1");
     require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
     cut_gbar = alloc<unsigned long long>(std::max(1, prm.n_levels));
     CF_CUDA(cudaMemset(cut_gbar, 0, sizeof(unsigned long long) * std::max(1, prm.n_levels)));
@@ -596,6 +611,8 @@ struct Problem {
       D.act_desc = D.desc;
       for (int c = 0; c < 5; ++c) D.act_off[c] = D.cutp_off[c];
       build_copy_lists(D, D.ent_node, D.ent_col_off, (const CutDesc*)D.desc, ncp);
+      if (ncp) method_bytes(D, ncp);
+      if (ncp && D.gmap && use_df && cta_cut && (prm.n_c * 4) % 2 == 0) build_df(D, ncp);
       sync();
     }
     build_coarse();
@@ -672,6 +689,116 @@ struct Problem {
     for (void* q : {(void*)Gd, (void*)doff, (void*)nnz}) {
       cudaFree(q);
       allocs.erase(std::remove(allocs.begin(), allocs.end(), q), allocs.end());
+    }
+  }
+
+  // method bytes of one cut colour step: per
+  // patch the paper's local solver streams A_j^{-1} (m^2), the element
+  // matrices of its cut cells ((p+1)^4 each), reads b_I and the coupled window
+  // values x_I, x_E (m + nnz) and writes x_I (m): 8 (m^2 + n_cut (p+1)^4 +
+  // 3 m + nnz) bytes, whatever the implementation (the patch maps of R13 are
+  // an implementation choice and are not counted)
+  void method_bytes(LevelData& D, int ncp) {
+    const int p = prm.p, e4 = (p + 1) * (p + 1) * (p + 1) * (p + 1);
+    std::vector<CutDesc> hd(ncp);
+    CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < 8; ++c) D.cut_method_bytes[c] = 0;
+    for (int c = 0; c < 4; ++c)
+      for (int k = D.cutp_off[c]; k < D.cutp_off[c + 1]; ++k) {
+        const CutDesc& d = hd[k];
+        const long long m = __builtin_popcountll(d.mask[0]) + __builtin_popcountll(d.mask[1]);
+        const long long nnz = d.map_off >= 0 ? (long long)(d.map_off >> 48) : 0;
+        int ncut = 0;
+        for (int q = 0; q < 4; ++q) ncut += d.cid[q] >= 0;
+        D.cut_method_bytes[c] += 8 * (m * m + (long long)ncut * e4 + 3 * m + nnz);
+      }
+  }
+
+  // dataflow plan of the level's cut sweeps (cutdf.cuh); off if a segment
+  // needs too many dependencies or the segments do not fit co-resident
+  void build_df(LevelData& D, int ncp) {
+    std::vector<CutDesc> hd(ncp);
+    CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
+    std::vector<double> hg(D.n_gmap);
+    CF_CUDA(cudaMemcpy(hg.data(), D.gmap, sizeof(double) * D.n_gmap, cudaMemcpyDeviceToHost));
+    int dev = 0, nsm = 0, per = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // the most CTAs per SM (smaller segments, more parallel work per step)
+    // whose segments all fit co-resident; df_budget > 0 fixes the budget
+    host::DfPlan pl;
+    bool ok = false;
+    for (int k = 4; k >= 1 && !ok; --k) {
+      const size_t budget = df_budget > 0 ? (size_t)df_budget : (size_t)((228 - k) * 1024 / k - 1024);
+      if (!host::df_build(hd, D.cutp_off, hg, D.a, budget, df_tile, pl)) {
+        if (verbose) std::fprintf(stderr, "[cutfem] n=%d: dataflow cut sweep off (dependencies)\n", D.a.n);
+        return;
+      }
+      // the attribute is per function and device: keep the largest any level needs
+      df_smem_max = std::max(df_smem_max, pl.smem);
+      CF_CUDA(cudaFuncSetAttribute(k_cut_df<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)df_smem_max));
+      CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cut_df<256>, 256, pl.smem));
+      ok = (long long)per * nsm >= pl.nseg;
+      if (df_budget > 0) break;
+    }
+    if (!ok) {
+      if (verbose)
+        std::fprintf(stderr, "[cutfem] n=%d: dataflow cut sweep off (%d segments > %d co-resident)\n", D.a.n, pl.nseg,
+                     per * nsm);
+      return;
+    }
+    D.df_blob = alloc<unsigned char>((int64_t)pl.blob.size());
+    D.df_seg_off = alloc<long long>(pl.nseg + 1);
+    D.df_dep_off = alloc<int>(pl.nseg + 1);
+    D.df_deps = alloc<int>(std::max<int64_t>(1, (int64_t)pl.deps.size()));
+    D.df_flags = alloc<unsigned>((int64_t)pl.nseg * DF_FLAG_STRIDE);
+    CF_CUDA(cudaMemcpy(D.df_blob, pl.blob.data(), pl.blob.size(), cudaMemcpyHostToDevice));
+    CF_CUDA(cudaMemcpy(D.df_seg_off, pl.seg_off.data(), sizeof(long long) * (pl.nseg + 1), cudaMemcpyHostToDevice));
+    CF_CUDA(cudaMemcpy(D.df_dep_off, pl.dep_off.data(), sizeof(int) * (pl.nseg + 1), cudaMemcpyHostToDevice));
+    if (!pl.deps.empty())
+      CF_CUDA(cudaMemcpy(D.df_deps, pl.deps.data(), sizeof(int) * pl.deps.size(), cudaMemcpyHostToDevice));
+    CF_CUDA(cudaMemset(D.df_flags, 0, sizeof(unsigned) * pl.nseg * DF_FLAG_STRIDE));
+    D.df_nseg = pl.nseg;
+    D.df_smem = pl.smem;
+    D.df_max_dep = pl.max_dep;
+    D.df_map_bytes = pl.map_bytes;
+    if (verbose)
+      std::fprintf(stderr, "[cutfem] n=%d: dataflow cut sweep, %d segments (<= %d co-resident), smem %zu B, "
+                           "max %d deps, blob %zu B\n", D.a.n, pl.nseg, per * nsm, pl.smem, pl.max_dep, pl.blob.size());
+  }
+
+  // the n_c x 4 cut steps of a smoothing step in one dataflow launch
+  void cut_sweeps_df(int l, double* x, const double* b, int reverse) {
+    LevelData& D = lv[l];
+    DfArgs A;
+    A.blob = D.df_blob;
+    A.seg_off = D.df_seg_off;
+    A.dep_off = D.df_dep_off;
+    A.deps = D.df_deps;
+    A.flags = D.df_flags;
+    A.x = x;
+    A.xs = D.xs;
+    A.b = b;
+    A.S = 4 * prm.n_c;
+    A.reverse = reverse;
+    A.trace = nullptr;
+    A.spin_ns = (unsigned)df_spin_ns;
+    static const bool trace = std::getenv("CUTFEM_DF_TRACE") != nullptr;
+    if (trace) A.trace = alloc<unsigned long long>((int64_t)D.df_nseg * 64);
+    launch_ex(df_coop, k_cut_df<256>, dim3(D.df_nseg), dim3(256), D.df_smem, A);
+    CF_LAUNCHED();
+    if (trace) {   // debug: per-phase times (us) of the launch, max over segments
+      std::vector<unsigned long long> t((size_t)D.df_nseg * 64);
+      CF_CUDA(cudaMemcpy(t.data(), A.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long t0 = ~0ull;
+      for (int g = 0; g < D.df_nseg; ++g) t0 = std::min(t0, t[(size_t)g * 64]);
+      std::fprintf(stderr, "[df] n=%d nseg=%d:", D.a.n, D.df_nseg);
+      for (int k = 0; k < 4 + 4 * A.S; ++k) {
+        unsigned long long mx = 0;
+        for (int g = 0; g < D.df_nseg; ++g) mx = std::max(mx, t[(size_t)g * 64 + k] - t0);
+        std::fprintf(stderr, " %.2f", mx * 1e-3);
+      }
+      std::fprintf(stderr, "\n");
     }
   }
 
@@ -1606,6 +1733,10 @@ struct Problem {
   }
 
   void cut_sweeps(int l, double* x, const double* b, int reverse) {
+    if (use_df && lv[l].df_nseg > 0 && !lv[l].part) {
+      cut_sweeps_df(l, x, b, reverse);
+      return;
+    }
     if (cut_grid7 && cut_gbar && !lv[l].part && lv[l].gmap && cut_map && prm.cut_mode == 0 && cta_cut &&
         prm.p <= 3 && (prm.n_c * 4) % 2 == 0) {
       int npmax = 0;
