@@ -9,7 +9,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #define CF_MAXP 4
@@ -142,16 +145,6 @@ struct LevelData {
   int64_t cut_bytes[8] = {};         // algorithmic bytes of one cut colour step (k_cut_step7) per colour
   void* desc = nullptr;              // CutDesc per cut patch (smoother2.cuh)
   double* xs = nullptr;              // shadow lattice vector for the ping-pong cut steps
-  // dataflow cut sweep (cutdf.cuh): segment blobs, dependencies, step flags
-  int df_nseg = 0;
-  size_t df_smem = 0;
-  unsigned char* df_blob = nullptr;
-  long long* df_seg_off = nullptr;
-  int* df_dep_off = nullptr;
-  int* df_deps = nullptr;
-  unsigned* df_flags = nullptr;
-  int df_max_dep = 0;
-  long long df_map_bytes = 0;        // G_j bytes of one launch (read once, applied n_c times)
   long long cut_method_bytes[8] = {};  // method bytes of one cut colour step per colour
   int32_t* copy_lists = nullptr;     // node lists: [prev][cur] = N_prev \ N_cur (prev = 4: read band)
   int copy_off[5][4] = {};           // offsets into copy_lists
@@ -220,5 +213,38 @@ inline void require(bool ok, int code, const std::string& msg) {
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Function attributes, occupancy, __constant__ tables and device-side tables
+// belong to a device: host-side caches of them are keyed by (call site, current
+// device) and filled under a mutex (the LocalComm ranks are host threads).
+inline std::mutex& dev_cache_mutex() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<std::pair<const void*, int>, int64_t>& dev_cache_map() {
+  static std::map<std::pair<const void*, int>, int64_t> m;
+  return m;
+}
+// value of compute() for (key, current device), computed once
+template <class F>
+int64_t dev_cached(const void* key, F&& compute) {
+  int dev = 0;
+  CF_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(dev_cache_mutex());
+  auto& m = dev_cache_map();
+  auto it = m.find({key, dev});
+  if (it != m.end()) return it->second;
+  const int64_t v = (int64_t)compute();
+  m[{key, dev}] = v;
+  return v;
+}
+// run fn() once per (key, current device)
+template <class F>
+void dev_once(const void* key, F&& fn) {
+  dev_cached(key, [&] {
+    fn();
+    return 1;
+  });
+}
 
 }  // namespace cf

@@ -22,8 +22,6 @@
 #include "dim3.cuh"
 #include "tables.cuh"
 #include "comm.cuh"
-#include "vcycle_cluster.cuh"
-#include "cutdf.cuh"
 
 namespace cf {
 
@@ -66,59 +64,21 @@ struct Problem {
   cudaStream_t cap_st = nullptr;
   bool built = false;
   bool broken = false;      // a partition failed half-way (capi refuses further hot-path calls)
-  bool persistent = false;  // one cooperative launch per smoothing step (env CUTFEM_PERSISTENT=1)
   bool fused = true;        // fused Cartesian colours (env CUTFEM_FUSED=0 disables)
-  int persistent_below = 0; // levels with n <= this use the cooperative one-launch smoothing step (env)
   bool use_mma = true;      // Cartesian patch map on fp64 tensor cores (env CUTFEM_MMA=0 disables)
   bool pingpong = true;     // cut steps without a scatter kernel (env CUTFEM_PINGPONG=0 disables)
   bool use_tma = true;      // TMA tile loads in the fused Cartesian sweep (env CUTFEM_TMA=0 disables)
   bool cta_cut = true;      // CTA of 64 threads per cut patch (env CUTFEM_CTACUT=0: one warp per patch)
-  // cut sweeps in one cluster launch when every colour has <= cluster_max cut
-  // patches (env CUTFEM_CLUSTER_MAX).  Off by default: measured no faster than
-  // one PDL launch per colour (the per-patch latency chain dominates either way)
-  int cluster_max = 0;
-  int cluster_size = 16;    // CTAs per cluster (non-portable 16; falls back to 8)
-  int cut2_v = 6;           // 2D CTA-per-patch cut step version (env CUTFEM_CUT2=4: six-barrier v4)
   int cut3_v = 3;           // 3D cut-patch kernel version (env CUTFEM_CUT3=2: lane-parallel jump array)
   bool tile_apply = true;   // TMA-tiled operator (env CUTFEM_TILEAPPLY=0: node-centric global gather)
   bool cart_split = false;  // force the two-launch Cartesian sweep through xs (env CUTFEM_CART_SPLIT=1)
   bool wide_halo = true;    // partition: wide-halo cut sweeps where the slabs are thick enough (env CUTFEM_WIDE_HALO=0)
   bool cut_map = true;      // cut steps through the precomputed dense patch maps, p <= 3 (env CUTFEM_CUTMAP=0)
-  // V-cycle levels with n <= this run in one cluster launch (env
-  // CUTFEM_VC_MAX_N; 0 = off).  Off by default: measured 1014 us (n <= 64) and
-  // 903 us (n <= 32) per config1 V-cycle vs 722 us with one PDL launch per
-  // step -- the cluster phases expose the dependent loads of the patch maps
-  // that the launch path issues before griddepcontrol.wait
-  int vc_max_n = 0;
-  int vc_cluster = 16;      // CTAs of that cluster (non-portable 16; falls back to 8)
-  // all cut sweeps of a smoothing step in one cooperative launch with grid
-  // barriers (env CUTFEM_CUT_GRID=1).  Off: measured 57.5 us vs 43.2 us for
-  // one PDL launch per step at config1 (a grid barrier costs more than a
-  // programmatic launch boundary)
-  bool cut_grid = false;
-  int cut_grid_min_n = 0;   // ... on levels with n >= this (env CUTFEM_CUT_GRID_MIN_N)
   int tc_big_n = 512;       // levels with n >= this use 32-cell fused tiles for p = 2 (env CUTFEM_TC32_MIN_N)
-  // levels whose colours have <= this many cut patches: cut sweeps in one
-  // cluster launch with the patch maps (env CUTFEM_CLUSTER7_MAX).  Off:
-  // measured slower than PDL launches (V-cycle 727 us with <= 64, 1030 us
-  // with <= 400, vs 679 us)
-  int cluster7_max = 0;
-  bool cut_grid7 = false;   // cut sweeps of large levels in one cooperative launch (env CUTFEM_CUT_GRID7;
-                            // measured slower: 48.2 vs 27.6 us per config1 sweep set, the grid barrier costs more than a PDL launch gap)
-  int cut_grid7_min_np = 256;  // ... when a colour has at least this many cut patches (CUTFEM_CUT_GRID7_MIN_NP)
-  unsigned long long* cut_gbar = nullptr;  // grid-barrier counters of k_cut_sweeps_grid7, one per level
   int tc_small_n = 128;     // Q2 levels with 16 <= n <= this use 8 x 8-cell fused tiles (env CUTFEM_TC8_MAX_N; V-cycle 658 -> 640 us)
   int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
-  // all cut steps of a smoothing step in one dataflow launch (cutdf.cuh) on
-  // unpartitioned levels (env CUTFEM_DF=0: one PDL launch per step)
-  bool use_df = true;
-  int df_budget = 0;            // shared-memory bytes per segment (env CUTFEM_DF_BUDGET; 0 = most CTAs per SM that fit)
-  int df_tile = 4;              // Morton tile of the segment packing, in vertices (env CUTFEM_DF_TILE)
-  size_t df_smem_max = 0;       // largest dynamic shared memory of any level's k_cut_df launch
-  int df_spin_ns = 0;           // __nanosleep back-off of the flag polls (env CUTFEM_DF_SPIN)
-  bool df_coop = false;         // cooperative launch attribute on k_cut_df (env CUTFEM_DF_COOP=1)
   // slab partition: comm != nullptr after partition()
   Comm* comm = nullptr;
   static constexpr int HALO = 4;   // halo width in cells (the fused Cartesian apron)
@@ -247,29 +207,9 @@ struct Problem {
     return per * nsm;
   }
 
-  // launch as one thread-block cluster of `cs` CTAs (grid = cs), with PDL
-  template <typename... KArgs, typename... Args>
-  cudaError_t launch_cluster(void (*kern)(KArgs...), int cs, dim3 b, size_t smem, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = b;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
-  }
 
   // ---------------------------------------------------------------- setup
   void setup_mesh() {
-    if (const char* e = std::getenv("CUTFEM_PERSISTENT")) persistent = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_FUSED")) fused = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_PDL")) pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_MMA")) use_mma = std::atoi(e) != 0;
@@ -277,33 +217,16 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_TMA")) use_tma = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CTACUT")) cta_cut = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUT3")) cut3_v = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_CUT2")) cut2_v = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_CLUSTER_MAX")) cluster_max = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_PERSISTENT_BELOW")) persistent_below = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY")) tile_apply = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CART_SPLIT")) cart_split = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_WIDE_HALO")) wide_halo = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUTMAP")) cut_map = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CUTFEM_VC_MAX_N")) vc_max_n = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_CUT_GRID")) cut_grid = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CUTFEM_CUT_GRID_MIN_N")) cut_grid_min_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TC8_MAX_N")) tc_small_n = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_CLUSTER7_MAX")) cluster7_max = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_CUT_GRID7")) cut_grid7 = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CUTFEM_CUT_GRID7_MIN_NP")) cut_grid7_min_np = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_DF")) use_df = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CUTFEM_DF_BUDGET")) df_budget = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_DF_TILE")) df_tile = std::atoi(e);
-    if (const char* e = std::getenv("CUTFEM_DF_COOP")) df_coop = std::atoi(e) != 0;
-    if (const char* e = std::getenv("CUTFEM_DF_SPIN")) df_spin_ns = std::atoi(e);
-    require(df_tile >= 1, ERR_ARG, "CUTFEM_DF_TILE must be >= 1");
     require(tcx_big == 16 || tcx_big == 24 || tcx_big == 32, ERR_ARG, "CUTFEM_TCX must be 16, 24 or 32");
-    cut_gbar = alloc<unsigned long long>(std::max(1, prm.n_levels));
-    CF_CUDA(cudaMemset(cut_gbar, 0, sizeof(unsigned long long) * std::max(1, prm.n_levels)));
     if (prm.dim == 3) {
       setup_mesh3();
       return;
@@ -612,7 +535,6 @@ struct Problem {
       for (int c = 0; c < 5; ++c) D.act_off[c] = D.cutp_off[c];
       build_copy_lists(D, D.ent_node, D.ent_col_off, (const CutDesc*)D.desc, ncp);
       if (ncp) method_bytes(D, ncp);
-      if (ncp && D.gmap && use_df && cta_cut && (prm.n_c * 4) % 2 == 0) build_df(D, ncp);
       sync();
     }
     build_coarse();
@@ -629,7 +551,6 @@ struct Problem {
     for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
     sync();
     built = true;
-    if (prm.dim == 2) prepare_vc();
   }
 
   // ping-pong copy lists (see k_cut_step): [prev][cur] = N_prev \ N_cur for
@@ -714,93 +635,7 @@ struct Problem {
       }
   }
 
-  // dataflow plan of the level's cut sweeps (cutdf.cuh); off if a segment
-  // needs too many dependencies or the segments do not fit co-resident
-  void build_df(LevelData& D, int ncp) {
-    std::vector<CutDesc> hd(ncp);
-    CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
-    std::vector<double> hg(D.n_gmap);
-    CF_CUDA(cudaMemcpy(hg.data(), D.gmap, sizeof(double) * D.n_gmap, cudaMemcpyDeviceToHost));
-    int dev = 0, nsm = 0, per = 0;
-    CF_CUDA(cudaGetDevice(&dev));
-    CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    // the most CTAs per SM (smaller segments, more parallel work per step)
-    // whose segments all fit co-resident; df_budget > 0 fixes the budget
-    host::DfPlan pl;
-    bool ok = false;
-    for (int k = 4; k >= 1 && !ok; --k) {
-      const size_t budget = df_budget > 0 ? (size_t)df_budget : (size_t)((228 - k) * 1024 / k - 1024);
-      if (!host::df_build(hd, D.cutp_off, hg, D.a, budget, df_tile, pl)) {
-        if (verbose) std::fprintf(stderr, "[cutfem] n=%d: dataflow cut sweep off (dependencies)\n", D.a.n);
-        return;
-      }
-      // the attribute is per function and device: keep the largest any level needs
-      df_smem_max = std::max(df_smem_max, pl.smem);
-      CF_CUDA(cudaFuncSetAttribute(k_cut_df<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)df_smem_max));
-      CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cut_df<256>, 256, pl.smem));
-      ok = (long long)per * nsm >= pl.nseg;
-      if (df_budget > 0) break;
-    }
-    if (!ok) {
-      if (verbose)
-        std::fprintf(stderr, "[cutfem] n=%d: dataflow cut sweep off (%d segments > %d co-resident)\n", D.a.n, pl.nseg,
-                     per * nsm);
-      return;
-    }
-    D.df_blob = alloc<unsigned char>((int64_t)pl.blob.size());
-    D.df_seg_off = alloc<long long>(pl.nseg + 1);
-    D.df_dep_off = alloc<int>(pl.nseg + 1);
-    D.df_deps = alloc<int>(std::max<int64_t>(1, (int64_t)pl.deps.size()));
-    D.df_flags = alloc<unsigned>((int64_t)pl.nseg * DF_FLAG_STRIDE);
-    CF_CUDA(cudaMemcpy(D.df_blob, pl.blob.data(), pl.blob.size(), cudaMemcpyHostToDevice));
-    CF_CUDA(cudaMemcpy(D.df_seg_off, pl.seg_off.data(), sizeof(long long) * (pl.nseg + 1), cudaMemcpyHostToDevice));
-    CF_CUDA(cudaMemcpy(D.df_dep_off, pl.dep_off.data(), sizeof(int) * (pl.nseg + 1), cudaMemcpyHostToDevice));
-    if (!pl.deps.empty())
-      CF_CUDA(cudaMemcpy(D.df_deps, pl.deps.data(), sizeof(int) * pl.deps.size(), cudaMemcpyHostToDevice));
-    CF_CUDA(cudaMemset(D.df_flags, 0, sizeof(unsigned) * pl.nseg * DF_FLAG_STRIDE));
-    D.df_nseg = pl.nseg;
-    D.df_smem = pl.smem;
-    D.df_max_dep = pl.max_dep;
-    D.df_map_bytes = pl.map_bytes;
-    if (verbose)
-      std::fprintf(stderr, "[cutfem] n=%d: dataflow cut sweep, %d segments (<= %d co-resident), smem %zu B, "
-                           "max %d deps, blob %zu B\n", D.a.n, pl.nseg, per * nsm, pl.smem, pl.max_dep, pl.blob.size());
-  }
 
-  // the n_c x 4 cut steps of a smoothing step in one dataflow launch
-  void cut_sweeps_df(int l, double* x, const double* b, int reverse) {
-    LevelData& D = lv[l];
-    DfArgs A;
-    A.blob = D.df_blob;
-    A.seg_off = D.df_seg_off;
-    A.dep_off = D.df_dep_off;
-    A.deps = D.df_deps;
-    A.flags = D.df_flags;
-    A.x = x;
-    A.xs = D.xs;
-    A.b = b;
-    A.S = 4 * prm.n_c;
-    A.reverse = reverse;
-    A.trace = nullptr;
-    A.spin_ns = (unsigned)df_spin_ns;
-    static const bool trace = std::getenv("CUTFEM_DF_TRACE") != nullptr;
-    if (trace) A.trace = alloc<unsigned long long>((int64_t)D.df_nseg * 64);
-    launch_ex(df_coop, k_cut_df<256>, dim3(D.df_nseg), dim3(256), D.df_smem, A);
-    CF_LAUNCHED();
-    if (trace) {   // debug: per-phase times (us) of the launch, max over segments
-      std::vector<unsigned long long> t((size_t)D.df_nseg * 64);
-      CF_CUDA(cudaMemcpy(t.data(), A.trace, t.size() * 8, cudaMemcpyDeviceToHost));
-      unsigned long long t0 = ~0ull;
-      for (int g = 0; g < D.df_nseg; ++g) t0 = std::min(t0, t[(size_t)g * 64]);
-      std::fprintf(stderr, "[df] n=%d nseg=%d:", D.a.n, D.df_nseg);
-      for (int k = 0; k < 4 + 4 * A.S; ++k) {
-        unsigned long long mx = 0;
-        for (int g = 0; g < D.df_nseg; ++g) mx = std::max(mx, t[(size_t)g * 64 + k] - t0);
-        std::fprintf(stderr, " %.2f", mx * 1e-3);
-      }
-      std::fprintf(stderr, "\n");
-    }
-  }
 
   // (ent_node, col_off[0..4]: the interior nodes of the swept patches per
   // colour; desc/ncp: their descriptors)
@@ -1063,27 +898,21 @@ struct Problem {
       return;
     }
     require(comm == nullptr, ERR_STATE, "the problem is already partitioned");
-    vc_built_top = -1;
     require(c->world >= 1 && c->rank >= 0 && c->rank < c->world, ERR_ARG, "bad rank / world");
     const int W = c->world, R = c->rank, p = prm.p;
     fused = true;
     pingpong = true;
-    persistent = false;
-    persistent_below = 0;
-    cluster_max = 0;
     bool finer = true;
     for (int l = prm.n_levels - 1; l >= 1; --l) {
       LevelData& D = lv[l];
       const int n = D.a.n, nl = D.a.nl, ld = D.a.ld, s = n / W, TC = D.tc;
-      // (levels the cluster V-cycle covers stay replicated: one launch, no exchanges)
-      const bool vc_level = vc_max_n > 0 && prm.cut_mode == 0 && p <= 3 && cut_map && n <= vc_max_n;
       // With the wide halo (default) only slabs thick enough for it are
       // partitioned: a thinner level would need an exchange per cut step
       // (4 n_c + 1 per smoothing step), which costs more than computing the
       // whole (small) level on every rank; CUTFEM_WIDE_HALO=0 partitions every
       // level of >= HALO + 1 rows with the narrow halo instead.
       const int S = 4 * prm.n_c, HW = 3 * S;   // wide halo: 3 cells per cut step (see build_wide)
-      const bool ok = finer && n % W == 0 && s % TC == 0 && s >= (wide_halo ? HW : HALO) + 1 && !vc_level;
+      const bool ok = finer && n % W == 0 && s % TC == 0 && s >= (wide_halo ? HW : HALO) + 1;
       finer = ok;
       if (!ok) continue;
       D.part = 1;
@@ -1114,6 +943,10 @@ struct Problem {
       };
       own_tiles(D.fused_tiles, D.n_fused_tiles);
       own_tiles(D.fused_ext, D.n_fused_ext);
+      // the in-place sweep's grid barrier releases at the next multiple of the
+      // grid size: restart its counter for the new (smaller) grid (stream-
+      // ordered after every launch issued so far)
+      if (D.gbar) CF_CUDA(cudaMemsetAsync(D.gbar, 0, sizeof(unsigned long long), st));
       // cut patches with vertex rows [c0 - 1, c1]
       const int ncp = D.cutp_off[4];
       std::vector<CutDesc> hd(ncp), kd;
@@ -1163,7 +996,6 @@ struct Problem {
       D.at1 = std::min(nt, ceil_div(D.c1 + 2, 16));
     }
     comm = c;
-    prepare_vc();
   }
 
   void build_coarse() {
@@ -1231,11 +1063,10 @@ struct Problem {
         constexpr int TX = 16;
         using S = ApplySmem<P, TX>;
         const CUtensorMap tm = host::lattice_tmap(x, L.nl, L.ld, S::RWP, S::RW);
-        static bool attr = false;
-        if (!attr) {
+        static const char attr_key = 0;   // per-device attribute (dev_once)
+        dev_once(&attr_key, [&] {
           CF_CUDA(cudaFuncSetAttribute(k_apply_tile<P, TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
-          attr = true;
-        }
+        });
         const int nt = ceil_div(L.n, TX);
         const int ty0 = D.part ? D.at0 : 0, ty1 = D.part ? D.at1 : nt;
         if (ty1 > ty0) launch(k_apply_tile<P, TX>, dim3(nt, ty1 - ty0), dim3(256), S::bytes, tm, L, b, y, ty0);
@@ -1255,11 +1086,10 @@ struct Problem {
     CF_DISPATCH(prm.p, {
       constexpr int TP = cart_tp<P>();
       const size_t smb = CartSmem<P, TP>::doubles * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
+      static const char attr_key = 0;   // per-device attribute (dev_once)
+      dev_once(&attr_key, [&] {
         CF_CUDA(cudaFuncSetAttribute(k_cart_colour_v2<P, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-        attr = true;
-      }
+      });
       k_cart_colour_v2<P, TP><<<D.n_cart_tiles[c], TP * TP * (2 * P - 1), smb, st>>>(
           D.a, D.cart_tiles + D.cart_tile_off[c], c, D.vkind, x, b);
     });
@@ -1276,12 +1106,11 @@ struct Problem {
       const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
       const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
       const size_t smb = wpb * pw;
-      static bool attr = false;
-      if (!attr) {
+      static const char attr_key = 0;   // per-device attribute (dev_once)
+      dev_once(&attr_key, [&] {
         CF_CUDA(cudaFuncSetAttribute(k_cut_colour_v3<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CF_CUDA(cudaFuncSetAttribute(k_cut_colour_v3<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-      }
+      });
       if (prm.cut_mode == 0)
         launch(k_cut_colour_v3<P, false>, dim3(ceil_div(np, wpb)), dim3(128), smb, D.a, desc, np, (const double*)D.ecut,
                (const double*)D.inv, (const double*)x, b, D.zbuf, wpb);
@@ -1297,58 +1126,6 @@ struct Problem {
     CF_LAUNCHED();
   }
 
-  // one cooperative launch for the whole smoothing step
-  void smooth_persistent(int l, double* x, const double* b, int reverse) {
-    LevelData& D = lv[l];
-    SmoothArgs A;
-    A.L = D.a;
-    A.tiles = D.cart_tiles;
-    A.desc = (const CutDesc*)D.desc;
-    for (int c = 0; c < 5; ++c) {
-      A.tile_off[c] = D.cart_tile_off[c];
-      A.cut_off[c] = D.cutp_off[c];
-      A.ent_off_c[c] = D.ent_col_off[c];
-    }
-    A.ent_node = D.ent_node;
-    A.ecut = D.ecut;
-    A.inv = D.inv;
-    A.vk = D.vkind;
-    A.zbuf = D.zbuf;
-    A.x = x;
-    A.b = b;
-    A.n_c = prm.n_c;
-    A.reverse = reverse;
-    CF_DISPATCH(prm.p, {
-      constexpr int TP = cart_tp<P>();
-      const size_t pw = CutSmem<P>::per_warp * sizeof(double);
-      A.cut_wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (110 * 1024) / pw));
-      const size_t smb = std::max<size_t>(CartSmem<P, TP>::doubles * sizeof(double), A.cut_wpb * pw);
-      void* fn = prm.cut_mode == 0 ? (void*)k_smooth_persistent<P, TP, false> : (void*)k_smooth_persistent<P, TP, true>;
-      static int max_blocks = -1;
-      if (max_blocks < 0) {
-        int nsm = 0, dev = 0, per_sm = 1 << 30;
-        CF_CUDA(cudaGetDevice(&dev));
-        CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        for (void* f : {(void*)k_smooth_persistent<P, TP, false>, (void*)k_smooth_persistent<P, TP, true>}) {
-          CF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          CF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-          int b = 0;
-          CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, 256, smb));
-          per_sm = std::min(per_sm, b);
-        }
-        max_blocks = std::max(1, per_sm * nsm);
-      }
-      int need = 1;
-      for (int c = 0; c < 4; ++c) {
-        need = std::max(need, D.n_cart_tiles[c]);
-        need = std::max(need, ceil_div(D.n_cutp[c], A.cut_wpb));
-      }
-      const int grid = std::min(need, max_blocks);
-      void* args[] = {&A};
-      CF_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), args, smb, st));
-    });
-    CF_LAUNCHED();
-  }
 
   // exchange after the Cartesian sweep: none when the wide-halo cut sweeps
   // follow (they start with their own wide exchange), else the narrow halo
@@ -1365,12 +1142,12 @@ struct Problem {
     using S = CartTmaSmem<P, TC, TCX>;
     const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);
     const CUtensorMap tmb = host::lattice_tmap(b, D.a.nl, D.a.ld, S::RWP, S::RW);
-    static int cap = -1;
-    if (cap < 0) {
+    static const char cap_key = 0;   // per-device attribute + occupancy (dev_cached)
+    const int cap = (int)dev_cached(&cap_key, [&] {
       CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT, TCX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
       CF_CUDA(cudaFuncSetAttribute(k_cart_fused_tma<P, TC, NT, TCX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-      cap = coresident(k_cart_fused_tma<P, TC, NT, TCX>, S::bytes, NT);
-    }
+      return coresident(k_cart_fused_tma<P, TC, NT, TCX>, S::bytes, NT);
+    });
     if (verbose) {
       std::fprintf(stderr, "[cutfem] level %d: %d fused tiles (%d ext), %d co-resident -> %s\n", l,
                    D.n_fused_tiles, D.n_fused_ext, cap, (!cart_split && D.n_fused_tiles <= cap) ? "in place" : "split");
@@ -1428,11 +1205,11 @@ struct Problem {
         if (use_mma) {
           const double* G = host::cart_map(P);
           const size_t smb = CartMMASmem<P, TC>::doubles * sizeof(double) + CartMMASmem<P, TC>::ints * sizeof(int);
-          static int cap = -1;
-          if (cap < 0) {
+          static const char cap_key = 0;   // per-device attribute + occupancy (dev_cached)
+          const int cap = (int)dev_cached(&cap_key, [&] {
             CF_CUDA(cudaFuncSetAttribute(k_cart_fused_mma<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-            cap = coresident(k_cart_fused_mma<P, TC>, smb);
-          }
+            return coresident(k_cart_fused_mma<P, TC>, smb);
+          });
           if (!cart_split && D.n_fused_tiles <= cap) {
             launch_ex(true, k_cart_fused_mma<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a,
                       (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, b, reverse, 1);
@@ -1449,11 +1226,11 @@ struct Problem {
         }
       }
       const size_t smb = CartFusedSmem<P, TC>::doubles * sizeof(double);
-      static int cap2 = -1;
-      if (cap2 < 0) {
+      static const char cap2_key = 0;   // per-device attribute + occupancy (dev_cached)
+      const int cap2 = (int)dev_cached(&cap2_key, [&] {
         CF_CUDA(cudaFuncSetAttribute(k_cart_fused<P, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-        cap2 = coresident(k_cart_fused<P, TC>, smb);
-      }
+        return coresident(k_cart_fused<P, TC>, smb);
+      });
       if (!cart_split && D.n_fused_tiles <= cap2) {
         launch_ex(true, k_cart_fused<P, TC>, dim3(D.n_fused_tiles), dim3(256), smb, D.a, (const int*)D.fused_tiles,
                   (const uint8_t*)D.vkind, x, b, reverse, 1);
@@ -1491,11 +1268,10 @@ struct Problem {
 #endif
           constexpr int NT = P <= 2 ? CF_CUT7_NT : 128;
           const size_t smb = CutMapSmem<P>::bytes;
-          static bool attr7 = false;
-          if (!attr7) {
+          static const char attr7_key = 0;   // per-device attribute (dev_once)
+          dev_once(&attr7_key, [&] {
             CF_CUDA(cudaFuncSetAttribute(k_cut_step7<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-            attr7 = true;
-          }
+          });
           launch(k_cut_step7<P, NT>, dim3(np + ceil_div(ncopy, NT)), dim3(NT), smb, D.a, desc, np,
                  (const double*)D.gmap, R, W, b, cl, ncopy);
           CF_LAUNCHED();
@@ -1506,42 +1282,22 @@ struct Problem {
     CF_DISPATCH(prm.p, {
       if (prm.cut_mode == 0 && cta_cut) {
         constexpr int NT = 64;
-        const size_t smb = CutSmem4<P>::doubles * sizeof(double);
-        static bool attr4 = false;
-        if (!attr4) {
-          CF_CUDA(cudaFuncSetAttribute(k_cut_step4<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          attr4 = true;
-        }
         const int cb = ceil_div(ncopy, NT);
-        static bool attr5 = false;
-        if (!attr5) {
-          CF_CUDA(cudaFuncSetAttribute(k_cut_step5<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          attr5 = true;
-        }
-        if (cut2_v >= 6) {
-          static bool attr6 = false;
-          if (!attr6) {
-            CF_CUDA(cudaFuncSetAttribute(k_cut_step6<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr6 = true;
-          }
-          launch(k_cut_step6<P, NT>, dim3(np + cb), dim3(NT), (size_t)CutGroup6<P>::bytes, D.a, desc, np,
-                 (const double*)D.ecut, (const double*)D.inv, R, W, b, cl, ncopy);
-        } else if (cut2_v >= 5)
-          launch(k_cut_step5<P, NT>, dim3(np + cb), dim3(NT), smb, D.a, desc, np, np, (const double*)D.ecut,
-                 (const double*)D.inv, R, W, b, cl, ncopy);
-        else
-          launch(k_cut_step4<P, NT>, dim3(np + cb), dim3(NT), smb, D.a, desc, np, np, (const double*)D.ecut,
-                 (const double*)D.inv, R, W, b, cl, ncopy);
+        static const char attr6_key = 0;   // per-device attribute (dev_once)
+        dev_once(&attr6_key, [&] {
+          CF_CUDA(cudaFuncSetAttribute(k_cut_step6<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        });
+        launch(k_cut_step6<P, NT>, dim3(np + cb), dim3(NT), (size_t)CutGroup6<P>::bytes, D.a, desc, np,
+               (const double*)D.ecut, (const double*)D.inv, R, W, b, cl, ncopy);
       } else {
         const size_t pw = CutSmem3<P>::per_warp * sizeof(double);
         const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (96 * 1024) / pw));
         const size_t smb = wpb * pw;
-        static bool attr = false;
-        if (!attr) {
+        static const char attr_key = 0;   // per-device attribute (dev_once)
+        dev_once(&attr_key, [&] {
           CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
           CF_CUDA(cudaFuncSetAttribute(k_cut_step<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          attr = true;
-        }
+        });
         const int pb = ceil_div(np, wpb), cb = ceil_div(ncopy, 128);
         if (prm.cut_mode == 0)
           launch(k_cut_step<P, false>, dim3(pb + cb), dim3(128), smb, D.a, desc, np, wpb, pb, (const double*)D.ecut,
@@ -1554,215 +1310,11 @@ struct Problem {
     CF_LAUNCHED();
   }
 
-  // the n_c sweeps over the cut colours with ping-pong buffers (x, xs); an
-  // even number of steps (4 n_c) leaves the result in x
-  // all cut sweeps of a smoothing step in one cluster-resident launch
-  // (levels whose colours have at most cluster_max cut patches)
-  bool cut_sweeps_cluster(int l, double* x, const double* b, int reverse) {
-    LevelData& D = lv[l];
-    CutSweepArgs A;
-    A.L = D.a;
-    A.desc = (const CutDesc*)D.desc;
-    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.cutp_off[c];
-    A.copy = D.copy_lists;
-    for (int i = 0; i < 5; ++i)
-      for (int c = 0; c < 4; ++c) {
-        A.copy_off[i][c] = D.copy_off[i][c];
-        A.copy_n[i][c] = D.copy_n[i][c];
-      }
-    A.ecut = D.ecut;
-    A.inv = D.inv;
-    A.x = x;
-    A.xs = D.xs;
-    A.b = b;
-    A.n_c = prm.n_c;
-    A.reverse = reverse;
-    bool ok = false;
-    CF_DISPATCH(prm.p, {
-      constexpr int G = P <= 2 ? 8 : (P == 3 ? 4 : 2);
-      const size_t smb = (size_t)G * ((CutGroup6<P>::bytes + 127) & ~127);
-      static int cs_ok = 0;
-      if (!cs_ok) {
-        CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-        CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster<P, G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        cs_ok = 1;
-      }
-      cudaError_t e = launch_cluster(k_cut_sweeps_cluster<P, G>, cluster_size, dim3(64 * G), smb, A);
-      if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        require(cluster_size > 8, ERR_CUDA, "cluster launch of the cut sweeps failed");
-        cluster_size = 8;
-        CF_CUDA(launch_cluster(k_cut_sweeps_cluster<P, G>, cluster_size, dim3(64 * G), smb, A));
-      }
-      ok = true;
-    });
-    CF_LAUNCHED();
-    return ok;
-  }
 
-  // all cut sweeps of a small level in one cluster launch with the patch maps
-  void cut_sweeps_cluster7(int l, double* x, const double* b, int reverse) {
-    LevelData& D = lv[l];
-    CutSweepArgs A;
-    std::memset(&A, 0, sizeof(A));
-    A.L = D.a;
-    A.desc = (const CutDesc*)D.act_desc;
-    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.act_off[c];
-    A.copy = D.copy_lists;
-    for (int i = 0; i < 5; ++i)
-      for (int c = 0; c < 4; ++c) {
-        A.copy_off[i][c] = D.copy_off[i][c];
-        A.copy_n[i][c] = D.copy_n[i][c];
-      }
-    A.x = x;
-    A.xs = D.xs;
-    A.b = b;
-    A.n_c = prm.n_c;
-    A.reverse = reverse;
-    A.gmap = D.gmap;
-    CF_DISPATCH(prm.p, {
-      if constexpr (P <= 3) {
-        constexpr int G = P <= 2 ? 4 : 2;
-        const size_t smb = (size_t)G * ((CutMapSmem<P>::bytes + 127) & ~(size_t)127);
-        static bool attr = false;
-        if (!attr) {
-          CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster7<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-          CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_cluster7<P, G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-          attr = true;
-        }
-        cudaError_t e = launch_cluster(k_cut_sweeps_cluster7<P, G>, cluster_size, dim3(64 * G), smb, A);
-        if (e != cudaSuccess) {
-          (void)cudaGetLastError();
-          require(cluster_size > 8, ERR_CUDA, "cluster launch of the cut sweeps failed");
-          cluster_size = 8;
-          CF_CUDA(launch_cluster(k_cut_sweeps_cluster7<P, G>, cluster_size, dim3(64 * G), smb, A));
-        }
-        CF_LAUNCHED();
-      }
-    });
-  }
 
-  // all cut sweeps of a smoothing step in one cooperative launch over the GPU
-  bool cut_sweeps_grid(int l, double* x, const double* b, int reverse) {
-    LevelData& D = lv[l];
-    CutSweepArgs A;
-    A.L = D.a;
-    A.desc = (const CutDesc*)D.act_desc;
-    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.act_off[c];
-    A.copy = D.copy_lists;
-    for (int i = 0; i < 5; ++i)
-      for (int c = 0; c < 4; ++c) {
-        A.copy_off[i][c] = D.copy_off[i][c];
-        A.copy_n[i][c] = D.copy_n[i][c];
-      }
-    A.ecut = D.ecut;
-    A.inv = D.inv;
-    A.x = x;
-    A.xs = D.xs;
-    A.b = b;
-    A.n_c = prm.n_c;
-    A.reverse = reverse;
-    CF_DISPATCH(prm.p, {
-      constexpr int G = P <= 2 ? 8 : (P == 3 ? 4 : 2);
-      const size_t smb = (size_t)G * ((CutGroup6<P>::bytes + 127) & ~127);
-      static int cap = -1;
-      if (cap < 0) {
-        CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_grid<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-        int nsm = 0, dev = 0, per = 0;
-        CF_CUDA(cudaGetDevice(&dev));
-        CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cut_sweeps_grid<P, G>, 64 * G, smb));
-        cap = per * nsm;
-      }
-      int npmax = 1;
-      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, D.act_off[c + 1] - D.act_off[c]);
-      const int grid = std::max(1, std::min(cap, ceil_div(npmax, G)));
-      launch_ex(true, k_cut_sweeps_grid<P, G>, dim3(grid), dim3(64 * G), smb, A);
-      CF_LAUNCHED();
-    });
-    return true;
-  }
 
-  // all cut sweeps of a large level in one cooperative launch with the patch
-  // maps (k_cut_sweeps_grid7); false if the grid does not fit co-resident
-  bool cut_sweeps_grid7(int l, double* x, const double* b, int reverse, int npmax) {
-    LevelData& D = lv[l];
-    CutSweepArgs A;
-    std::memset(&A, 0, sizeof(A));
-    A.L = D.a;
-    A.desc = (const CutDesc*)D.act_desc;
-    for (int c = 0; c < 5; ++c) A.cut_off[c] = D.act_off[c];
-    A.copy = D.copy_lists;
-    for (int i = 0; i < 5; ++i)
-      for (int c = 0; c < 4; ++c) {
-        A.copy_off[i][c] = D.copy_off[i][c];
-        A.copy_n[i][c] = D.copy_n[i][c];
-      }
-    A.x = x;
-    A.xs = D.xs;
-    A.b = b;
-    A.n_c = prm.n_c;
-    A.reverse = reverse;
-    A.gmap = D.gmap;
-    bool ok = false;
-    CF_DISPATCH(prm.p, {
-      if constexpr (P <= 3) {
-#ifndef CF_GRID7_G
-#define CF_GRID7_G 1     // patches per CTA of k_cut_sweeps_grid7
-#endif
-        constexpr int G = CF_GRID7_G, NTG = 128;
-        const size_t smb = (size_t)G * ((CutMapSmem<P>::bytes + 127) & ~(size_t)127);
-        static int cap = -1;
-        if (cap < 0) {
-          CF_CUDA(cudaFuncSetAttribute(k_cut_sweeps_grid7<P, G, NTG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
-          int nsm = 0, dev = 0, per = 0;
-          CF_CUDA(cudaGetDevice(&dev));
-          CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-          CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cut_sweeps_grid7<P, G, NTG>, NTG * G, smb));
-          cap = per * nsm;
-        }
-        const int grid = std::min(cap, ceil_div(npmax, G));
-        if (grid > 0) {
-          launch_ex(true, k_cut_sweeps_grid7<P, G, NTG>, dim3(grid), dim3(NTG * G), smb, A, cut_gbar + l);
-          CF_LAUNCHED();
-          ok = true;
-        }
-      }
-    });
-    return ok;
-  }
 
   void cut_sweeps(int l, double* x, const double* b, int reverse) {
-    if (use_df && lv[l].df_nseg > 0 && !lv[l].part) {
-      cut_sweeps_df(l, x, b, reverse);
-      return;
-    }
-    if (cut_grid7 && cut_gbar && !lv[l].part && lv[l].gmap && cut_map && prm.cut_mode == 0 && cta_cut &&
-        prm.p <= 3 && (prm.n_c * 4) % 2 == 0) {
-      int npmax = 0;
-      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].act_off[c + 1] - lv[l].act_off[c]);
-      if (npmax >= cut_grid7_min_np && (cluster7_max <= 0 || npmax > cluster7_max) &&
-          cut_sweeps_grid7(l, x, b, reverse, npmax))
-        return;
-    }
-    if (cluster7_max > 0 && !lv[l].part && lv[l].gmap && cut_map && prm.cut_mode == 0 && cta_cut && prm.p <= 3) {
-      int npmax = 0;
-      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].act_off[c + 1] - lv[l].act_off[c]);
-      if (npmax <= cluster7_max) {
-        cut_sweeps_cluster7(l, x, b, reverse);
-        return;
-      }
-    }
-    if (cut_grid && !lv[l].part && prm.cut_mode == 0 && cta_cut && (prm.n_c * 4) % 2 == 0 &&
-        lv[l].a.n >= cut_grid_min_n) {
-      cut_sweeps_grid(l, x, b, reverse);
-      return;
-    }
-    if (cluster_max > 0 && prm.cut_mode == 0 && cta_cut && (prm.n_c * 4) % 2 == 0) {
-      int npmax = 0;
-      for (int c = 0; c < 4; ++c) npmax = std::max(npmax, lv[l].n_cutp[c]);
-      if (npmax <= cluster_max && cut_sweeps_cluster(l, x, b, reverse)) return;
-    }
     double* bufs[2] = {x, lv[l].xs};
     LevelData& D = lv[l];
     if (comm && D.wide) {
@@ -1807,18 +1359,10 @@ struct Problem {
       if (reverse) cart_fused(l, x, b, 1);
       return;
     }
-    if (persistent_below > 0 && lv[l].a.n <= persistent_below) {
-      smooth_persistent(l, x, b, reverse);
-      return;
-    }
     if (pingpong && fused) {
       if (!reverse) cart_fused(l, x, b, 0);
       cut_sweeps(l, x, b, reverse);
       if (reverse) cart_fused(l, x, b, 1);
-      return;
-    }
-    if (persistent) {
-      smooth_persistent(l, x, b, reverse);
       return;
     }
     if (fused) {
@@ -1878,95 +1422,11 @@ struct Problem {
     CF_LAUNCHED();
   }
 
-  // coarse end of the V-cycle in one cluster launch (vcycle_cluster.cuh):
-  // the highest level it covers (0 = not used)
-  int vc_top() {
-    if (vc_max_n <= 0 || prm.dim != 2 || prm.cut_mode != 0 || prm.p > 3 || !cut_map) return 0;
-    int top = 0;
-    for (int l = 1; l < prm.n_levels; ++l) {
-      const LevelData& D = lv[l];
-      if (D.a.n > vc_max_n || D.part || (D.act_off[4] > 0 && !D.gmap)) break;
-      top = l;
-    }
-    return top;
-  }
-  CoarseLevel* vc_levels = nullptr;
-  int vc_built_top = -1;
-  // per-level arguments of the cluster V-cycle (built outside any graph capture:
-  // at the end of build_patches and of partition)
-  void prepare_vc() {
-    const int top = vc_top();
-    if (top > 0) {
-      std::vector<CoarseLevel> h(top + 1);
-      for (int l = 0; l <= top; ++l) {
-        const LevelData& D = lv[l];
-        CoarseLevel& V = h[l];
-        std::memset(&V, 0, sizeof(V));
-        V.L = D.a;
-        V.cart_list = D.cart_list;
-        for (int c = 0; c < 5; ++c) {
-          V.cart_off[c] = D.cart_off[c];
-          V.cut_off[c] = D.act_off[c];
-        }
-        V.desc = (const CutDesc*)D.act_desc;
-        V.gmap = D.gmap;
-        V.copy = D.copy_lists;
-        for (int i = 0; i < 5; ++i)
-          for (int c = 0; c < 4; ++c) {
-            V.copy_off[i][c] = D.copy_off[i][c];
-            V.copy_n[i][c] = D.copy_n[i][c];
-          }
-        V.x = D.x;
-        V.b = D.b;
-        V.r = D.r;
-        V.xs = D.xs;
-      }
-      if (!vc_levels) vc_levels = alloc<CoarseLevel>(VC_MAXL);
-      require(top < VC_MAXL, ERR_SIZE, "too many cluster V-cycle levels");
-      CF_CUDA(cudaMemcpy(vc_levels, h.data(), sizeof(CoarseLevel) * (top + 1), cudaMemcpyHostToDevice));
-    }
-    vc_built_top = top;
-  }
-  void vcycle_cluster(int top, double* x, const double* b) {
-    require(vc_built_top == top, ERR_STATE, "cluster V-cycle arguments not prepared");
-    CoarseArgs A;
-    A.lv = vc_levels;
-    A.lmax = top;
-    A.n_c = prm.n_c;
-    A.symmetric = prm.symmetric;
-    A.Gc = host::cart_map(prm.p);
-    A.c_inv = c_inv;
-    A.c_nodes = c_nodes;
-    A.n0 = n0;
-    A.x = x;
-    A.b = b;
-    CF_DISPATCH(prm.p, {
-      if constexpr (P <= 3) {
-        static bool attr = false;
-        if (!attr) {
-          CF_CUDA(cudaFuncSetAttribute(k_vcycle_cluster<P>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-          attr = true;
-        }
-        cudaError_t e = launch_cluster(k_vcycle_cluster<P>, vc_cluster, dim3(256), 0, A);
-        if (e != cudaSuccess) {
-          (void)cudaGetLastError();
-          require(vc_cluster > 8, ERR_CUDA, "cluster launch of the coarse V-cycle failed");
-          vc_cluster = 8;
-          CF_CUDA(launch_cluster(k_vcycle_cluster<P>, vc_cluster, dim3(256), 0, A));
-        }
-        CF_LAUNCHED();
-      }
-    });
-  }
 
   // V-cycle on level l with initial guess x (P l.124, l.217)
   void vcycle(int l, double* x, const double* b) {
     if (l == 0) {
       coarse_solve(b, x);
-      return;
-    }
-    if (const int top = vc_top(); top > 0 && l == top) {
-      vcycle_cluster(top, x, b);
       return;
     }
     LevelData& D = lv[l];
@@ -2303,7 +1763,6 @@ struct Problem {
     for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
     sync();
     built = true;
-    if (prm.dim == 2) prepare_vc();
   }
 
   void apply3(int l, const double* x, double* y, const double* b) {
@@ -2351,12 +1810,11 @@ struct Problem {
           CUtensorMap tm;
           std::memset(&tm, 0, sizeof(tm));
           if (tma3) tm = host::lattice_tmap3(x, D.a.nl, D.a.ld, Cut3SmemV3<P, true>::RS, 4 * P + 1, 4 * P + 1);
-          static bool attr3 = false;
-          if (!attr3) {
+          static const char attr3_key = 0;   // per-device attribute (dev_once)
+          dev_once(&attr3_key, [&] {
             CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v3<P, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v3<P, 128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr3 = true;
-          }
+          });
           if (tma3)
             launch(k_cut_colour3v3<P, 128, true>, dim3(np), dim3(128), Cut3SmemV3<P, true>::bytes, tm, D.a,
                    (const CutDesc3*)D.act_desc + base, np, (const double*)D.inv, (const double*)x, b, D.zbuf);
@@ -2367,11 +1825,10 @@ struct Problem {
       } else
       CF_DISPATCH3(prm.p, {
         const size_t pw = Cut3Smem<P>::per_warp * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
+        static const char attr_key = 0;   // per-device attribute (dev_once)
+        dev_once(&attr_key, [&] {
           CF_CUDA(cudaFuncSetAttribute(k_cut_colour3v2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          attr = true;
-        }
+        });
         launch(k_cut_colour3v2<P>, dim3(np), dim3(128), pw, D.a, (const CutDesc3*)D.act_desc + base, np,
                (const double*)D.inv, (const double*)x, b, D.zbuf);
       });

@@ -404,62 +404,6 @@ __global__ void __launch_bounds__(TP* TP*(2 * P - 1)) k_cart_colour_v2(LevelArgs
   cart_tile<P, TP>(L, tiles[blockIdx.x], colour, vk, x, b, sm);
 }
 
-// ---- persistent smoothing step ---------------------------------------------
-// All colour steps of one application of S (P eq. smoother-split) in one
-// cooperative launch: Cartesian colours (CTA per tile), then n_c sweeps of
-// cut colours (warp per patch, corrections to zbuf, grid barrier, scatter,
-// grid barrier).  A grid barrier separates dependent colour steps; the
-// order is reversed for the adjoint (post-)smoother (R9).
-struct SmoothArgs {
-  LevelArgs L;
-  const int* tiles;
-  int tile_off[5];
-  const CutDesc* desc;
-  int cut_off[5];
-  int64_t ent_off_c[5];
-  const int32_t* ent_node;
-  const double* ecut;
-  const double* inv;
-  const uint8_t* vk;
-  double* zbuf;
-  double* x;
-  const double* b;
-  int n_c, reverse, cut_wpb;
-};
-
-template <int P, int TP, bool QUAD>
-__global__ void __launch_bounds__(256) k_smooth_persistent(SmoothArgs A) {
-  extern __shared__ double sm[];
-  __shared__ SmTab T;
-  load_smtab<P>(T);
-  __syncthreads();
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  const int nphase = 4 + 4 * A.n_c;
-  const int w = threadIdx.x >> 5;
-  for (int s = 0; s < nphase; ++s) {
-    const int ph = A.reverse ? nphase - 1 - s : s;
-    if (ph < 4) {
-      const int c = ph, nt = A.tile_off[c + 1] - A.tile_off[c];
-      for (int t = blockIdx.x; t < nt; t += gridDim.x) cart_tile<P, TP>(A.L, A.tiles[A.tile_off[c] + t], c, A.vk, A.x, A.b, sm);
-      grid.sync();
-    } else {
-      const int c = (ph - 4) & 3, np = A.cut_off[c + 1] - A.cut_off[c];
-      if (w < A.cut_wpb) {
-        for (int k = blockIdx.x * A.cut_wpb + w; k < np; k += gridDim.x * A.cut_wpb) {
-          const CutDesc d = A.desc[A.cut_off[c] + k];
-          cut_patch_z<P, QUAD>(A.L, d, A.ecut, A.inv, A.x, A.b, A.zbuf, T, sm + (size_t)w * CutSmem<P>::per_warp);
-        }
-      }
-      grid.sync();
-      const int64_t e1 = A.ent_off_c[c + 1];
-      for (int64_t e = A.ent_off_c[c] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
-           e += (int64_t)gridDim.x * blockDim.x)
-        A.x[A.ent_node[e]] += A.zbuf[e];
-      if (s + 1 < nphase) grid.sync();
-    }
-  }
-}
-
 }  // namespace cf
 
 namespace cf {
@@ -1200,334 +1144,6 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
 
 namespace cf {
 
-// ---- cut colour step v4: a CTA of NT threads per patch ---------------------
-// Same arithmetic as cut_patch_z3 with the work split over NT threads:
-// (face, k, l) jump jobs, (face, k, q) moment jobs, (cell, local row) jobs
-// for the cell + ghost-face terms, a fixed-order gather per block row, then
-// A_j^{-1} r; shortens the per-patch dependency chain ~3x.
-template <int P>
-struct CutSmem4 {
-  static constexpr int NB = (P + 1) * (P + 1), BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, NJ = 12 * P * (P + 1);
-  static constexpr int doubles = WS * WS + 2 * NJ + 4 * NB + MM + MM * MM + 4 * NB * NB + MM;
-};
-
-template <int P, int NT>
-__global__ void __launch_bounds__(NT) k_cut_step4(LevelArgs L, const CutDesc* desc, int np, int patch_blocks,
-                                                  const double* ecut, const double* inv, const double* R, double* W,
-                                                  const double* b, const int32_t* copy, int ncopy) {
-  using S = CutSmem4<P>;
-  constexpr int NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, NJ = S::NJ, PP = P * (P + 1);
-  __shared__ SmTab T;
-  extern __shared__ double sm4[];
-  const int tid = threadIdx.x;
-  CF_TSTAMP(0);
-  pdl_trigger();
-  if ((int)blockIdx.x >= patch_blocks) {
-    const int e = (blockIdx.x - patch_blocks) * NT + tid;
-    if (e < ncopy) {
-      const int32_t node = copy[e];
-      pdl_wait();
-      W[node] = R[node];
-    }
-    return;
-  }
-  double* Wp = sm4;
-  double* Jt = Wp + WS * WS;
-  double* Jm = Jt + NJ;
-  double* Yc = Jm + NJ;        // [4][NB]
-  double* Rr = Yc + 4 * NB;    // [MM]
-  double* Ai = Rr + MM;        // [MM*MM]
-  double* Ec = Ai + MM * MM;   // [4][NB*NB]
-  double* zs = Ec + 4 * NB * NB;
-  __shared__ CutDesc sd;
-  if (tid == 0) sd = desc[blockIdx.x];
-  load_smtab<P>(T);
-  __syncthreads();
-  CF_TSTAMP(1);
-  const CutDesc& d = sd;
-  const int m = mask_count(d);
-  const double* Ag = inv + d.inv_off;
-  for (int e = tid; e < m * m; e += NT) cp_async8(Ai + e, Ag + e);
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (d.cid[q] >= 0)
-      for (int e = tid; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
-  pdl_wait();
-  CF_TSTAMP(2);
-  for (int e = tid; e < WS * WS; e += NT) {
-    const int r = e / WS, c = e - r * WS;
-    const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
-    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, R + (size_t)bb * L.ld + a);
-    else Wp[e] = 0.0;
-  }
-  // this thread's block row (if interior): b and its index in the interior set
-  constexpr int RPT = (MM + NT - 1) / NT;
-  double bv[RPT];
-  int iidx[RPT];
-#pragma unroll
-  for (int t = 0; t < RPT; ++t) {
-    const int loc = tid + NT * t;
-    iidx[t] = -1;
-    bv[t] = 0.0;
-    if (loc < MM) {
-      const unsigned long long word = d.mask[loc >> 6];
-      if ((word >> (loc & 63)) & 1ull) {
-        iidx[t] = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
-        bv[t] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
-      }
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  CF_TSTAMP(3);
-  for (int job = tid; job < NJ; job += NT) {
-    const int f = job / PP, rem = job - f * PP, k = rem / (P + 1) + 1, l = rem % (P + 1);
-    int axis, w1x, w1y, w2x, w2y;
-    face_cells(f, axis, w1x, w1y, w2x, w2y);
-    const int k1 = desc_kind(d, w1x, w1y), k2 = desc_kind(d, w2x, w2y);
-    double s = 0.0;
-    if (k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT)) {
-      const double* X1 = Wp + (P * w1y) * WS + P * w1x;
-      const double* X2 = Wp + (P * w2y) * WS + P * w2x;
-      const int sn = axis == 0 ? 1 : WS, st = axis == 0 ? WS : 1;
-#pragma unroll
-      for (int nn = 0; nn <= P; ++nn) s = fma(T.d1[k][nn], X1[l * st + nn * sn], fma(-T.d0[k][nn], X2[l * st + nn * sn], s));
-    }
-    Jt[job] = s;
-  }
-  __syncthreads();
-  for (int job = tid; job < NJ; job += NT) {
-    const int base = job - job % (P + 1), q = job % (P + 1);
-    double s = 0.0;
-#pragma unroll
-    for (int l = 0; l <= P; ++l) s = fma(T.M[q][l], Jt[base + l], s);
-    Jm[job] = s;
-  }
-  __syncthreads();
-  for (int job = tid; job < 4 * NB; job += NT) {
-    const int q = job / NB, t = job - q * NB;
-    const int dx = q & 1, dy = q >> 1, kx = t % (P + 1), ky = t / (P + 1);
-    const int kind = desc_kind(d, dx + 1, dy + 1);
-    double y = 0.0;
-    if (kind != OUTSIDE) {
-      const double* X = Wp + (P * (dy + 1)) * WS + P * (dx + 1);
-      if (kind == INSIDE) {
-        y = inside_row<P>(T, X, WS, kx, ky);
-      } else {
-        const double* Er = Ec + q * NB * NB + t * NB;
-#pragma unroll
-        for (int l = 0; l < NB; ++l) y = fma(Er[l], X[(l / (P + 1)) * WS + l % (P + 1)], y);
-      }
-      const int fl = 2 * dx + dy, fr = 2 * (dx + 1) + dy, fb = 6 + 2 * dy + dx, ft = 6 + 2 * (dy + 1) + dx;
-#pragma unroll
-      for (int kk = 1; kk <= P; ++kk) {
-        const double gk = L.gs[kk];
-        y = fma(-gk * T.d0[kk][kx], Jm[fl * PP + (kk - 1) * (P + 1) + ky], y);
-        y = fma(gk * T.d1[kk][kx], Jm[fr * PP + (kk - 1) * (P + 1) + ky], y);
-        y = fma(-gk * T.d0[kk][ky], Jm[fb * PP + (kk - 1) * (P + 1) + kx], y);
-        y = fma(gk * T.d1[kk][ky], Jm[ft * PP + (kk - 1) * (P + 1) + kx], y);
-      }
-    }
-    Yc[job] = y;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < RPT; ++t) {
-    const int loc = tid + NT * t;
-    if (iidx[t] < 0) continue;
-    const int ra = loc % BS, rb = loc / BS;
-    double y = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int kx = ra - P * (q & 1), ky = rb - P * (q >> 1);
-      if (kx >= 0 && kx <= P && ky >= 0 && ky <= P) y += Yc[q * NB + ky * (P + 1) + kx];
-    }
-    Rr[iidx[t]] = bv[t] - y;
-  }
-  __syncthreads();
-  CF_TSTAMP(4);
-  for (int i = tid; i < m; i += NT) {
-    double z = 0.0;
-    for (int q = 0; q < m; ++q) z = fma(Ai[q * m + i], Rr[q], z);
-    zs[i] = z;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int t = 0; t < RPT; ++t) {
-    const int loc = tid + NT * t;
-    if (iidx[t] < 0) continue;
-    const int ra = loc % BS, rb = loc / BS;
-    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + zs[iidx[t]];
-  }
-  CF_TSTAMP(5);
-}
-
-
-// v5: the v4 step with three barriers instead of six: (1) ghost-face jumps and
-// their M-moments computed in registers by one thread per (face, order)
-// together with the cell parts of the (cell, row) outputs, (2) the interior
-// rows gather their cells' outputs plus those cells' ghost-face terms (a
-// 12-bit ghost mask skips the others), (3) thread i applies row i of the
-// local inverse and writes its node directly.
-template <int P, int NT>
-__global__ void __launch_bounds__(NT) k_cut_step5(LevelArgs L, const CutDesc* desc, int np, int patch_blocks,
-                                                  const double* ecut, const double* inv, const double* R, double* W,
-                                                  const double* b, const int32_t* copy, int ncopy) {
-  using S = CutSmem4<P>;
-  constexpr int NB = S::NB, BS = S::BS, WS = S::WS, MM = S::MM, PP = P * (P + 1), N1 = P + 1;
-  __shared__ SmTab T;
-  __shared__ CutDesc sd;
-  __shared__ unsigned gmask;
-  __shared__ short Lc[MM];
-  extern __shared__ double sm5[];
-  const int tid = threadIdx.x;
-  CF_TSTAMP(0);
-  pdl_trigger();
-  if ((int)blockIdx.x >= patch_blocks) {
-    const int e = (blockIdx.x - patch_blocks) * NT + tid;
-    if (e < ncopy) {
-      const int32_t node = copy[e];
-      pdl_wait();
-      W[node] = R[node];
-    }
-    return;
-  }
-  double* Wp = sm5;
-  double* Jm = Wp + WS * WS;   // [12 faces][P][N1]
-  double* Yc = Jm + 12 * PP;   // [4][NB]
-  double* Rr = Yc + 4 * NB;    // [MM]
-  double* Ai = Rr + MM;        // [MM*MM]
-  double* Ec = Ai + MM * MM;   // [4][NB*NB]
-  if (tid == 0) {
-    sd = desc[blockIdx.x];
-    gmask = 0u;
-  }
-  load_smtab<P>(T);
-  __syncthreads();
-  CF_TSTAMP(1);
-  const CutDesc& d = sd;
-  const int m = mask_count(d);
-  const double* Ag = inv + d.inv_off;
-  for (int e = tid; e < m * m; e += NT) cp_async8(Ai + e, Ag + e);
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (d.cid[q] >= 0)
-      for (int e = tid; e < NB * NB; e += NT) cp_async8(Ec + q * NB * NB + e, ecut + (size_t)d.cid[q] * NB * NB + e);
-  pdl_wait();
-  CF_TSTAMP(2);
-  for (int e = tid; e < WS * WS; e += NT) {
-    const int r = e / WS, c = e - r * WS;
-    const int a = P * (d.I - 2) + c, bb = P * (d.J - 2) + r;
-    if (a >= 0 && bb >= 0 && a < L.nl && bb < L.nl) cp_async8(Wp + e, R + (size_t)bb * L.ld + a);
-    else Wp[e] = 0.0;
-  }
-  for (int loc = tid; loc < MM; loc += NT) {
-    const unsigned long long word = d.mask[loc >> 6];
-    if ((word >> (loc & 63)) & 1ull) {
-      const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
-      Lc[i] = (short)loc;
-      Rr[i] = b[(size_t)(P * (d.J - 1) + loc / BS) * L.ld + P * (d.I - 1) + loc % BS];
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  CF_TSTAMP(3);
-  // (1) face moments and cell parts
-  for (int job = tid; job < 12 * P + 4 * NB; job += NT) {
-    if (job >= 12 * P) {
-      const int jr = job - 12 * P, q = jr / NB, t = jr - q * NB;
-      const int dx = q & 1, dy = q >> 1, kx = t % N1, ky = t / N1;
-      const int kind = desc_kind(d, dx + 1, dy + 1);
-      double y = 0.0;
-      if (kind != OUTSIDE) {
-        const double* X = Wp + (P * (dy + 1)) * WS + P * (dx + 1);
-        if (kind == INSIDE) {
-          y = inside_row<P>(T, X, WS, kx, ky);
-        } else {
-          const double* Er = Ec + q * NB * NB + t * NB;
-#pragma unroll
-          for (int l = 0; l < NB; ++l) y = fma(Er[l], X[(l / N1) * WS + l % N1], y);
-        }
-      }
-      Yc[jr] = y;
-      continue;
-    }
-    const int f = job / P, k = job - f * P + 1;
-    int axis, w1x, w1y, w2x, w2y;
-    face_cells(f, axis, w1x, w1y, w2x, w2y);
-    const int k1 = desc_kind(d, w1x, w1y), k2 = desc_kind(d, w2x, w2y);
-    if (!(k1 != OUTSIDE && k2 != OUTSIDE && (k1 == CUT || k2 == CUT))) continue;
-    if (k == 1) atomicOr(&gmask, 1u << f);
-    const double* X1 = Wp + (P * w1y) * WS + P * w1x;
-    const double* X2 = Wp + (P * w2y) * WS + P * w2x;
-    const int sn = axis == 0 ? 1 : WS, st = axis == 0 ? WS : 1;
-    double J[N1];
-#pragma unroll
-    for (int l = 0; l < N1; ++l) {
-      double a = 0.0;
-#pragma unroll
-      for (int nn = 0; nn <= P; ++nn) a = fma(T.d1[k][nn], X1[l * st + nn * sn], fma(-T.d0[k][nn], X2[l * st + nn * sn], a));
-      J[l] = a;
-    }
-#pragma unroll
-    for (int q = 0; q < N1; ++q) {
-      double a = 0.0;
-#pragma unroll
-      for (int l = 0; l < N1; ++l) a = fma(T.M[q][l], J[l], a);
-      Jm[f * PP + (k - 1) * N1 + q] = a;
-    }
-  }
-  __syncthreads();
-  CF_TSTAMP(4);
-  // (2) residual on the interior rows
-  const unsigned gm = gmask;
-  for (int i = tid; i < m; i += NT) {
-    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
-    double y = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int dx = q & 1, dy = q >> 1;
-      const int kx = ra - P * dx, ky = rb - P * dy;
-      if (kx < 0 || kx > P || ky < 0 || ky > P) continue;
-      double yq = Yc[q * NB + ky * N1 + kx];
-      const int fl = 2 * dx + dy, fr = 2 * (dx + 1) + dy, fb = 6 + 2 * dy + dx, ft = 6 + 2 * (dy + 1) + dx;
-      if ((gm >> fl) & 1u)
-#pragma unroll
-        for (int kk = 1; kk <= P; ++kk) yq = fma(-L.gs[kk] * T.d0[kk][kx], Jm[fl * PP + (kk - 1) * N1 + ky], yq);
-      if ((gm >> fr) & 1u)
-#pragma unroll
-        for (int kk = 1; kk <= P; ++kk) yq = fma(L.gs[kk] * T.d1[kk][kx], Jm[fr * PP + (kk - 1) * N1 + ky], yq);
-      if ((gm >> fb) & 1u)
-#pragma unroll
-        for (int kk = 1; kk <= P; ++kk) yq = fma(-L.gs[kk] * T.d0[kk][ky], Jm[fb * PP + (kk - 1) * N1 + kx], yq);
-      if ((gm >> ft) & 1u)
-#pragma unroll
-        for (int kk = 1; kk <= P; ++kk) yq = fma(L.gs[kk] * T.d1[kk][ky], Jm[ft * PP + (kk - 1) * N1 + kx], yq);
-      y += yq;
-    }
-    Rr[i] -= y;
-  }
-  __syncthreads();
-  CF_TSTAMP(5);
-  // (3) z = A_j^{-1} r, written to the interior nodes
-  for (int i = tid; i < m; i += NT) {
-    double z0 = 0.0, z1 = 0.0;
-    int q = 0;
-    for (; q + 1 < m; q += 2) {
-      z0 = fma(Ai[q * m + i], Rr[q], z0);
-      z1 = fma(Ai[(q + 1) * m + i], Rr[q + 1], z1);
-    }
-    if (q < m) z0 = fma(Ai[q * m + i], Rr[q], z0);
-    const int loc = Lc[i], ra = loc % BS, rb = loc / BS;
-    W[(size_t)(P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra] = Wp[(P + rb) * WS + P + ra] + (z0 + z1);
-  }
-  CF_TSTAMP(6);
-}
-
-}  // namespace cf
-
-namespace cf {
-
 // ---- operator A x (or b - A x) on a TMA-staged tile ------------------------
 // CTA per TX x TX cells; the x tile with a one-cell halo is loaded by TMA
 // (zero-filled outside the lattice); one thread per owned lattice node sums
@@ -1839,163 +1455,6 @@ __global__ void __launch_bounds__(NT) k_cut_step6(LevelArgs L, const CutDesc* de
   CF_TSTAMP(3);
 }
 
-// ---- all n_c x 4 cut colour steps of one smoothing step in ONE launch: a
-// cluster of CS CTAs, each with G groups of 64 threads (one patch per group
-// at a time); the ping-pong steps are separated by cluster barriers
-// (barrier.cluster arrive.release / wait.acquire orders the global-memory
-// writes of one step before the reads of the next), which replaces a kernel
-// boundary on levels whose colours have at most a few hundred cut patches.
-struct CutSweepArgs {
-  LevelArgs L;
-  const CutDesc* desc;
-  int cut_off[5];           // patches of colour c: [cut_off[c], cut_off[c+1])
-  const int32_t* copy;      // copy lists N_prev \ N_cur
-  int copy_off[5][4], copy_n[5][4];
-  const double* ecut;
-  const double* inv;
-  double* x;                // in: x; out: x (even step count) or xs
-  double* xs;
-  const double* b;
-  int n_c, reverse;
-  const double* gmap;       // cut-patch maps (k_cut_sweeps_cluster7)
-};
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ unsigned cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ unsigned cluster_nctas() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-  return r;
-}
-
-template <int P, int G>
-__global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster(CutSweepArgs A) {
-  using S = CutGroup6<P>;
-  __shared__ SmTab T;
-  extern __shared__ __align__(128) unsigned char smc[];
-  const int tid = threadIdx.x, grp = tid >> 6, gt = tid & 63;
-  const int cr = (int)cluster_rank(), cs = (int)cluster_nctas();
-  unsigned char* gsm = smc + (size_t)grp * ((S::bytes + 127) & ~127);
-  CF_TSTAMP(0);
-  pdl_trigger();
-  // stream this level's setup data (descriptors, inverses, element matrices)
-  // into L2 while the first step starts
-  if (tid == 0) {
-    const int np = A.cut_off[4];
-    const size_t dsz = (size_t)np * sizeof(CutDesc), chunk = (dsz + cs - 1) / cs;
-    if (chunk && cr * chunk < dsz) prefetch_l2((const char*)A.desc + cr * chunk, min(chunk, dsz - cr * chunk));
-  }
-  load_smtab<P>(T);
-  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
-  auto first_patch = [&](int s) { return cr * G + grp; };   // round-0 patch index of this group in step s
-  // prologue of step 0 (independent of x)
-  {
-    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c], k = first_patch(0);
-    if (k < np) cut6_prologue<P, 64>(A.desc, A.cut_off[c] + k, A.ecut, A.inv, gsm, gt, 1 + grp);
-  }
-  __syncthreads();
-  pdl_wait();
-  CF_TSTAMP(1);
-  double* bufs[2] = {A.x, A.xs};
-  int prev = 4;
-  const int nsteps = A.n_c * 4;
-  for (int s = 0; s < nsteps; ++s) {
-    const int c = step_colour(s);
-    const double* R = bufs[s & 1];
-    double* W = bufs[(s + 1) & 1];
-    // copy list of this step (W <- R on N_prev \ N_c)
-    const int nco = A.copy_n[prev][c];
-    const int32_t* cl = A.copy + A.copy_off[prev][c];
-    for (int e = cr * 64 * G + tid; e < nco; e += cs * 64 * G) W[cl[e]] = R[cl[e]];
-    // the patches of colour c, one per group per round (round 0's prologue
-    // was issued before the previous barrier)
-    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
-    const int rounds = (np + cs * G - 1) / (cs * G);
-    for (int r = 0; r < rounds; ++r) {
-      const int k = (r * cs + cr) * G + grp;
-      if (k < np) {
-        if (r > 0) cut6_prologue<P, 64>(A.desc, p0 + k, A.ecut, A.inv, gsm, gt, 1 + grp);
-        cut6_main<P, 64>(A.L, T, R, W, A.b, gsm, gt, 1 + grp);
-        group_sync(1 + grp, 64);   // the group's shared buffers are reused next
-      }
-    }
-    // prologue of the next step's round-0 patch, overlapping the barrier
-    if (s + 1 < nsteps) {
-      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn], kn = first_patch(s + 1);
-      if (kn < npn) cut6_prologue<P, 64>(A.desc, A.cut_off[cn] + kn, A.ecut, A.inv, gsm, gt, 1 + grp);
-    }
-    prev = c;
-    cluster_sync_all();
-    if (s < 5) CF_TSTAMP(2 + s);
-  }
-  CF_TSTAMP(7);
-}
-
-}  // namespace cf
-
-namespace cf {
-
-// ---- all n_c x 4 cut colour steps of one smoothing step in ONE cooperative
-// launch over the whole GPU: CTAs of G groups of 64 threads (one patch per
-// group per round, the v6 group routine), grid-wide barriers between the
-// ping-pong steps instead of kernel boundaries.  The window of a step is read
-// with ld.global.cg (the previous step was written by other SMs in this
-// launch); the next step's descriptor / inverse / element-matrix prologue is
-// issued before the barrier.
-template <int P, int G>
-__global__ void __launch_bounds__(64 * G) k_cut_sweeps_grid(CutSweepArgs A) {
-  using S = CutGroup6<P>;
-  __shared__ SmTab T;
-  extern __shared__ __align__(128) unsigned char smg[];
-  const int tid = threadIdx.x, grp = tid >> 6, gt = tid & 63;
-  const int cr = (int)blockIdx.x, cs = (int)gridDim.x;
-  unsigned char* gsm = smg + (size_t)grp * ((S::bytes + 127) & ~127);
-  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-  pdl_trigger();
-  load_smtab<P>(T);
-  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
-  const int k0 = cr * G + grp;   // round-0 patch of this group
-  {
-    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c];
-    if (k0 < np) cut6_prologue<P, 64>(A.desc, A.cut_off[c] + k0, A.ecut, A.inv, gsm, gt, 1 + grp);
-  }
-  __syncthreads();
-  pdl_wait();
-  double* bufs[2] = {A.x, A.xs};
-  int prev = 4;
-  const int nsteps = A.n_c * 4;
-  for (int s = 0; s < nsteps; ++s) {
-    const int c = step_colour(s);
-    const double* R = bufs[s & 1];
-    double* W = bufs[(s + 1) & 1];
-    const int nco = A.copy_n[prev][c];
-    const int32_t* cl = A.copy + A.copy_off[prev][c];
-    for (int e = cr * 64 * G + tid; e < nco; e += cs * 64 * G) W[cl[e]] = __ldcg(R + cl[e]);
-    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
-    const int rounds = (np + cs * G - 1) / (cs * G);
-    for (int r = 0; r < rounds; ++r) {
-      const int k = (r * cs + cr) * G + grp;
-      if (k < np) {
-        if (r > 0) cut6_prologue<P, 64>(A.desc, p0 + k, A.ecut, A.inv, gsm, gt, 1 + grp);
-        cut6_main<P, 64, true>(A.L, T, R, W, A.b, gsm, gt, 1 + grp);
-        group_sync(1 + grp, 64);
-      }
-    }
-    if (s + 1 < nsteps) {
-      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn];
-      if (k0 < npn) cut6_prologue<P, 64>(A.desc, A.cut_off[cn] + k0, A.ecut, A.inv, gsm, gt, 1 + grp);
-      grid.sync();
-    }
-    prev = c;
-  }
-}
-
 }  // namespace cf
 
 namespace cf {
@@ -2236,121 +1695,6 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
   cut7_prologue<P, NT>(desc, blockIdx.x, G, sm7, tid, 0);
   pdl_wait();
   cut7_main<P, NT, false>(L, R, W, b, sm7, tid, 0);
-}
-
-// all n_c x 4 cut steps of a smoothing step in ONE launch of one
-// thread-block cluster (CTAs of G groups of 64 threads, the step-7 routine,
-// cluster barriers between the ping-pong steps; the next step's prologue is
-// issued before the barrier).  For small levels, where a launch per step
-// costs more than the step.
-template <int P, int G>
-__global__ void __launch_bounds__(64 * G) k_cut_sweeps_cluster7(CutSweepArgs A) {
-  using S = CutMapSmem<P>;
-  extern __shared__ __align__(128) unsigned char smc7[];
-  const int tid = threadIdx.x, grp = tid >> 6, gt = tid & 63;
-  const int cr = (int)cluster_rank(), cs = (int)cluster_nctas();
-  unsigned char* gsm = smc7 + (size_t)grp * ((S::bytes + 127) & ~(size_t)127);
-  pdl_trigger();
-  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
-  const int k0 = cr * G + grp;
-  {
-    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c];
-    if (k0 < np) cut7_prologue<P, 64>(A.desc, A.cut_off[c] + k0, A.gmap, gsm, gt, 1 + grp);
-  }
-  pdl_wait();
-  cluster_sync_all();
-  double* bufs[2] = {A.x, A.xs};
-  int prev = 4;
-  const int nsteps = A.n_c * 4;
-  for (int s = 0; s < nsteps; ++s) {
-    const int c = step_colour(s);
-    const double* R = bufs[s & 1];
-    double* W = bufs[(s + 1) & 1];
-    const int nco = A.copy_n[prev][c];
-    const int32_t* cl = A.copy + A.copy_off[prev][c];
-    for (int e = cr * 64 * G + tid; e < nco; e += cs * 64 * G) W[cl[e]] = __ldcg(R + cl[e]);
-    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
-    const int rounds = (np + cs * G - 1) / (cs * G);
-    for (int r = 0; r < rounds; ++r) {
-      const int k = (r * cs + cr) * G + grp;
-      if (k < np) {
-        if (r > 0) cut7_prologue<P, 64>(A.desc, p0 + k, A.gmap, gsm, gt, 1 + grp);
-        cut7_main<P, 64, true>(A.L, R, W, A.b, gsm, gt, 1 + grp);
-        group_sync(1 + grp, 64);
-      }
-    }
-    if (s + 1 < nsteps) {
-      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn];
-      if (k0 < npn) cut7_prologue<P, 64>(A.desc, A.cut_off[cn] + k0, A.gmap, gsm, gt, 1 + grp);
-    }
-    prev = c;
-    cluster_sync_all();
-  }
-}
-
-// grid-wide barrier with release/acquire: the CTAs' global writes before the
-// barrier are visible to every CTA after it (the cut steps read the previous
-// step's W through L2).  Counter as grid_barrier(): monotonic, one per level.
-__device__ __forceinline__ void grid_barrier_mem(unsigned long long* ctr) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long nb = gridDim.x;
-    unsigned long long t, v;
-    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(t) : "l"(ctr) : "memory");
-    const unsigned long long target = (t / nb + 1) * nb;
-    do {
-      asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
-// all n_c x 4 cut steps of a smoothing step in ONE cooperative launch over the
-// GPU (k_cut_sweeps_cluster7 with blockIdx / gridDim for the cluster rank /
-// size and a grid barrier between the ping-pong steps): removes the launch
-// gap of each of the 8 cut colour steps on large levels.
-template <int P, int G, int NTG>
-__global__ void __launch_bounds__(NTG * G) k_cut_sweeps_grid7(CutSweepArgs A, unsigned long long* gbar) {
-  using S = CutMapSmem<P>;
-  extern __shared__ __align__(128) unsigned char smg7[];
-  const int tid = threadIdx.x, grp = tid / NTG, gt = tid % NTG;
-  const int cr = (int)blockIdx.x, cs = (int)gridDim.x;
-  unsigned char* gsm = smg7 + (size_t)grp * ((S::bytes + 127) & ~(size_t)127);
-  auto step_colour = [&](int s) { return A.reverse ? 3 - (s & 3) : (s & 3); };
-  const int k0 = cr * G + grp;
-  {
-    const int c = step_colour(0), np = A.cut_off[c + 1] - A.cut_off[c];
-    if (k0 < np) cut7_prologue<P, NTG>(A.desc, A.cut_off[c] + k0, A.gmap, gsm, gt, 1 + grp);
-  }
-  pdl_wait();
-  double* bufs[2] = {A.x, A.xs};
-  int prev = 4;
-  const int nsteps = A.n_c * 4;
-  for (int s = 0; s < nsteps; ++s) {
-    const int c = step_colour(s);
-    const double* R = bufs[s & 1];
-    double* W = bufs[(s + 1) & 1];
-    const int nco = A.copy_n[prev][c];
-    const int32_t* cl = A.copy + A.copy_off[prev][c];
-    for (int e = cr * NTG * G + tid; e < nco; e += cs * NTG * G) W[cl[e]] = __ldcg(R + cl[e]);
-    const int p0 = A.cut_off[c], np = A.cut_off[c + 1] - p0;
-    const int rounds = (np + cs * G - 1) / (cs * G);
-    for (int r = 0; r < rounds; ++r) {
-      const int k = (r * cs + cr) * G + grp;
-      if (k < np) {
-        if (r > 0) cut7_prologue<P, NTG>(A.desc, p0 + k, A.gmap, gsm, gt, 1 + grp);
-        cut7_main<P, NTG, true>(A.L, R, W, A.b, gsm, gt, 1 + grp);
-        group_sync(1 + grp, NTG);
-      }
-    }
-    if (s + 1 < nsteps) {
-      const int cn = step_colour(s + 1), npn = A.cut_off[cn + 1] - A.cut_off[cn];
-      if (k0 < npn) cut7_prologue<P, NTG>(A.desc, A.cut_off[cn] + k0, A.gmap, gsm, gt, 1 + grp);
-    }
-    prev = c;
-    grid_barrier_mem(gbar);
-    if (s == 0) pdl_trigger();   // every CTA is resident: dependents may be scheduled
-  }
 }
 
 }  // namespace cf

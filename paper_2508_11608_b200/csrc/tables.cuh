@@ -214,9 +214,9 @@ inline void build_tab(int p, Tab& t) {
     }
 }
 
-inline void upload_tables() {
-  static bool done = false;
-  if (done) return;
+inline void upload_tables() {   // __constant__ / __device__ tables: once per device
+  static const char key = 0;
+  dev_once(&key, [] {
   Tab tabs[CF_MAXP + 1];
   std::memset(&tabs[0], 0, sizeof(Tab));
   for (int p = 1; p <= CF_MAXP; ++p) build_tab(p, tabs[p]);
@@ -226,7 +226,7 @@ inline void upload_tables() {
   for (int n = 1; n <= CF_MAXNQ; ++n) gauss_legendre(n, gx[n], gw[n]);
   CF_CUDA(cudaMemcpyToSymbol(c_gx, gx, sizeof(gx)));
   CF_CUDA(cudaMemcpyToSymbol(c_gw, gw, sizeof(gw)));
-  done = true;
+  });
 }
 
 }  // namespace host
@@ -304,9 +304,9 @@ namespace cf {
 namespace host {
 // per-degree dense patch maps in global memory (p = 1..3), built once per process
 inline const double* cart_map(int p) {
-  static const double* maps[CF_MAXP + 1] = {nullptr};
+  static const char keys[CF_MAXP + 1] = {};   // device pointer per (degree, device)
   if (p < 1 || p > 3) return nullptr;
-  if (!maps[p]) {
+  return (const double*)dev_cached(&keys[p], [&] {
     Tab t;
     build_tab(p, t);
     int rp = 0, cp = 0;
@@ -314,9 +314,8 @@ inline const double* cart_map(int p) {
     void* d = nullptr;
     CF_CUDA(cudaMalloc(&d, G.size() * sizeof(double)));
     CF_CUDA(cudaMemcpy(d, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice));
-    maps[p] = (const double*)d;
-  }
-  return maps[p];
+    return (int64_t)d;
+  });
 }
 }  // namespace host
 }  // namespace cf
@@ -383,9 +382,9 @@ inline std::vector<double> cart_affine_map3(int p, const Tab& t, int& cols_pad) 
 }
 
 inline const double* cart_map3(int p) {
-  static const double* maps[3] = {nullptr};
+  static const char keys[CF_MAXP + 1] = {};   // device pointer per (degree, device)
   if (p < 1 || p > 2) return nullptr;
-  if (!maps[p]) {
+  return (const double*)dev_cached(&keys[p], [&] {
     Tab t;
     build_tab(p, t);
     int cp = 0;
@@ -393,9 +392,8 @@ inline const double* cart_map3(int p) {
     void* d = nullptr;
     CF_CUDA(cudaMalloc(&d, G.size() * sizeof(double)));
     CF_CUDA(cudaMemcpy(d, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice));
-    maps[p] = (const double*)d;
-  }
-  return maps[p];
+    return (int64_t)d;
+  });
 }
 }  // namespace host
 }  // namespace cf

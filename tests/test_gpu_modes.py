@@ -48,20 +48,15 @@ def run_smoother(w, env=None, oracle_kw=None, **gkw):
 
 @pytest.mark.parametrize("env", [{"CUTFEM_MMA": "0"}, {"CUTFEM_FUSED": "0"}, {"CUTFEM_PINGPONG": "0"},
                                  {"CUTFEM_PDL": "0"}, {"CUTFEM_TMA": "0"}, {"CUTFEM_CTACUT": "0"},
-                                 {"CUTFEM_TILEAPPLY": "0"}, {"CUTFEM_CUT2": "4", "CUTFEM_CLUSTER_MAX": "0"},
-                                 {"CUTFEM_CUT2": "5", "CUTFEM_CLUSTER_MAX": "0"}, {"CUTFEM_CLUSTER_MAX": "512"},
-                                 {"CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CART_SPLIT": "1", "CUTFEM_TMA": "0"},
+                                 {"CUTFEM_TILEAPPLY": "0"}, {"CUTFEM_CART_SPLIT": "1"},
+                                 {"CUTFEM_CART_SPLIT": "1", "CUTFEM_TMA": "0"},
                                  {"CUTFEM_CART_SPLIT": "1", "CUTFEM_MMA": "0"}, {"CUTFEM_TC32_MIN_N": "32"},
-                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CUT_GRID": "1"}, {"CUTFEM_CUTMAP": "0"}, {"CUTFEM_VC_MAX_N": "0"}, {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_TCX": "24"},
-                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_TCX": "16", "CUTFEM_CART_SPLIT": "1"},
-                                 {"CUTFEM_CLUSTER7_MAX": "100000"}, {"CUTFEM_CUT_GRID7": "0"},
-                                 {"CUTFEM_CUT_GRID7": "1", "CUTFEM_CUT_GRID7_MIN_NP": "1"}, {"CUTFEM_DF": "0"},
-                                 {"CUTFEM_DF_TILE": "4"}, {"CUTFEM_DF_BUDGET": "6000"}, {"CUTFEM_DF_TILE": "64"}],
+                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_CART_SPLIT": "1"}, {"CUTFEM_CUTMAP": "0"},
+                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_TCX": "24"},
+                                 {"CUTFEM_TC32_MIN_N": "32", "CUTFEM_TCX": "16", "CUTFEM_CART_SPLIT": "1"}],
                          ids=["fd", "separate", "no-pingpong", "no-pdl", "no-tma", "warp-per-cut-patch", "node-apply",
-                              "cut-step-v4", "cut-step-v5", "cluster-cut-sweeps", "cart-split-tma",
-                              "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split", "cut-sweeps-one-grid-launch", "cut-step-matrix-free", "vcycle-launch-per-step", "tile24x32", "tile16x32-split", "cluster-cut-sweeps-maps",
-                              "cut-step-launch-per-colour", "cut-sweeps-grid7-all-levels", "cut-steps-per-launch",
-                              "dataflow-tile4", "dataflow-small-segments", "dataflow-tile64"])
+                              "cart-split-tma", "cart-per-colour-mma", "cart-per-colour-fd", "tile32", "tile32-split",
+                              "cut-step-matrix-free", "tile24x32", "tile16x32-split"])
 def test_alternative_paths(env):
     run_smoother(W, env=env)
 
@@ -138,60 +133,3 @@ def test_cart_split_equals_inplace_fullsize():
         outs.append(g.to_host(x))
         g.close()
     np.testing.assert_array_equal(outs[0], outs[1])
-
-
-@pytest.mark.parametrize("vc_max_n", ["0", "16", "64", "100000"], ids=["launches", "n<=16", "n<=64", "all-levels"])
-@pytest.mark.parametrize("p", [1, 2, 3])
-def test_vcycle_cluster_levels(vc_max_n, p):
-    """coarse end of the V-cycle in one cluster launch (vcycle_cluster.cuh) for
-    0 / some / all levels: V-cycle vs the oracle's, identical CG iterations"""
-    from paper_2508_11608_b200 import cutfem
-    w = workloads.paper_level(p, 7 if p > 1 else 6)
-    os.environ["CUTFEM_VC_MAX_N"] = vc_max_n
-    try:
-        g = cutfem.Problem.from_workload(w)
-    finally:
-        os.environ.pop("CUTFEM_VC_MAX_N", None)
-    o = from_workload(w)
-    lf = o.fine.lv
-    bl = lattice_random(w, 77, None)
-    x = g.zeros()
-    g.vcycle(x, g.to_device(bl))
-    assert rel_err(compact(lf, g.to_host(x)), o.precondition(compact(lf, bl))) < 10 * TOL
-    xs = g.zeros()
-    it, rel = g.solve_cg_mg(xs, g.to_device(bl), tol=1e-8, max_it=200)
-    xo, ito, _ = o.solve_cg(compact(lf, bl), 1e-8, 200)
-    assert it == ito and rel <= 1e-8
-    assert rel_err(compact(lf, g.to_host(xs)), xo) < 1e-7
-
-
-def _problem(w, env):
-    from paper_2508_11608_b200 import cutfem
-    saved = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        return cutfem.Problem.from_workload(w)
-    finally:
-        for k, v in saved.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
-
-
-@pytest.mark.parametrize("w", [workloads.CONFIG1, workloads.with_degree(workloads.paper_level(2, 9), 3),
-                               workloads.paper_level(1, 9)], ids=["config1", "q3", "q1"])
-def test_dataflow_cut_sweep_bitexact_vs_step_launches(w):
-    # the dataflow sweep (cutdf.cuh) evaluates every patch map row in the order
-    # of k_cut_step7, so repeated smoothing steps (graph replays included) are
-    # bit-identical to one launch per cut colour step on every level
-    ga, gb = _problem(w, {}), _problem(w, {"CUTFEM_DF": "0"})
-    for l in range(1, w.n_levels):
-        xl, bl = lattice_random(w, 70 + l, l), lattice_random(w, 90 + l, l)
-        xa, xb = ga.to_device(xl, l), gb.to_device(xl, l)
-        ba, bb = ga.to_device(bl, l), gb.to_device(bl, l)
-        for it in range(3):
-            for rev in (False, True):
-                ga.smooth(l, xa, ba, rev)
-                gb.smooth(l, xb, bb, rev)
-        assert np.array_equal(ga.to_host(xa, l), gb.to_host(xb, l)), l

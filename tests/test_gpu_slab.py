@@ -38,13 +38,17 @@ def _cutfem():
     return cutfem
 
 
-def run_ranks(w, world, fn, timeout=300, env=None):
-    """fn(rank, problem, stream) on `world` threads; returns the per-rank results."""
+def run_ranks(w, world, fn, timeout=300, env=None, pre=None):
+    """fn(rank, problem, stream) on `world` threads; returns the per-rank results.
+    pre(problem): work on the unpartitioned problem before partition()."""
     cutfem = _cutfem()
     comms = cutfem.Comm.local(world)
     gs = []
     for c in comms:
         g = with_env(env, lambda: cutfem.Problem.from_workload(w))
+        if pre is not None:
+            pre(g)
+            torch.cuda.synchronize()
         g.partition(c)
         gs.append(g)
     torch.cuda.synchronize()
@@ -123,6 +127,39 @@ def test_partition_layout(w, world):
     # monotone: partitioned levels form a suffix of the hierarchy
     flags = [gs[0].partition_info(l)["part"] for l in range(w.n_levels)]
     assert flags == sorted(flags)
+
+
+def test_smooth_before_partition():
+    """smoothing steps on the unpartitioned problem (in-place cooperative
+    Cartesian sweep: its grid-barrier counter advances by the full tile count),
+    then partition() (fewer tiles per rank) and partitioned steps: still
+    bit-exact, no hang (the counter restarts for the new grid)"""
+    w, world = W_Q2, 2
+    L = w.n_levels - 1
+    x0, b0 = workloads.lattice_vector(w, 13), workloads.lattice_vector(w, 14)
+
+    def pre(g):
+        x, b = g.to_device(x0), g.to_device(b0)
+        for rev in (False, True, False):
+            g.smooth(L, x, b, reverse=rev)
+
+    g1 = single(w)
+    x1 = g1.to_device(x0)
+    for _ in range(2):
+        g1.smooth(L, x1, g1.to_device(b0))
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        x, b = g.to_device(x0), g.to_device(b0)
+        for _ in range(2):
+            g.smooth(L, x, b, stream=s.cuda_stream)
+        return x
+
+    xs, gs = run_ranks(w, world, fn, pre=pre, timeout=120)
+    ref = x1.cpu().numpy().reshape(-1, g1.lattice_shape(L)[1])[:, :g1.lattice_shape(L)[0]]
+    for g, x in zip(gs, xs):
+        r0, r1, a = owned(g, x, L)
+        np.testing.assert_array_equal(a, ref[r0:r1])
 
 
 TC32 = {"CUTFEM_TC32_MIN_N": "128"}   # 32-cell fused tiles on the 128^2 / 256^2 levels
