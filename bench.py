@@ -32,7 +32,6 @@ import workloads  # noqa: E402
 METRIC = "smoother DoF/s (one multiplicative vertex-patch smoothing step, finest level)"
 UNIT = "DoF/s"
 WORKLOAD = workloads.CONFIG1
-ORACLE_SAMPLE_LEVEL = 6           # 128 x 128 cells of the same hierarchy (bounded CPU sample)
 
 
 from paper_2508_11608_b200.dist import max_over_ranks, rank_env, strong_throughput  # noqa: E402
@@ -92,14 +91,15 @@ def cpu_cores():
 
 
 def oracle_sample(steps):
-    """Time the oracle smoothing step on a bounded sample of the workload."""
-    from oracle.solver import from_workload
-    w = workloads.Workload(WORKLOAD.name + f"-level{ORACLE_SAMPLE_LEVEL}", WORKLOAD.x0, WORKLOAD.y0, WORKLOAD.length,
-                           WORKLOAD.n_coarse, ORACLE_SAMPLE_LEVEL + 1, WORKLOAD.cx, WORKLOAD.cy, WORKLOAD.r,
-                           WORKLOAD.p, WORKLOAD.n_c)
-    h = from_workload(w)
-    ld = h.fine
-    lv = ld.lv
+    """Time the oracle (as it stands) on the benched configuration: one
+    smoothing step on the finest level of config1 (512^2, 680 065 DoFs); only
+    that level's LevelData is built (~20 s), then `steps` timed steps."""
+    from oracle.assemble import Params
+    from oracle.geometry import Circle, Level
+    from oracle.solver import LevelData
+    w = WORKLOAD
+    lv = Level(w.x0, w.y0, w.length, w.n_fine, Circle(w.cx, w.cy, w.r), w.p)
+    ld = LevelData(lv, Params())
     b = workloads.lattice_vector(w, 2)[lv.dof_nodes]
     x = workloads.lattice_vector(w, 1)[lv.dof_nodes]
     times = []
@@ -111,8 +111,9 @@ def oracle_sample(steps):
             times.append(time.perf_counter() - t0)
     sec = float(np.mean(times))
     return {"value": lv.n_dofs / sec, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle smoothing step on level {ORACLE_SAMPLE_LEVEL} ({lv.n}x{lv.n} cells, {lv.n_dofs} DoFs) "
-                      f"of the {WORKLOAD.name} hierarchy, mean of {len(times)} steps, numpy/scipy, one process, BLAS limited to 1 thread"}, sec
+            "sample": f"oracle smoothing step on the benched level ({lv.n}x{lv.n} cells, {lv.n_dofs} DoFs) of "
+                      f"{WORKLOAD.name}, mean of {len(times)} steps (setup excluded), numpy/scipy, one process, "
+                      f"BLAS limited to 1 thread"}, sec
 
 
 def run_reference(args, rank, world):
@@ -125,7 +126,8 @@ def run_reference(args, rank, world):
     out = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
            "steps": steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD.name, "sample_level": ORACLE_SAMPLE_LEVEL},
+           "config": {"workload": WORKLOAD.name, "cells_per_side": WORKLOAD.n_fine, "degree": WORKLOAD.p,
+                      "n_c": WORKLOAD.n_c, "level": "finest (the benched smoothing step)"},
            "cpu_baseline": cb,
            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -224,22 +226,33 @@ def main():
         cut_bytes = (float(np.sum(8 * m_all * m_all + 8 * (2 * p + 1) ** 2 + 24 * m_all)) +
                      8.0 * nb * nb * info.n_cut) / 4.0 / world
     per_step = {"cart_sweep": cart_ms, "cut_sweeps": sweeps_ms}
+    # the method's bytes of one cut colour step (library):
+    # A_j^{-1}, cut-cell element matrices, b_I, x read / written -- what the
+    # paper's local solver streams, independent of the patch maps we apply
+    cut_method = float(sum(info.cut_method_bytes[:4])) / 4.0 / world
     kernels = {
         "k_cart_fused_tma (4 Cartesian colours, one launch)": {
             "launches_per_step": 1, "avg_launch_ms": cart_ms, "bytes_per_launch": cart_bytes,
             "achieved_gbs": cart_bytes / (cart_ms * 1e-3) / 1e9},
         "k_cut_step7 (one cut colour)": {
-            "launches_per_step": n_cut_launch, "avg_launch_ms": cut_ms, "bytes_per_launch": cut_bytes,
-            "achieved_gbs": cut_bytes / (cut_ms * 1e-3) / 1e9}}
+            "launches_per_step": n_cut_launch, "avg_launch_ms": cut_ms, "bytes_per_launch": cut_method,
+            "achieved_gbs": cut_method / (cut_ms * 1e-3) / 1e9,
+            "implementation_bytes_per_launch": cut_bytes,
+            "implementation_gbs": cut_bytes / (cut_ms * 1e-3) / 1e9}}
     if per_step["cart_sweep"] >= per_step["cut_sweeps"]:
         dom, d_bytes, d_ms = "k_cart_fused_tma<P=%d> (fused Cartesian sweep)" % p, cart_bytes, cart_ms
     else:
-        dom, d_bytes, d_ms = ("k_cut_step7<P=%d> (cut colour step, patch maps)" % p if sum(info.cut_step_bytes[:4]) else "k_cut_step6<P=%d> (cut colour step)" % p), cut_bytes, cut_ms
+        dom, d_bytes, d_ms = "k_cut_step7<P=%d> (cut colour step, patch maps)" % p, cut_method, cut_ms
     achieved = d_bytes / (d_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(dom.split("<")[0])
+    # the whole smoothing step on the method's bytes: Cartesian sweep + 4 n_c cut steps
+    step_bytes = cart_bytes + n_cut_launch * cut_method
+    step_ms = total_ms / args.steps
+    step_roof = {"bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (step_ms * 1e-3) / 1e9,
+                 "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak}
 
     # fp64 tensor-core roofline of the fused Cartesian sweep (a dense contraction:
     # x_int = G [b_int; x_block] per patch, G of (2p-1)^2 x ((2p-1)^2 + (2p+1)^2)),
@@ -348,7 +361,8 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": d_bytes, "avg_launch_ms": d_ms,
-                         "step_share_ms": per_step},
+                         "bytes_basis": "method bytes (DESIGN.md (d)); traffic = ncu dram bytes per launch",
+                         "step_share_ms": per_step, "step": step_roof},
             "kernels": kernels,
             "roofline_fp64_cartesian": roof_fp64,
             "vcycle": {"ms": v_ms, "dofs_per_s": n_dofs / (v_ms * 1e-3)},

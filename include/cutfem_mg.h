@@ -87,6 +87,10 @@ typedef struct {
   int64_t cut_step_bytes[8];   /* algorithmic bytes of one cut colour step per colour with the
                                   precomputed patch maps (descriptor, map, gathered x and b,
                                   written x per patch); 0 without maps */
+  int64_t cut_method_bytes[8]; /* the method's bytes of one cut colour step per colour, whatever
+                                  the implementation: per patch
+                                  8 (m^2 [A_j^{-1}] + n_cut (p+1)^{2d} [cut-cell matrices]
+                                  + 3 m + nnz [b_I, x_I read, x_I written, coupled x_E]) */
 } cutfem_level_info;
 
 /* ---- setup ------------------------------------------------------------ */

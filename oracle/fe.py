@@ -37,10 +37,16 @@ def lagrange_polys(p):
     return tuple(polys)
 
 
+@lru_cache(maxsize=None)
+def lagrange_derivs(p, k):
+    """d^k L_i / dxi^k, i = 0..p, as polynomials (cached)."""
+    return tuple(L.deriv(k) if k > 0 else L for L in lagrange_polys(p))
+
+
 def basis_1d(p, x, k=0):
     """Matrix [i, q] = d^k L_i / dxi^k (x_q) on the reference interval [0,1]."""
     x = np.asarray(x, dtype=np.float64)
-    return np.array([L.deriv(k)(x) if k > 0 else L(x) for L in lagrange_polys(p)])
+    return np.array([D(x) for D in lagrange_derivs(p, k)])
 
 
 def gauss_legendre(n):

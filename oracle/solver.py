@@ -98,14 +98,27 @@ class LevelData:
         A_ng = assemble_matrix(lv, prm, with_ghost=False) if local == "no_ghost" else None
         for idx, pt in enumerate(self.patches):
             self.groups[(pt.kind, pt.colour)].append(idx)
-            I = pt.interior
-            if I.size == 0:
-                self.inv.append(np.zeros((0, 0)))
+        # A_j[r, c] = A_l[I_r, I_c] (l.156), gathered for all patches of one
+        # interior size at once (scipy element lookup), inverted as a stack
+        Asel = (A_ng if A_ng is not None else self.A).tocsr()
+        self.inv = [None] * len(self.patches)
+        by_m = {}
+        for idx, pt in enumerate(self.patches):
+            by_m.setdefault(pt.interior.size, []).append(idx)
+        for m, idxs in by_m.items():
+            if m == 0:
+                for idx in idxs:
+                    self.inv[idx] = np.zeros((0, 0))
                 continue
-            Aj = (A_ng if A_ng is not None else self.A)[I][:, I].toarray()
+            Is = np.stack([self.patches[idx].interior for idx in idxs])          # (k, m)
+            rows = np.repeat(Is, m, axis=1).ravel()                               # I_r, r-major
+            cols = np.tile(Is, (1, m)).ravel()                                    # I_c
+            Aj = np.asarray(Asel[rows, cols]).reshape(len(idxs), m, m)
             if self.bnd is not None:
-                Aj = Aj - self.bnd[idx][:, I].toarray()
-            self.inv.append(np.linalg.inv(Aj))
+                Aj = Aj - np.stack([self.bnd[idx][:, self.patches[idx].interior].toarray() for idx in idxs])
+            inv = np.linalg.inv(Aj)
+            for q, idx in enumerate(idxs):
+                self.inv[idx] = inv[q]
 
     def colour_step(self, x, b, kind, colour):
         """One colour of the multiplicative smoother: the residual b - A x is

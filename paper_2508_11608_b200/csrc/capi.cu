@@ -130,6 +130,7 @@ int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out) 
       out->n_cutp[c] = D.n_cutp[c];
     }
     for (int c = 0; c < 8; ++c) out->cut_step_bytes[c] = D.gmap ? D.cut_bytes[c] : 0;
+    for (int c = 0; c < 8; ++c) out->cut_method_bytes[c] = D.cut_method_bytes[c];
     out->n_vol_qp = D.n_vq;
     out->n_surf_qp = D.n_sq;
     out->h = D.a.h;

@@ -637,6 +637,25 @@ struct Problem {
 
 
 
+  // 3D: per patch 8 (m^2 + n_cut (p+1)^6 + (2p+1)^3 + 2 m): inverse, cut-cell
+  // matrices, the patch block of x (the residual's reach through the patch
+  // cells), b_I, written correction
+  void method_bytes3(LevelData& D, int ncp) {
+    const int p = prm.p, e6 = (int)std::pow(p + 1, 6), bs3 = (2 * p + 1) * (2 * p + 1) * (2 * p + 1);
+    std::vector<CutDesc3> hd(ncp);
+    CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc3) * ncp, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < 8; ++c) {
+      D.cut_method_bytes[c] = 0;
+      for (int k = D.cutp_off[c]; k < D.cutp_off[c + 1]; ++k) {
+        const CutDesc3& d = hd[k];
+        const long long m = __builtin_popcountll(d.mask[0]) + __builtin_popcountll(d.mask[1]);
+        int ncut = 0;
+        for (int q = 0; q < 8; ++q) ncut += d.cid[q] >= 0;
+        D.cut_method_bytes[c] += 8 * (m * m + (long long)ncut * e6 + bs3 + 2 * m);
+      }
+    }
+  }
+
   // (ent_node, col_off[0..4]: the interior nodes of the swept patches per
   // colour; desc/ncp: their descriptors)
   void build_copy_lists(LevelData& D, const int32_t* ent_node, const int64_t* col_off, const CutDesc* desc, int ncp) {
@@ -1740,6 +1759,7 @@ struct Problem {
                                                                             D.cutp_inv, (CutDesc3*)D.desc)));
         CF_LAUNCHED();
       }
+      if (ncp) method_bytes3(D, ncp);
       D.act_desc = D.desc;
       D.act_cart = D.cart_list;
       D.act_ent = D.ent_node;

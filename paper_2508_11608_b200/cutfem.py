@@ -43,7 +43,8 @@ class LevelInfo(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int), ("n", ctypes.c_int), ("nl", ctypes.c_int), ("ld", ctypes.c_int), ("n_dofs", ctypes.c_int64),
                 ("n_inside", ctypes.c_int), ("n_cut", ctypes.c_int), ("n_ghost_faces", ctypes.c_int),
                 ("n_cart", ctypes.c_int * 8), ("n_cutp", ctypes.c_int * 8), ("n_vol_qp", ctypes.c_int64),
-                ("n_surf_qp", ctypes.c_int64), ("h", ctypes.c_double), ("cut_step_bytes", ctypes.c_int64 * 8)]
+                ("n_surf_qp", ctypes.c_int64), ("h", ctypes.c_double), ("cut_step_bytes", ctypes.c_int64 * 8),
+                ("cut_method_bytes", ctypes.c_int64 * 8)]
 
 
 _P = ctypes.c_void_p

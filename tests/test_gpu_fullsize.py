@@ -1,9 +1,10 @@
 """Parity at BASELINE.json's full size (configs[1]: circle, Q2, 512x512,
-680065 DoFs) in the configuration bench.py times: structure bit-exact on the
-finest level (whole arrays, patch kinds on sampled vertices), the operator
-element by element, every colour step on sampled patches (the oracle computes
-those patches one by one), and properties of the smoothing step and the CG
-solve that hold at any size."""
+680065 DoFs) in the configuration bench.py times, against the oracle's whole
+hierarchy built in this session (~2 min of CPU): structure bit-exact on the
+finest level, the operator, the fused Cartesian sweep (k_cart_fused_tma, the
+benched kernel) and the cut sweeps (k_cut_step7) forward and reverse, whole
+smoothing steps forward and reverse, one V-cycle, all element by element, and
+the CG iteration count identical; plus sampled single colour steps."""
 import functools
 
 import numpy as np
@@ -12,7 +13,8 @@ import pytest
 import workloads
 from gpu_util import KIND, compact, rel_err
 from oracle.assemble import Params, assemble_matrix
-from oracle.geometry import CUTPATCH, Circle, Level, vertex_patch
+from oracle.geometry import CARTESIAN, CUTPATCH, Circle, Level, vertex_patch
+from oracle.solver import from_workload
 
 pytestmark = pytest.mark.gpu
 
@@ -21,9 +23,13 @@ TOL = 1e-10
 
 
 @functools.lru_cache(maxsize=1)
+def oracle_hierarchy():
+    return from_workload(W)
+
+
 def oracle_level():
-    lv = Level(W.x0, W.y0, W.length, W.n_fine, Circle(W.cx, W.cy, W.r), W.p)
-    return lv, assemble_matrix(lv, Params())
+    h = oracle_hierarchy()
+    return h.fine.lv, h.fine.A
 
 
 @functools.lru_cache(maxsize=1)
@@ -130,3 +136,78 @@ def test_cg_fullsize_true_residual():
     b = compact(lv, bl)
     res = np.linalg.norm(b - A @ compact(lv, g.to_host(x))) / np.linalg.norm(b)
     assert rel <= W.tol and res <= 1.01 * W.tol and it <= 12
+
+
+def _inputs(seed_x, seed_b):
+    lv, _ = oracle_level()
+    xl, bl = workloads.lattice_vector(W, seed_x), workloads.lattice_vector(W, seed_b)
+    return xl, bl, compact(lv, xl), compact(lv, bl)
+
+
+@pytest.mark.parametrize("reverse", [0, 1])
+def test_cartesian_sweep_fullsize(reverse):
+    # colour_step kind 2 = the fused Cartesian sweep of the bench (k_cart_fused_tma,
+    # all four colours in one launch) vs the oracle's four Cartesian colour steps
+    h = oracle_hierarchy()
+    g = gpu()
+    L = W.n_levels - 1
+    xl, bl, x0, b0 = _inputs(41, 42)
+    x = g.to_device(xl)
+    g.colour_step(L, 2, reverse, x, g.to_device(bl))
+    xo = x0.copy()
+    for c in (3, 2, 1, 0) if reverse else (0, 1, 2, 3):
+        h.fine.colour_step(xo, b0, CARTESIAN, c)
+    assert rel_err(compact(h.fine.lv, g.to_host(x)), xo) < TOL
+
+
+@pytest.mark.parametrize("reverse", [0, 1])
+def test_cut_sweeps_fullsize(reverse):
+    # colour_step kind 3 = the n_c sweeps over the cut colours (k_cut_step7 chain)
+    h = oracle_hierarchy()
+    g = gpu()
+    L = W.n_levels - 1
+    xl, bl, x0, b0 = _inputs(43, 44)
+    x = g.to_device(xl)
+    g.colour_step(L, 3, reverse, x, g.to_device(bl))
+    xo = x0.copy()
+    seq = [c for _ in range(W.n_c) for c in range(4)]
+    for c in seq[::-1] if reverse else seq:
+        h.fine.colour_step(xo, b0, CUTPATCH, c)
+    assert rel_err(compact(h.fine.lv, g.to_host(x)), xo) < TOL
+
+
+@pytest.mark.parametrize("reverse", [0, 1])
+def test_smooth_fullsize_vs_oracle(reverse):
+    # the benched call: one smoothing step S(x, b) on the 512^2 level
+    h = oracle_hierarchy()
+    g = gpu()
+    L = W.n_levels - 1
+    xl, bl, x0, b0 = _inputs(31, 32)
+    x = g.to_device(xl)
+    g.smooth(L, x, g.to_device(bl), bool(reverse))
+    xo = h.fine.smooth(x0.copy(), b0, W.n_c, reverse=bool(reverse))
+    assert rel_err(compact(h.fine.lv, g.to_host(x)), xo) < TOL
+
+
+def test_vcycle_fullsize_vs_oracle():
+    # one V-cycle from x = 0: 2 (L-1) smoothing steps, transfers and the exact
+    # coarse solve; tolerance 10 x TOL (R14)
+    h = oracle_hierarchy()
+    g = gpu()
+    _, bl, _, b0 = _inputs(31, 32)
+    x = g.zeros()
+    g.vcycle(x, g.to_device(bl))
+    assert rel_err(compact(h.fine.lv, g.to_host(x)), h.precondition(b0)) < 10 * TOL
+
+
+def test_cg_fullsize_iterations_equal_oracle():
+    # north_star: identical CG iteration counts at full size
+    h = oracle_hierarchy()
+    g = gpu()
+    _, bl, _, b0 = _inputs(31, 32)
+    x = g.zeros()
+    it, rel = g.solve_cg_mg(x, g.to_device(bl), tol=W.tol, max_it=100)
+    xo, ito, hist = h.solve_cg(b0, W.tol)
+    assert it == ito, (it, ito)
+    assert rel <= W.tol and hist[-1] <= W.tol * hist[0]
+    assert rel_err(compact(h.fine.lv, g.to_host(x)), xo) < 1e-7
