@@ -69,6 +69,12 @@ typedef struct {
                            from the cut quadrature at setup, 1 = quadrature on the fly */
   int dim;              /* 2 (circle, default when 0) or 3 (sphere; degree 1..2) */
   double z0, cz;        /* 3D: box corner z and sphere centre z (the box is a cube of side length) */
+  int domain;           /* 0: the circle / sphere level set above (unfitted, cut cells, Nitsche +
+                           ghost penalty); 1: FITTED box -- Omega = the open background box itself,
+                           homogeneous Dirichlet condition imposed strongly (no DoF on the box
+                           boundary), every patch at an interior vertex is Cartesian (the paper's
+                           "Square" baseline, P Table 1 / Fig. 2; BASELINE configs[4]); cx, cy, cz,
+                           r are ignored */
 } cutfem_params;
 
 /* Per-level sizes and counts. */

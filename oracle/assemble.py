@@ -136,8 +136,9 @@ def assemble_matrix(lv, prm, with_ghost=True, with_cells=True):
             rows.append(np.repeat(d, d.size)); cols.append(np.tile(d, d.size)); vals.append(M.ravel())
     if not rows:
         return sp.csr_matrix((lv.n_dofs, lv.n_dofs))
-    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
-                      shape=(lv.n_dofs, lv.n_dofs)).tocsr()
+    R, C, V = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    keep = (R >= 0) & (C >= 0)   # nodes without a DoF (fitted boundary: u = 0 strongly) drop out
+    A = sp.coo_matrix((V[keep], (R[keep], C[keep])), shape=(lv.n_dofs, lv.n_dofs)).tocsr()
     A.sum_duplicates()
     return A
 
@@ -160,14 +161,15 @@ def assemble_rhs(lv, prm, f, g):
             else:
                 vp, vw, sp_, sw, sn = cut_cell_rules(xl, xh, yl, yh, lv.circle, prm.n_q)
             d = cell_dofs(lv, i, j)
+            ok = d >= 0   # (fitted boundary nodes carry no DoF / test function)
             if len(vw):
                 v, _, _ = eval_basis(lv, i, j, vp)
-                b[d] += v @ (vw * f(vp[:, 0], vp[:, 1]))
+                b[d[ok]] += (v @ (vw * f(vp[:, 0], vp[:, 1])))[ok]
             if len(sw):
                 v, sx, sy = eval_basis(lv, i, j, sp_)
                 dn = sx * sn[:, 0] + sy * sn[:, 1]
                 gv = sw * g(sp_[:, 0], sp_[:, 1])
-                b[d] += -(dn @ gv) + (prm.gamma_D / lv.h) * (v @ gv)
+                b[d[ok]] += (-(dn @ gv) + (prm.gamma_D / lv.h) * (v @ gv))[ok]
     return b
 
 
@@ -187,6 +189,7 @@ def l2_error(lv, u, exact, n_q):
             if not len(vw):
                 continue
             v, _, _ = eval_basis(lv, i, j, vp)
-            uh = u[cell_dofs(lv, i, j)] @ v
+            d = cell_dofs(lv, i, j)
+            uh = np.where(d >= 0, u[np.maximum(d, 0)], 0.0) @ v
             err += float(np.sum(vw * (uh - exact(vp[:, 0], vp[:, 1])) ** 2))
     return np.sqrt(err)

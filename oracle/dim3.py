@@ -22,7 +22,7 @@ import scipy.sparse as sp
 
 from .assemble import Params
 from .fe import basis_1d, gauss_legendre, gauss_lobatto_nodes
-from .geometry import CARTESIAN, CUT, CUTPATCH, INSIDE, OUTSIDE, Patch
+from .geometry import CARTESIAN, CUT, CUTPATCH, INSIDE, OUTSIDE, Patch, is_fitted
 
 
 @dataclass(frozen=True)
@@ -86,6 +86,8 @@ def classify3(lv):
     to the closed cell box, summed in the order x, y, z."""
     s = lv.sphere
     n = lv.n
+    if is_fitted(s):
+        return np.full((n, n, n), INSIDE, dtype=np.int8)
     idx = np.arange(n, dtype=np.float64)
     out = np.full((n, n, n), CUT, dtype=np.int8)
     q, f = [], []
@@ -111,6 +113,8 @@ def node_mask3(lv):
         for ky in range(p + 1):
             for kx in range(p + 1):
                 m[kz:kz + n * p:p, ky:ky + n * p:p, kx:kx + n * p:p] |= act
+    if is_fitted(lv.sphere):   # strong Dirichlet: no DoF on the box boundary
+        m[0], m[-1], m[:, 0], m[:, -1], m[:, :, 0], m[:, :, -1] = (False,) * 6
     return m
 
 
@@ -335,8 +339,9 @@ def assemble_matrix3(lv, prm, with_ghost=True, with_cells=True):
         for axis, i, j, k in ghost_faces3(lv):
             d, M = ghost_face_matrix3(lv, axis, i, j, k, prm)
             rows.append(np.repeat(d, d.size)); cols.append(np.tile(d, d.size)); vals.append(M.ravel())
-    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
-                      shape=(lv.n_dofs, lv.n_dofs)).tocsr()
+    R, C, V = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    keep = (R >= 0) & (C >= 0)   # nodes without a DoF (fitted boundary: u = 0 strongly) drop out
+    A = sp.coo_matrix((V[keep], (R[keep], C[keep])), shape=(lv.n_dofs, lv.n_dofs)).tocsr()
     A.sum_duplicates()
     return A
 
@@ -354,6 +359,8 @@ def vertex_patch3(lv, I, J, K):
     cells = [c for c in block if lv.active(*c)]
     if not cells:
         return None
+    if is_fitted(lv.sphere) and not (0 < I < lv.n and 0 < J < lv.n and 0 < K < lv.n):
+        return None   # vertices contained in the open box (P l.143)
     pt = Patch()
     pt.I, pt.J = I, J
     pt.K = K
@@ -418,7 +425,7 @@ def prolongation_matrix3(coarse, fine):
             for ny in range(p + 1):
                 for nx in range(p + 1):
                     wgt = bx[nx] * by[ny] * bz[nz]
-                    if wgt != 0.0:
-                        ic = coarse.dof_index[((C[2] * p + nz) * nlc + C[1] * p + ny) * nlc + C[0] * p + nx]
+                    ic = coarse.dof_index[((C[2] * p + nz) * nlc + C[1] * p + ny) * nlc + C[0] * p + nx]
+                    if wgt != 0.0 and ic >= 0:   # (ic < 0: fitted boundary node, coefficient 0)
                         rows.append(jf); cols.append(int(ic)); vals.append(wgt)
     return sp.csr_matrix((vals, (rows, cols)), shape=(fine.n_dofs, coarse.n_dofs))

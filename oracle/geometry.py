@@ -29,6 +29,22 @@ class Circle:
     r: float
 
 
+@dataclass(frozen=True)
+class FittedBox:
+    """Fitted domain: Omega = the open background box itself (its boundary on
+    mesh lines), homogeneous Dirichlet condition imposed strongly (nodes on
+    the box boundary carry no DoF).  The paper's "Square" baseline (PAPER.md
+    Table 1 l.219-238, Fig. 2 square curves l.388-399) and BASELINE.json
+    configs[4]'s fitted cube: every cell is Inside, there are no cut cells,
+    ghost faces or Nitsche terms, and patches sit at the vertices contained
+    in Omega (P l.143 read literally: the interior vertices), all Cartesian.
+    Used for 2D and 3D levels."""
+
+
+def is_fitted(dom):
+    return isinstance(dom, FittedBox)
+
+
 class Level:
     """One level M_l of the nested Cartesian hierarchy with its geometry."""
 
@@ -80,6 +96,8 @@ def classify_cells(lv):
     x0 + i*h and x0 + (i+1)*h (product rounded, then sum)."""
     c = lv.circle
     n = lv.n
+    if is_fitted(c):
+        return np.full((n, n), INSIDE, dtype=np.int8)
     r2 = c.r * c.r
     idx = np.arange(n, dtype=np.float64)
     xl, xh = lv.x0 + idx * lv.h, lv.x0 + (idx + 1.0) * lv.h
@@ -106,6 +124,8 @@ def node_mask(lv):
     for ky in range(p + 1):
         for kx in range(p + 1):
             m[ky:ky + n * p:p, kx:kx + n * p:p] |= act
+    if is_fitted(lv.circle):   # strong Dirichlet: no DoF on the box boundary
+        m[0, :] = m[-1, :] = m[:, 0] = m[:, -1] = False
     return m
 
 
@@ -137,6 +157,8 @@ def vertex_patch(lv, I, J, vertices="active"):
     cells = [c for c in block if lv.active(*c)]
     if not cells:
         return None
+    if is_fitted(lv.circle) and not (0 < I < lv.n and 0 < J < lv.n):
+        return None   # vertices contained in the open box (P l.143)
     if vertices == "inside":
         X = lv.x0 + I * lv.h - lv.circle.cx
         Y = lv.y0 + J * lv.h - lv.circle.cy

@@ -295,11 +295,14 @@ def fractional_iterations(n_it, r_final, r_0):
 
 
 def from_workload(w, prm=None, **kw):
-    """Hierarchy for a workloads.Workload description (2D circle or 3D sphere)."""
+    """Hierarchy for a workloads.Workload description (2D circle or 3D sphere,
+    or the fitted box, oracle.geometry.FittedBox)."""
+    from .geometry import FittedBox
+    fitted = getattr(w, "domain", "cut") == "fitted"
     if getattr(w, "dim", 2) == 3:
         from .dim3 import Level3, Sphere
-        sph = Sphere(w.cx, w.cy, w.cz, w.r)
-        levels = [Level3(w.x0, w.y0, w.z0, w.length, w.n_coarse * 2 ** l, sph, w.p) for l in range(w.n_levels)]
+        dom = FittedBox() if fitted else Sphere(w.cx, w.cy, w.cz, w.r)
+        levels = [Level3(w.x0, w.y0, w.z0, w.length, w.n_coarse * 2 ** l, dom, w.p) for l in range(w.n_levels)]
         return Hierarchy(None, None, None, None, None, None, w.p, prm=prm, n_c=w.n_c, levels=levels, **kw)
-    return Hierarchy(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, Circle(w.cx, w.cy, w.r), w.p,
-                     prm=prm, n_c=w.n_c, **kw)
+    dom = FittedBox() if fitted else Circle(w.cx, w.cy, w.r)
+    return Hierarchy(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, dom, w.p, prm=prm, n_c=w.n_c, **kw)

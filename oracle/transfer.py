@@ -38,7 +38,7 @@ def prolongation_matrix(coarse, fine):
         for n in range(p + 1):
             for m in range(p + 1):
                 wgt = bx[m] * by[n]
-                if wgt != 0.0:
-                    ic = coarse.dof_index[(J * p + n) * coarse.nl + (I * p + m)]
+                ic = coarse.dof_index[(J * p + n) * coarse.nl + (I * p + m)]
+                if wgt != 0.0 and ic >= 0:   # (ic < 0: fitted boundary node, coefficient 0)
                     rows.append(jf); cols.append(int(ic)); vals.append(wgt)
     return sp.csr_matrix((vals, (rows, cols)), shape=(fine.n_dofs, coarse.n_dofs))

@@ -62,7 +62,9 @@ int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* ou
     cf::require(prm->n_coarse >= 1 && prm->n_levels >= 1 && prm->n_levels <= 16, cf::ERR_ARG, "bad level counts");
     cf::require(((int64_t)prm->n_coarse << (prm->n_levels - 1)) * prm->degree < 60000, cf::ERR_SIZE,
                 "finest lattice too large");
-    cf::require(prm->length > 0 && prm->r > 0, cf::ERR_ARG, "box length and radius must be positive");
+    cf::require(prm->domain == 0 || prm->domain == 1, cf::ERR_ARG, "domain must be 0 (level set) or 1 (fitted box)");
+    cf::require(prm->length > 0 && (prm->domain == 1 || prm->r > 0), cf::ERR_ARG,
+                "box length and radius must be positive");
     cf::require(prm->n_q >= 0 && prm->n_q <= CF_MAXNQ, cf::ERR_ARG, "n_q must be 0..12");
     cf::require(prm->n_c >= 1, cf::ERR_ARG, "n_c must be >= 1");
     *out = nullptr;
@@ -88,6 +90,7 @@ int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* ou
     P.symmetric = prm->symmetric;
     cf::require(prm->cut_mode == 0 || prm->cut_mode == 1, cf::ERR_ARG, "cut_mode must be 0 or 1");
     P.cut_mode = prm->cut_mode;
+    P.domain = prm->domain;
     use_stream(pb, stream);
     try {
       pb->p.setup_mesh();
@@ -142,7 +145,7 @@ int cutfem_apply_operator(cutfem_problem pb, int level, const double* x, double*
     check_level(pb, level);
     cf::require(x && y && x != y, cf::ERR_ARG, "x, y must be distinct non-null device pointers");
     use_stream(pb, stream);
-    pb->p.apply(level, x, y, nullptr);
+    pb->p.apply_entry(level, x, y);
   });
 }
 
@@ -152,7 +155,10 @@ int cutfem_smooth(cutfem_problem pb, int level, double* x, const double* b, int 
     check_level(pb, level);
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
-    pb->p.graphed(1, x, b, level * 2 + (reverse ? 1 : 0), [&]() { pb->p.smooth(level, x, b, reverse); });
+    pb->p.graphed(1, x, b, level * 2 + (reverse ? 1 : 0), [&]() {
+      pb->p.zero_boundary(level, x);
+      pb->p.smooth(level, x, b, reverse);
+    });
   });
 }
 
@@ -165,6 +171,7 @@ int cutfem_colour_step(cutfem_problem pb, int level, int kind, int colour, doubl
                 "a partitioned level only exposes the whole sweeps (kind 2, 3)");
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
+    pb->p.zero_boundary(level, x);
     if (pb->p.prm.dim == 3) {
       cf::require(kind <= 1 && colour < 8, cf::ERR_ARG, "3D colour step: kind 0/1, colour 0..7");
       if (kind == 0) pb->p.cart_step3(level, colour, x, b);
@@ -288,7 +295,10 @@ int cutfem_vcycle(cutfem_problem pb, double* x, const double* b, void* stream) {
     cf::require(x && b && (const double*)x != b, cf::ERR_ARG, "x, b must be distinct non-null device pointers");
     use_stream(pb, stream);
     const int L = pb->p.prm.n_levels - 1;
-    pb->p.graphed(2, x, b, 0, [&]() { pb->p.vcycle(L, x, b); });
+    pb->p.graphed(2, x, b, 0, [&]() {
+      pb->p.zero_boundary(L, x);
+      pb->p.vcycle(L, x, b);
+    });
   });
 }
 
@@ -324,7 +334,10 @@ int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const doubl
     CF_CUDA(cudaMemcpyAsync(pb->p.hb, b_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
     double* dx = pb->p.hx;
     const double* db = pb->p.hb;
-    pb->p.graphed(1, dx, db, level * 2 + (reverse ? 1 : 0), [&]() { pb->p.smooth(level, dx, db, reverse); });
+    pb->p.graphed(1, dx, db, level * 2 + (reverse ? 1 : 0), [&]() {
+      pb->p.zero_boundary(level, dx);
+      pb->p.smooth(level, dx, db, reverse);
+    });
     CF_CUDA(cudaMemcpyAsync(x_host, pb->p.hx, bytes, cudaMemcpyDeviceToHost, pb->p.st));
     pb->p.sync();
   });

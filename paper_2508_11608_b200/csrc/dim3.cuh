@@ -30,6 +30,10 @@ __global__ void k_classify3(LevelArgs L, int8_t* ct) {
   const int n = L.n;
   if (c >= (int64_t)n * n * n) return;
   const int i = c % n, j = (c / n) % n, k = c / ((int64_t)n * n);
+  if (L.fitted) {   // fitted box: every cell is Inside
+    ct[c] = INSIDE;
+    return;
+  }
   double lo[3], hi[3];
   cell_bounds3(L, i, j, k, lo, hi);
   const double cc[3] = {L.cx, L.cy, L.cz};
@@ -61,6 +65,7 @@ __global__ void k_mask3(LevelArgs L, const int8_t* ct, uint8_t* mask, int* count
       for (int j = j0; j <= j1; ++j)
         for (int i = i0; i <= i1; ++i)
           if (cell_kind3(L, i, j, k) != OUTSIDE) m = 1;
+    if (L.fitted && (a == 0 || b == 0 || c == 0 || a == nl - 1 || b == nl - 1 || c == nl - 1)) m = 0;
   }
   mask[o] = m;
   if (m) atomicAdd(count, 1);
@@ -547,7 +552,7 @@ __global__ void k_vertex_kind3(LevelArgs L, uint8_t* vk) {
         ninside += k == INSIDE;
       }
   uint8_t r = V_NONE;
-  if (nact > 0) {
+  if (nact > 0 && !(L.fitted && (I == 0 || J == 0 || K == 0 || I == n || J == n || K == n))) {
     bool cart = ninside == 8;
     for (int axis = 0; axis < 3 && cart; ++axis)
       for (int side = 0; side < 2 && cart; ++side)

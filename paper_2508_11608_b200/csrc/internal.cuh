@@ -58,6 +58,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 struct LevelArgs {
   int n, p, nl, ld;
   int dim;                           // 2 or 3
+  int fitted;                        // fitted box: every cell Inside, no DoF on the box boundary
   double h, x0, y0, z0;
   double cx, cy, cz, r;
   double gDh;                        // gamma_D / h
@@ -180,6 +181,7 @@ struct LevelData {
 struct Params {
   double x0, y0, z0, length, cx, cy, cz, r, gamma_D, gamma_k[CF_MAXP];
   int dim, n_coarse, n_levels, p, sigma, n_q, n_c, symmetric, cut_mode;
+  int domain;   // 0: circle / sphere level set; 1: fitted box (strong Dirichlet on its boundary)
 };
 
 // launch accounting for the bench's gpu_launches claim

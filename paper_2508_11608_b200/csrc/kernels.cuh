@@ -710,6 +710,29 @@ __global__ void k_cg_direction(double* p, const double* z, const double* sc, int
 }
 
 // dst = mask ? src : 0
+// fitted box: zero the lattice nodes on the box boundary (no DoF, u = 0
+// strongly), which the cell kernels read as part of their cells: 2D the 4
+// boundary lines (4 nl threads), 3D the 6 boundary faces (6 nl^2 threads)
+__global__ void k_zero_boundary(LevelArgs L, double* v) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int nl = L.nl, ld = L.ld;
+  if (L.dim == 3) {
+    if (t >= 6 * (int64_t)nl * nl) return;
+    const int f = (int)(t / ((int64_t)nl * nl)), r = (int)(t % ((int64_t)nl * nl)), u = r % nl, w = r / nl;
+    const int e = (f & 1) ? nl - 1 : 0;
+    int a, b, c;
+    if (f < 2) a = e, b = u, c = w;
+    else if (f < 4) a = u, b = e, c = w;
+    else a = u, b = w, c = e;
+    v[((size_t)c * nl + b) * ld + a] = 0.0;
+    return;
+  }
+  if (t >= 4 * (int64_t)nl) return;
+  const int f = (int)(t / nl), u = (int)(t % nl), e = (f & 1) ? nl - 1 : 0;
+  const int a = f < 2 ? e : u, b = f < 2 ? u : e;
+  v[(size_t)b * ld + a] = 0.0;
+}
+
 __global__ void k_masked_copy(double* dst, const double* src, const uint8_t* mask, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = mask[i] ? src[i] : 0.0;

@@ -242,6 +242,7 @@ struct Problem {
       std::memset(&L, 0, sizeof(L));
       L.n = prm.n_coarse << l;
       L.p = p;
+      L.fitted = prm.domain == 1;
       L.nl = L.n * p + 1;
       L.ld = (L.nl + 1) & ~1;
       L.h = prm.length / L.n;
@@ -1051,6 +1052,31 @@ struct Problem {
   }
 
   // ------------------------------------------------------------- hot path
+  // fitted box: the cell kernels read the boundary nodes of their cells, so x
+  // must be 0 there (the API ignores non-DoF entries on input): zeroed in place
+  // at the public entry points (smooth, vcycle, colour_step); a no-op for the
+  // level-set domain, whose kernels never read a non-DoF node
+  void zero_boundary(int l, double* x) {
+    if (prm.domain != 1) return;
+    const LevelArgs& L = lv[l].a;
+    const int64_t n = prm.dim == 3 ? 6 * (int64_t)L.nl * L.nl : 4 * (int64_t)L.nl;
+    launch(k_zero_boundary, dim3(ceil_div(n, 256)), dim3(256), 0, L, x);
+    CF_LAUNCHED();
+  }
+  // public operator: x is const, so in fitted mode it is copied with the DoF
+  // mask into the level's residual workspace first
+  void apply_entry(int l, const double* x, double* y) {
+    if (prm.domain == 1) {
+      LevelData& D = lv[l];
+      const int64_t nv = vsize(l);
+      k_masked_copy<<<4 * 148, 256, 0, st>>>(D.r, x, D.mask, nv);
+      CF_LAUNCHED();
+      apply(l, D.r, y, nullptr);
+      return;
+    }
+    apply(l, x, y, nullptr);
+  }
+
   void apply(int l, const double* x, double* y, const double* b) {
     if (prm.dim == 3) {
       apply3(l, x, y, b);
@@ -1552,6 +1578,7 @@ struct Problem {
       L.dim = 3;
       L.n = prm.n_coarse << l;
       L.p = p;
+      L.fitted = prm.domain == 1;
       L.nl = L.n * p + 1;
       L.ld = (L.nl + 1) & ~1;
       L.h = prm.length / L.n;

@@ -21,6 +21,10 @@ __device__ __forceinline__ void cell_bounds(const LevelArgs& L, int i, int j, do
 __global__ void k_classify(LevelArgs L, int8_t* ct) {
   int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
   if (i >= L.n || j >= L.n) return;
+  if (L.fitted) {   // fitted box: Omega is the background box, every cell is Inside
+    ct[j * L.n + i] = INSIDE;
+    return;
+  }
   double xl, xh, yl, yh;
   cell_bounds(L, i, j, xl, xh, yl, yh);
   double r2 = __dmul_rn(L.r, L.r);
@@ -55,6 +59,8 @@ __global__ void k_mask(LevelArgs L, const int8_t* ct, uint8_t* mask, int* count)
     for (int j = j0; j <= j1; ++j)
       for (int i = i0; i <= i1; ++i)
         if (cell_active(L, ct, i, j)) m = 1;
+    // fitted box: strong Dirichlet, no DoF on the box boundary
+    if (L.fitted && (a == 0 || b == 0 || a == L.nl - 1 || b == L.nl - 1)) m = 0;
   }
   mask[(size_t)b * L.ld + a] = m;
   if (m) atomicAdd(count, 1);
@@ -242,7 +248,8 @@ __global__ void k_vertex_kind(LevelArgs L, const int8_t* ct, uint8_t* vk) {
       ninside += k == INSIDE;
     }
   uint8_t v = V_NONE;
-  if (nact > 0) {
+  // fitted box: patches at the vertices contained in the open box (P l.143)
+  if (nact > 0 && !(L.fitted && (I == 0 || J == 0 || I == n || J == n))) {
     bool cart = ninside == 4;
     const int nb[8][2] = {{-2, -1}, {-2, 0}, {1, -1}, {1, 0}, {-1, -2}, {0, -2}, {-1, 1}, {0, 1}};
     for (int q = 0; q < 8 && cart; ++q)

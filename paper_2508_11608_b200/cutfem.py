@@ -36,7 +36,7 @@ class Params(ctypes.Structure):
                 ("gamma_D", ctypes.c_double), ("gamma_k", ctypes.c_double * 4), ("sigma", ctypes.c_int),
                 ("n_q", ctypes.c_int), ("n_c", ctypes.c_int), ("symmetric", ctypes.c_int),
                 ("cut_mode", ctypes.c_int), ("dim", ctypes.c_int), ("z0", ctypes.c_double),
-                ("cz", ctypes.c_double)]
+                ("cz", ctypes.c_double), ("domain", ctypes.c_int)]
 
 
 class LevelInfo(ctypes.Structure):
@@ -115,10 +115,10 @@ def launch_count():
 
 
 def make_params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D=0.0, gamma_k=(-1, -1, -1, -1),
-                sigma=-1, n_q=0, n_c=2, symmetric=1, cut_mode=0, dim=2, z0=0.0, cz=0.0):
+                sigma=-1, n_q=0, n_c=2, symmetric=1, cut_mode=0, dim=2, z0=0.0, cz=0.0, domain=0):
     g = (ctypes.c_double * 4)(*[float(v) for v in (list(gamma_k) + [-1] * 4)[:4]])
     return Params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D, g, sigma, n_q, n_c, symmetric,
-                  cut_mode, dim, z0, cz)
+                  cut_mode, dim, z0, cz, domain)
 
 
 NCCL_ID_BYTES = 128
@@ -195,7 +195,8 @@ class Problem:
     @classmethod
     def from_workload(cls, w, stream=None, **kw):
         prm = make_params(w.x0, w.y0, w.length, w.n_coarse, w.n_levels, w.p, w.cx, w.cy, w.r, n_c=w.n_c,
-                          dim=getattr(w, "dim", 2), z0=getattr(w, "z0", 0.0), cz=getattr(w, "cz", 0.0), **kw)
+                          dim=getattr(w, "dim", 2), z0=getattr(w, "z0", 0.0), cz=getattr(w, "cz", 0.0),
+                          domain=1 if getattr(w, "domain", "cut") == "fitted" else 0, **kw)
         return cls(prm, stream)
 
     def build_patches(self, stream=None):
