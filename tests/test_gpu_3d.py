@@ -125,3 +125,30 @@ def test_alternative_cut_kernels_3d(env, monkeypatch):
         xo = xl[dn].copy()
         ld.colour_step(xo, bl[dn], KIND[1], c)
         assert rel_err(g.to_host(x, l)[dn], xo) < TOL, c
+
+
+def test_sphere64_fullsize_vs_oracle_goldens():
+    # 3D at 64^3 (Q2, 910 701 DoFs; the multi-wave level of config2's
+    # hierarchy, TMA cut-patch windows): forward / reverse smoothing step,
+    # V-cycle and CG count vs the oracle's outputs written by
+    # scripts/make_fullsize_goldens.py (oracle only) on a fixed subset of DoFs
+    # (every DoF within 3 h of the sphere + every 11th other one)
+    import os
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "fullsize_sphere64.npz"))
+    w = workloads.sphere("sphere-Q2-64^3", 2, 6, 2)
+    assert str(d["workload"]) == w.name
+    g = gpu(w)
+    L = w.n_levels - 1
+    assert g.level_info(L).n_dofs == int(d["n_dofs"])
+    nodes = np.flatnonzero(g.dof_mask(L).ravel())[d["idx"]]
+    xl, bl = rnd(w, 31, None), rnd(w, 32, None)
+    for rev, key in ((False, "y_fwd"), (True, "y_rev")):
+        x = g.to_device(xl)
+        g.smooth(L, x, g.to_device(bl), rev)
+        assert rel_err(g.to_host(x)[nodes], d[key]) < TOL, key
+    v = g.zeros()
+    g.vcycle(v, g.to_device(bl))
+    assert rel_err(g.to_host(v)[nodes], d["v"]) < 10 * TOL
+    xs = g.zeros()
+    it, rel = g.solve_cg_mg(xs, g.to_device(bl), tol=float(d["tol"]), max_it=100)
+    assert it == int(d["cg_it"]) and rel <= float(d["tol"])
