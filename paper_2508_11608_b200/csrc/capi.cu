@@ -58,7 +58,7 @@ int cutfem_setup_mesh(const cutfem_params* prm, void* stream, cutfem_problem* ou
     cf::require(prm != nullptr && out != nullptr, cf::ERR_ARG, "null argument");
     cf::require(prm->degree >= 1 && prm->degree <= CF_MAXP, cf::ERR_ARG, "degree must be 1..4");
     cf::require(prm->dim == 0 || prm->dim == 2 || prm->dim == 3, cf::ERR_ARG, "dim must be 2 or 3");
-    cf::require(prm->dim != 3 || prm->degree <= 2, cf::ERR_ARG, "3D supports degree 1..2");
+    cf::require(prm->dim != 3 || prm->degree <= 3, cf::ERR_ARG, "3D supports degree 1..3");
     cf::require(prm->n_coarse >= 1 && prm->n_levels >= 1 && prm->n_levels <= 16, cf::ERR_ARG, "bad level counts");
     cf::require(((int64_t)prm->n_coarse << (prm->n_levels - 1)) * prm->degree < 60000, cf::ERR_SIZE,
                 "finest lattice too large");

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(128) k_cut_elem3(LevelArgs L, double* E) {
   cut_cell_warp3<P>(L, cid, sX[w], acc);
 #pragma unroll
   for (int t = 0; t < NB; ++t)
-    if (lane == t) E[((int64_t)cid * NB + t) * NB + col] = acc[t];
+    if (lane == (t & 31)) E[((int64_t)cid * NB + t) * NB + col] = acc[t];   // (all lanes hold the sums; NB > 32 for Q3)
 }
 
 // ---- element pieces shared by the patch kernels and the operator ------------
@@ -662,15 +662,21 @@ template <int P>
 struct CartMMA3 {
   static constexpr int NE = 2 * P + 1, NI = 2 * P - 1, NINT = NI * NI * NI, NEXT = NE * NE * NE, K = NINT + NEXT;
   static constexpr int KS = (K + 3) / 4, COLS = 4 * KS, MF = NINT / 8, RR = NINT - 8 * MF, ROWS = 8 * ((NINT + 7) / 8);
+  // Q3 (G = 128 x 468 doubles, 468 KB): G is staged through shared memory in
+  // chunks of KC k-steps shared by the CTA's NW warps (one L2 read of G per
+  // CTA instead of per warp); Q1 / Q2 read G (<= 38 KB) through L1
+  static constexpr bool STAGE = P >= 3;
+  static constexpr int NW = STAGE ? 8 : 4, KC = 8, GS = 4 * KC + 4;   // GS: padded row stride (2 wavefronts)
 };
 
 template <int P>
-__global__ void __launch_bounds__(128) k_cart_colour3(LevelArgs L, const int* plist, int np, const double* G,
-                                                     double* x, const double* b) {
+__global__ void __launch_bounds__(32 * CartMMA3<P>::NW) k_cart_colour3(LevelArgs L, const int* plist, int np,
+                                                                      const double* G, double* x, const double* b) {
   using C = CartMMA3<P>;
-  constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS, MF = C::MF, RR = C::RR;
+  constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS, MF = C::MF, RR = C::RR, NW = C::NW;
   __shared__ int koff[C::COLS];
   __shared__ int roff[NINT];
+  __shared__ double gs[C::STAGE ? C::ROWS * C::GS : 1];
   const int tid = threadIdx.x, lane = tid & 31, nl = L.nl, ld = L.ld;
   pdl_trigger();
   for (int k = tid; k < C::COLS; k += blockDim.x) {
@@ -689,8 +695,8 @@ __global__ void __launch_bounds__(128) k_cart_colour3(LevelArgs L, const int* pl
     roff[r] = ((ic + 1) * nl + ib + 1) * ld + ia + 1;
   }
   __syncthreads();
-  const int g = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
-  if (8 * g >= np) return;
+  const int g = blockIdx.x * NW + (tid >> 5);
+  if (!C::STAGE && 8 * g >= np) return;   // (staged: every warp takes part in the chunk loads)
   const int pq = 8 * g + (lane >> 2), nv = L.n + 1;
   const double hinv = 1.0 / L.h;   // G holds the h = 1 map; A scales with h in 3D
   int64_t base = -1;
@@ -706,15 +712,39 @@ __global__ void __launch_bounds__(128) k_cart_colour3(LevelArgs L, const int* pl
   for (int mt = 0; mt < MF; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
 #pragma unroll
   for (int rr = 0; rr < RR; ++rr) rs[rr] = 0.0;
-  for (int ks = 0; ks < KS; ++ks) {
-    const int ko = koff[4 * ks + (lane & 3)];
-    double v = 0.0;
-    if (base >= 0 && ko >= 0) v = ko >= (1 << 30) ? b[base + ko - (1 << 30)] * hinv : x[base + ko];
+  if constexpr (C::STAGE) {
+    for (int ks0 = 0; ks0 < KS; ks0 += C::KC) {
+      const int nk = KS - ks0 < C::KC ? KS - ks0 : C::KC;
+      __syncthreads();
+      for (int e = tid; e < C::ROWS * 4 * nk; e += blockDim.x) {
+        const int r = e / (4 * nk), c = e - r * 4 * nk;
+        gs[r * C::GS + c] = __ldg(G + r * C::COLS + 4 * ks0 + c);
+      }
+      __syncthreads();
+      for (int kk = 0; kk < nk; ++kk) {
+        const int ks = ks0 + kk;
+        const int ko = koff[4 * ks + (lane & 3)];
+        double v = 0.0;
+        if (base >= 0 && ko >= 0) v = ko >= (1 << 30) ? b[base + ko - (1 << 30)] * hinv : x[base + ko];
 #pragma unroll
-    for (int mt = 0; mt < MF; ++mt)
-      dmma(__ldg(G + (8 * mt + (lane >> 2)) * C::COLS + 4 * ks + (lane & 3)), v, acc[mt][0], acc[mt][1]);
+        for (int mt = 0; mt < MF; ++mt)
+          dmma(gs[(8 * mt + (lane >> 2)) * C::GS + 4 * kk + (lane & 3)], v, acc[mt][0], acc[mt][1]);
 #pragma unroll
-    for (int rr = 0; rr < RR; ++rr) rs[rr] = fma(__ldg(G + (8 * MF + rr) * C::COLS + 4 * ks + (lane & 3)), v, rs[rr]);
+        for (int rr = 0; rr < RR; ++rr) rs[rr] = fma(gs[(8 * MF + rr) * C::GS + 4 * kk + (lane & 3)], v, rs[rr]);
+      }
+    }
+    if (8 * g >= np) return;
+  } else {
+    for (int ks = 0; ks < KS; ++ks) {
+      const int ko = koff[4 * ks + (lane & 3)];
+      double v = 0.0;
+      if (base >= 0 && ko >= 0) v = ko >= (1 << 30) ? b[base + ko - (1 << 30)] * hinv : x[base + ko];
+#pragma unroll
+      for (int mt = 0; mt < MF; ++mt)
+        dmma(__ldg(G + (8 * mt + (lane >> 2)) * C::COLS + 4 * ks + (lane & 3)), v, acc[mt][0], acc[mt][1]);
+#pragma unroll
+      for (int rr = 0; rr < RR; ++rr) rs[rr] = fma(__ldg(G + (8 * MF + rr) * C::COLS + 4 * ks + (lane & 3)), v, rs[rr]);
+    }
   }
   // all reads of this warp's patches are done before any write (each patch's
   // reads are its own block; same-colour blocks do not contain other interiors)
@@ -897,8 +927,32 @@ struct __align__(16) CutDesc3 {
   unsigned long long kinds[2];   // 2 bits per cell of the 4x4x4 window, index (wz*4 + wy)*4 + wx
   int cid[8];                    // cut ids of the patch cells q = dx + 2 dy + 4 dz (-1 if not cut)
   long long inv_off;
-  unsigned long long mask[2];    // interior set over the (2p+1)^3 block (p <= 2: <= 125 bits)
+  unsigned long long mask[6];    // interior set over the (2p+1)^3 block (p <= 3: <= 343 bits)
 };
+static_assert(sizeof(CutDesc3) == 128, "CutDesc3 is two 64-byte lines");
+
+// interior-set bit mask of a 3D cut patch: count, membership, rank (index of
+// the interior DoF in A_j's order = number of set bits below it); words beyond
+// (2p+1)^3 bits are zero
+template <int P>
+__device__ __forceinline__ int mask_count3(const CutDesc3& d) {
+  constexpr int NW = ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 63) / 64;
+  int s = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) s += __popcll(d.mask[w]);
+  return s;
+}
+__device__ __forceinline__ bool mask_bit3(const CutDesc3& d, int loc) { return (d.mask[loc >> 6] >> (loc & 63)) & 1ull; }
+template <int P>
+__device__ __forceinline__ int mask_rank3(const CutDesc3& d, int loc) {
+  constexpr int NW = ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 63) / 64;
+  const int w = loc >> 6;
+  int s = __popcll(d.mask[w] & ((1ull << (loc & 63)) - 1ull));
+#pragma unroll
+  for (int q = 0; q < NW; ++q)
+    if (q < w) s += __popcll(d.mask[q]);
+  return s;
+}
 
 __device__ __forceinline__ int dkind3(const CutDesc3& d, int wx, int wy, int wz) {
   const int idx = (wz * 4 + wy) * 4 + wx;
@@ -928,7 +982,7 @@ __global__ void k_cut_desc3(LevelArgs L, const int* plist, int np, const int64_t
   }
   d.e0 = (int)ent_off[k];
   d.inv_off = inv_off[k];
-  d.mask[0] = d.mask[1] = 0ull;
+  for (int w = 0; w < 6; ++w) d.mask[w] = 0ull;
   for (int64_t e = ent_off[k]; e < ent_off[k + 1]; ++e) d.mask[ent_loc[e] >> 6] |= 1ull << (ent_loc[e] & 63);
   desc[k] = d;
 }
@@ -951,7 +1005,7 @@ __device__ void cut_patch_z3d(const LevelArgs& L, const CutDesc3& d, const doubl
   double* Jm = Jt + NJ;
   double* Yc = Jm + NJ;        // [8][NB] per-cell outputs
   double* Rr = Yc + 8 * NB;    // [MM]
-  const int m = __popcll(d.mask[0]) + __popcll(d.mask[1]);
+  const int m = mask_count3<P>(d);
   pdl_wait();
   for (int e = lane; e < WS * WS * WS; e += NT) {
     const int a = P * (d.I - 2) + e % WS, bb = P * (d.J - 2) + (e / WS) % WS, c = P * (d.K - 2) + e / (WS * WS);
@@ -1029,9 +1083,8 @@ __device__ void cut_patch_z3d(const LevelArgs& L, const CutDesc3& d, const doubl
   __syncthreads();
   // gather the interior rows (fixed cell order), residual
   for (int loc = lane; loc < MM; loc += NT) {
-    const unsigned long long word = d.mask[loc >> 6];
-    if (!((word >> (loc & 63)) & 1ull)) continue;
-    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    if (!mask_bit3(d, loc)) continue;
+    const int i = mask_rank3<P>(d, loc);
     const int ra = loc % BS, rb = (loc / BS) % BS, rc = loc / (BS * BS);
     double y = 0.0;
     for (int q = 0; q < 8; ++q) {
@@ -1107,7 +1160,7 @@ __global__ void __launch_bounds__(NT) k_cut_colour3v3(const __grid_constant__ CU
     if (TMA) mbar_init(bar, 1);
   }
   __syncthreads();
-  const int m = __popcll(d.mask[0]) + __popcll(d.mask[1]);
+  const int m = mask_count3<P>(d);
   // setup-time data (element matrices of the cut cells, local inverse): start
   // streaming it into L2 now, overlapping the previous kernel's tail (PDL)
   if (lane < 8) {
@@ -1133,9 +1186,8 @@ __global__ void __launch_bounds__(NT) k_cut_colour3v3(const __grid_constant__ CU
   }
   // residual rhs of the interior rows (independent of the window)
   for (int loc = lane; loc < MM; loc += NT) {
-    const unsigned long long word = d.mask[loc >> 6];
-    if (!((word >> (loc & 63)) & 1ull)) continue;
-    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    if (!mask_bit3(d, loc)) continue;
+    const int i = mask_rank3<P>(d, loc);
     const int ra = loc % BS, rb = (loc / BS) % BS, rc = loc / (BS * BS);
     Rr[i] = b[((size_t)(P * (d.K - 1) + rc) * L.nl + P * (d.J - 1) + rb) * L.ld + P * (d.I - 1) + ra];
   }
@@ -1212,9 +1264,8 @@ __global__ void __launch_bounds__(NT) k_cut_colour3v3(const __grid_constant__ CU
   // cells' ghost-face terms; residual = b - A x on the interior
   const unsigned long long gm = gmask;
   for (int loc = lane; loc < MM; loc += NT) {
-    const unsigned long long word = d.mask[loc >> 6];
-    if (!((word >> (loc & 63)) & 1ull)) continue;
-    const int i = (loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull));
+    if (!mask_bit3(d, loc)) continue;
+    const int i = mask_rank3<P>(d, loc);
     const int ra = loc % BS, rb = (loc / BS) % BS, rc = loc / (BS * BS);
     double y = 0.0;
 #pragma unroll

@@ -40,7 +40,8 @@ int64_t g_launches = 0;
   switch (p) {                                            \
     case 1: { constexpr int P = 1; __VA_ARGS__; } break;  \
     case 2: { constexpr int P = 2; __VA_ARGS__; } break;  \
-    default: throw Error(ERR_ARG, "3D supports degree 1..2"); \
+    case 3: { constexpr int P = 3; __VA_ARGS__; } break;  \
+    default: throw Error(ERR_ARG, "3D supports degree 1..3"); \
   }
 
 template <int P> constexpr int cart_tp() { return P == 1 ? 16 : (P == 2 ? 8 : (P == 3 ? 7 : 6)); }
@@ -649,7 +650,8 @@ struct Problem {
       D.cut_method_bytes[c] = 0;
       for (int k = D.cutp_off[c]; k < D.cutp_off[c + 1]; ++k) {
         const CutDesc3& d = hd[k];
-        const long long m = __builtin_popcountll(d.mask[0]) + __builtin_popcountll(d.mask[1]);
+        long long m = 0;
+        for (int w = 0; w < 6; ++w) m += __builtin_popcountll(d.mask[w]);
         int ncut = 0;
         for (int q = 0; q < 8; ++q) ncut += d.cid[q] >= 0;
         D.cut_method_bytes[c] += 8 * (m * m + (long long)ncut * e6 + bs3 + 2 * m);
@@ -1023,7 +1025,7 @@ struct Problem {
     const int64_t nv = vsize(0);
     int* nodes = alloc<int>(nv);
     n0 = select(D.mask, (int)nv, nodes);
-    require(n0 <= 160, ERR_SIZE, "coarse level has more than 160 DoFs; use a coarser level 0");
+    require(n0 <= 4096, ERR_SIZE, "coarse level has more than 4096 DoFs; use a coarser level 0");
     c_nodes = nodes;
     c_inv = alloc<double>((int64_t)n0 * n0);
     double* e = alloc<double>(nv);
@@ -1045,8 +1047,12 @@ struct Problem {
     int64_t* ioff = alloc<int64_t>(2);
     CF_CUDA(cudaMemcpyAsync(ioff, hz, sizeof(hz), cudaMemcpyHostToDevice, st));
     size_t smb = (size_t)(n0 * n0 + 2 * n0) * sizeof(double);
-    CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smb, 48 * 1024)));
-    k_batched_inverse<<<1, 256, smb, st>>>(offs, ioff, c_inv, 1);
+    if (smb <= 200 * 1024) {
+      CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smb, 48 * 1024)));
+      k_batched_inverse<<<1, 256, smb, st>>>(offs, ioff, c_inv, 1);
+    } else {   // (3D Q3: 343 coarse DoFs) in place in global memory
+      k_batched_inverse_gmem<<<1, 1024, 2 * n0 * sizeof(double), st>>>(offs, ioff, c_inv, 1, 0);
+    }
     CF_LAUNCHED();
     sync();
   }
@@ -1773,12 +1779,21 @@ struct Problem {
                             L, D.cutp_list, D.cutp_ent, D.ent_loc, D.ent_patch, D.n_ent, D.cutp_inv, D.inv,
                             prm.cut_mode)));
         CF_LAUNCHED();
-        const size_t smb = (size_t)(mmax * mmax + 2 * mmax) * sizeof(double);
-        require(smb <= 200 * 1024, ERR_SIZE, "cut patch too large for the batched inverse");
+        // local inverses in shared memory up to m = 160 (200 KB), larger ones
+        // (3D Q3: m up to 343) in global memory
+        int mfit = 1;
+        while ((size_t)((mfit + 1) * (mfit + 1) + 2 * (mfit + 1)) * sizeof(double) <= 200 * 1024) ++mfit;
+        const int msm = std::min(mmax, mfit);
+        const size_t smb = (size_t)(msm * msm + 2 * msm) * sizeof(double);
         CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smb, 48 * 1024)));
         k_batched_inverse<<<ncp, 256, smb, st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp);
         CF_LAUNCHED();
+        if (mmax > mfit) {
+          k_batched_inverse_gmem<<<ncp, 512, 2 * mmax * sizeof(double), st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp,
+                                                                               mfit + 1);
+          CF_LAUNCHED();
+        }
       }
       D.desc = alloc<CutDesc3>(ncp);
       if (ncp) {
@@ -1839,8 +1854,9 @@ struct Problem {
     LevelData& D = lv[l];
     const int np = D.act_cart_off[c + 1] - D.act_cart_off[c];
     if (!np) return;
-    CF_DISPATCH3(prm.p, (launch(k_cart_colour3<P>, dim3(ceil_div(ceil_div(np, 8), 4)), dim3(128), 0, D.a,
-                                (const int*)(D.act_cart + D.act_cart_off[c]), np, host::cart_map3(P), x, b)));
+    CF_DISPATCH3(prm.p, (launch(k_cart_colour3<P>, dim3(ceil_div(ceil_div(np, 8), CartMMA3<P>::NW)),
+                                dim3(32 * CartMMA3<P>::NW), 0, D.a, (const int*)(D.act_cart + D.act_cart_off[c]), np,
+                                host::cart_map3(P), x, b)));
     CF_LAUNCHED();
   }
 

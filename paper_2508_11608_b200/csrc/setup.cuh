@@ -330,11 +330,40 @@ __global__ void k_square(const int* m, int n, int* out) {
 // In-place Gauss-Jordan inverse of SPD matrices (no pivoting needed for SPD).
 // One CTA per matrix; matrix plus pivot row/column staged in dynamic shared
 // memory ((m*m + 2m) doubles).
+// the same Gauss-Jordan elimination in place in global memory, for local
+// matrices too large for shared memory (3D Q3 cut patches, m up to 343): one
+// CTA per patch, the pivot row / column staged in shared memory (2 m doubles)
+__global__ void k_batched_inverse_gmem(const int64_t* ent_off, const int64_t* inv_off, double* inv, int np,
+                                       int mmin) {
+  extern __shared__ double rc[];
+  const int k = blockIdx.x;
+  if (k >= np) return;
+  const int m = (int)(ent_off[k + 1] - ent_off[k]);
+  if (m < mmin) return;   // done by k_batched_inverse
+  double* A = inv + inv_off[k];
+  double* rowk = rc;
+  double* colk = rc + m;
+  for (int c = 0; c < m; ++c) {
+    const double piv = A[(int64_t)c * m + c];
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {
+      rowk[e] = (e == c ? 1.0 : A[(int64_t)c * m + e]) / piv;
+      colk[e] = A[(int64_t)e * m + c];
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < (int64_t)m * m; e += blockDim.x) {
+      const int i = (int)(e / m), jj = (int)(e % m);
+      A[e] = (i == c) ? rowk[jj] : ((jj == c ? 0.0 : A[e]) - colk[i] * rowk[jj]);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_batched_inverse(const int64_t* ent_off, const int64_t* inv_off, double* inv, int np) {
   extern __shared__ double sm[];
   int k = blockIdx.x;
   if (k >= np) return;
   int m = (int)(ent_off[k + 1] - ent_off[k]);
+  if ((size_t)(m * m + 2 * m) * sizeof(double) > 200 * 1024) return;   // k_batched_inverse_gmem
   double* A = inv + inv_off[k];
   double* rowk = sm + m * m;
   double* colk = rowk + m;

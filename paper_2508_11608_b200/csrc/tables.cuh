@@ -383,7 +383,7 @@ inline std::vector<double> cart_affine_map3(int p, const Tab& t, int& cols_pad) 
 
 inline const double* cart_map3(int p) {
   static const char keys[CF_MAXP + 1] = {};   // device pointer per (degree, device)
-  if (p < 1 || p > 2) return nullptr;
+  if (p < 1 || p > 3) return nullptr;
   return (const double*)dev_cached(&keys[p], [&] {
     Tab t;
     build_tab(p, t);

@@ -1,6 +1,6 @@
 """CUDA 3D (sphere) path vs the 3D oracle through the C ABI: structure
 bit-exact, operator / colour steps / smoothing steps / transfer to 1e-10,
-V-cycle to 1e-9, identical CG iteration counts."""
+V-cycle to 1e-9, identical CG iteration counts; Q1, Q2 and Q3."""
 import functools
 
 import numpy as np
@@ -17,6 +17,7 @@ CASES = [
     workloads.sphere("sphere-Q1-16", 2, 4, 1),
     workloads.sphere("sphere-Q2-8", 2, 3, 2),
     workloads.sphere("offc-Q2-8", 2, 3, 2, x0=-0.5, length=1.0, c=(0.0137, -0.0211, 0.0093), r=0.3071),
+    workloads.sphere("sphere-Q3-8", 2, 3, 3),    # Q3 (configs[3]'s degree): m up to 189 > 160 (global-memory inverse)
 ]
 IDS = [w.name for w in CASES]
 
@@ -152,3 +153,25 @@ def test_sphere64_fullsize_vs_oracle_goldens():
     xs = g.zeros()
     it, rel = g.solve_cg_mg(xs, g.to_device(bl), tol=float(d["tol"]), max_it=100)
     assert it == int(d["cg_it"]) and rel <= float(d["tol"])
+
+
+def test_sphere_q3_16_smoother_vcycle_cg():
+    # Q3 at 16^3 (63 001 DoFs, 2310 cut patches, interiors up to 183 DoFs):
+    # smoothing steps forward / reverse, V-cycle, identical CG count
+    w = workloads.sphere("sphere-Q3-16", 2, 4, 3)
+    o, g = oracle(w), gpu(w)
+    L = w.n_levels - 1
+    lv = o.fine.lv
+    xl, bl = rnd(w, 41, None), rnd(w, 42, None)
+    for rev in (False, True):
+        x = g.to_device(xl)
+        g.smooth(L, x, g.to_device(bl), rev)
+        xo = o.fine.smooth(xl[lv.dof_nodes].copy(), bl[lv.dof_nodes], w.n_c, reverse=rev)
+        assert rel_err(g.to_host(x)[lv.dof_nodes], xo) < TOL, rev
+    v = g.zeros()
+    g.vcycle(v, g.to_device(bl))
+    assert rel_err(g.to_host(v)[lv.dof_nodes], o.precondition(bl[lv.dof_nodes])) < 10 * TOL
+    xs = g.zeros()
+    it, rel = g.solve_cg_mg(xs, g.to_device(bl), tol=1e-8, max_it=100)
+    _, ito, _ = o.solve_cg(bl[lv.dof_nodes], 1e-8, 100)
+    assert it == ito and rel <= 1e-8
