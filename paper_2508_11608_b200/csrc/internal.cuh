@@ -199,7 +199,8 @@ extern int64_t g_launches;
     ++cf::g_launches;                                                                   \
     cudaError_t _e = cudaGetLastError();                                                \
     if (_e != cudaSuccess)                                                              \
-      throw cf::Error(cf::ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      throw cf::Error(cf::ERR_CUDA, std::string("kernel launch (") + __FILE__ + ":" + std::to_string(__LINE__) + \
+                                        "): " + cudaGetErrorString(_e));                \
   } while (0)
 
 enum { ERR_ARG = 1, ERR_CUDA = 2, ERR_STATE = 3, ERR_GEOMETRY = 4, ERR_SIZE = 5 };

@@ -142,13 +142,17 @@ struct Problem {
     CF_CUDA(cub::DeviceSelect::Flagged(scratch(bytes), bytes, it, flags, out, d_count, n, st));
     return read_count();
   }
-  // exclusive scan of n ints into n+1 int64 offsets; returns the total
+  // exclusive scan of n ints into n+1 int64 offsets; returns the total.  The
+  // ints are widened first: CUB accumulates in the input type, and sums such
+  // as the local-inverse sizes (3D Q3: sum m_j^2 ~ 5e9) overflow 32 bits
   int64_t scan64(const int* in, int n, int64_t* out) {
     size_t bytes = 0;
     CF_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
     if (n == 0) return 0;
-    CF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out + 1, n, st));
-    CF_CUDA(cub::DeviceScan::InclusiveSum(scratch(bytes), bytes, in, out + 1, n, st));
+    k_widen<<<ceil_div(n, 256), 256, 0, st>>>(in, n, out + 1);
+    CF_LAUNCHED();
+    CF_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, out + 1, out + 1, n, st));
+    CF_CUDA(cub::DeviceScan::InclusiveSum(scratch(bytes), bytes, out + 1, out + 1, n, st));
     int64_t tot = 0;
     CF_CUDA(cudaMemcpyAsync(&tot, out + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     sync();

@@ -322,6 +322,11 @@ __global__ void k_cut_interior(LevelArgs L, const int8_t* ct, const int* plist, 
   if (!WRITE) count[k] = m;
 }
 
+__global__ void k_widen(const int* in, int n, int64_t* out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = in[k];
+}
+
 __global__ void k_square(const int* m, int n, int* out) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) out[k] = m[k] * m[k];

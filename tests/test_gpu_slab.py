@@ -328,6 +328,8 @@ def test_world1_transports(transport):
 # ---- 3D: slabs of z-planes (narrow halo, one exchange per colour step) ----
 S3_Q2 = workloads.sphere("sphere-Q2-32", 2, 5, 2)                      # 2 .. 32 cells per side
 S3_Q1 = workloads.sphere("sphere-Q1-32-off", 2, 5, 1, c=(0.031, -0.017, 0.023), r=0.93)
+S3_Q3 = workloads.sphere("sphere-Q3-16", 2, 4, 3)        # configs[3] degree
+C3_Q2 = workloads.fitted("cube-Q2-24", 3, 4, 2, dim=3)   # configs[4] fitted cube
 
 
 def _rows3(g, v, level=-1):
@@ -338,7 +340,7 @@ def _rows3(g, v, level=-1):
     return a[info["r0"]:info["r1"]], info
 
 
-@pytest.mark.parametrize("w,world", [(S3_Q2, 2), (S3_Q2, 4), (S3_Q1, 2)])
+@pytest.mark.parametrize("w,world", [(S3_Q2, 2), (S3_Q2, 4), (S3_Q1, 2), (S3_Q3, 2), (C3_Q2, 2)])
 def test_3d_partition_bitexact(w, world):
     """3D smoothing steps (forward, reverse), operator and V-cycle on the owned
     planes bit-exact vs one rank; CG iteration counts identical"""
