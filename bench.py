@@ -373,11 +373,10 @@ def main():
             gk.close()
             return out
         cube, square = measure(workloads.CONFIG4_CUBE), measure(workloads.CONFIG4_SQUARE)
-        # BASELINE configs[3] (degree Q3) at the largest single-GPU size (workloads.CONFIG3)
+        # BASELINE configs[3]: 3D sphere, Q3, 256^3 (workloads.CONFIG3; Q4 not supported in 3D)
         cfg3q = measure(workloads.CONFIG3)
-        cfg3q["note"] = ("configs[3] asks 256^3 Q3/Q4 slab-partitioned: the dense Q3 cut-patch inverses "
-                         "(~30 GB at 128^3) would be ~4x that at 256^3 on every rank (replicated setup); "
-                         "3D Q4 is not supported (DESIGN.md row n4)")
+        cfg3q["note"] = ("cut-patch inverses stored packed symmetric (m (m+1)/2 per patch) above 35 % of free "
+                         "memory; 3D Q4 is not supported (DESIGN.md row n4)")
         cfg4 = {"cube_3d": cube, "square_2d": square, "l2": "flushed before every timed step",
                 "cut_overhead": {
                     "sphere_vs_cube_smoothing_dofs_per_s_ratio": (cfg3["smoothing_dofs_per_s"] /

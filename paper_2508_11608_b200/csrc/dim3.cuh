@@ -579,10 +579,13 @@ __global__ void k_vertex_flags3(int n, const uint8_t* vk, uint8_t kind, int colo
 }
 
 // local matrix column of a 3D cut patch (setup)
+// (entries [e_lo, e_lo + n_ent) of the patches [j0, ...); column kcol of
+// patch j goes to the chunk buffer inv at inv_off[j - j0], m x m row-major)
 template <int P>
 __global__ void __launch_bounds__(64) k_local_matrix3(LevelArgs L, const int* plist_all, const int64_t* ent_off,
                                                      const uint16_t* ent_loc, const int32_t* ent_patch, int64_t n_ent,
-                                                     const int64_t* inv_off, double* inv, int quad) {
+                                                     const int64_t* inv_off, double* inv, int quad, int64_t e_lo,
+                                                     int j0) {
   constexpr int BS = 2 * P + 1, WS = 4 * P + 1, N1 = P + 1;
   __shared__ SmTab T;
   __shared__ double sW[2][WS * WS * WS];
@@ -591,8 +594,8 @@ __global__ void __launch_bounds__(64) k_local_matrix3(LevelArgs L, const int* pl
   load_smtab<P>(T);
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t e = blockIdx.x * 2LL + w;
-  if (e >= n_ent) return;
+  const int64_t e = e_lo + blockIdx.x * 2LL + w;
+  if (e >= e_lo + n_ent) return;
   const int j = ent_patch[e], nv = L.n + 1;
   const int I = plist_all[j] % nv, J = (plist_all[j] / nv) % nv, K = plist_all[j] / (nv * nv);
   const int64_t e0 = ent_off[j];
@@ -608,8 +611,53 @@ __global__ void __launch_bounds__(64) k_local_matrix3(LevelArgs L, const int* pl
   __syncwarp();
   local_block_apply3<P>(L, I, J, K, sW[w], sY[w], T, sJ[w], quad != 0);
   __syncwarp();
-  double* A = inv + inv_off[j];
+  double* A = inv + inv_off[j - j0];
   for (int i = lane; i < m; i += 32) A[(int64_t)i * m + kcol] = sY[w][ent_loc[e0 + i]];
+}
+
+// Symmetric local inverses in PACKED mode (large problems, e.g. 3D Q3 at
+// 256^3 where the dense inverses would not fit): the lower triangle by rows,
+// row i at i (i+1) / 2, m (m+1) / 2 doubles per patch (half the dense
+// storage).  Packing of a chunk of full Gauss-Jordan inverses (symmetric up to
+// rounding): A(i, q) = F[i m + q], q <= i.
+__global__ void k_pack_sym(const int64_t* ent_off, const int64_t* full_off, const double* full,
+                           const int64_t* pack_off, double* pack, int np) {
+  const int k = blockIdx.x;
+  if (k >= np) return;
+  const int m = (int)(ent_off[k + 1] - ent_off[k]);
+  const double* F = full + full_off[k];
+  double* Pk = pack + pack_off[k];
+  for (int i = threadIdx.y; i < m; i += blockDim.y)
+    for (int q = threadIdx.x; q <= i; q += blockDim.x) Pk[(int64_t)i * (i + 1) / 2 + q] = F[(int64_t)i * m + q];
+}
+
+// z_i = sum_q A(i, q) r_q, A packed as above: for each q the lanes i < q read
+// A(q, i) = row q (consecutive i: coalesced), the lanes i >= q their own row i
+// (sequential per lane, sector reuse in L1)
+__device__ __forceinline__ double packed_sym_row(const double* A, const double* r, int m, int i) {
+  const int64_t ri = (int64_t)i * (i + 1) / 2;
+  double z0 = 0.0, z1 = 0.0;
+  int q = 0;
+  for (; q + 1 < m; q += 2) {
+    const int64_t a0 = i < q ? (int64_t)q * (q + 1) / 2 + i : ri + q;
+    const int64_t a1 = i < q + 1 ? (int64_t)(q + 1) * (q + 2) / 2 + i : ri + q + 1;
+    z0 = fma(__ldg(A + a0), r[q], z0);
+    z1 = fma(__ldg(A + a1), r[q + 1], z1);
+  }
+  if (q < m) z0 = fma(__ldg(A + (i < q ? (int64_t)q * (q + 1) / 2 + i : ri + q)), r[q], z0);
+  return z0 + z1;
+}
+
+// z_i = sum_q A[q m + i] r_q, A dense (default): coalesced over i for every q
+__device__ __forceinline__ double dense_col_dot(const double* A, const double* r, int m, int i) {
+  double z0 = 0.0, z1 = 0.0;
+  int q = 0;
+  for (; q + 1 < m; q += 2) {
+    z0 = fma(__ldg(A + (int64_t)q * m + i), r[q], z0);
+    z1 = fma(__ldg(A + (int64_t)(q + 1) * m + i), r[q + 1], z1);
+  }
+  if (q < m) z0 = fma(__ldg(A + (int64_t)q * m + i), r[q], z0);
+  return z0 + z1;
 }
 
 // ---- 3D smoother kernels ----------------------------------------------------
@@ -648,11 +696,7 @@ __global__ void __launch_bounds__(64) k_cut_colour3(LevelArgs L, const int* plis
   for (int i = lane; i < m; i += 32) sR[w][i] = b[ent_node[e0 + i]] - sY[w][ent_loc[e0 + i]];
   __syncwarp();
   const double* A = inv + inv_off[j];
-  for (int i = lane; i < m; i += 32) {
-    double z = 0.0;
-    for (int q = 0; q < m; ++q) z = fma(A[(int64_t)q * m + i], sR[w][q], z);
-    zbuf[e0 + i] = z;
-  }
+  for (int i = lane; i < m; i += 32) zbuf[e0 + i] = L.sym_packed ? packed_sym_row(A, sR[w], m, i) : dense_col_dot(A, sR[w], m, i);
 }
 
 // Cartesian colour step in 3D: x_int_new = G [b_int; x_ext] for groups of 8
@@ -1098,11 +1142,7 @@ __device__ void cut_patch_z3d(const LevelArgs& L, const CutDesc3& d, const doubl
   }
   __syncthreads();
   const double* A = inv + d.inv_off;
-  for (int i = lane; i < m; i += NT) {
-    double z = 0.0;
-    for (int q = 0; q < m; ++q) z = fma(__ldg(A + (int64_t)q * m + i), Rr[q], z);
-    zbuf[d.e0 + i] = z;
-  }
+  for (int i = lane; i < m; i += NT) zbuf[d.e0 + i] = L.sym_packed ? packed_sym_row(A, Rr, m, i) : dense_col_dot(A, Rr, m, i);
 }
 
 template <int P>
@@ -1166,7 +1206,7 @@ __global__ void __launch_bounds__(NT) k_cut_colour3v3(const __grid_constant__ CU
   if (lane < 8) {
     if (d.cid[lane] >= 0) prefetch_l2(L.ecut + (size_t)d.cid[lane] * NB * NB, NB * NB * sizeof(double));
   } else if (lane == 8) {
-    prefetch_l2(inv + d.inv_off, (size_t)m * m * sizeof(double));
+    prefetch_l2(inv + d.inv_off, (size_t)(L.sym_packed ? m * (m + 1) / 2 : m * m) * sizeof(double));
   }
   pdl_wait();
   if (TMA) {
@@ -1298,16 +1338,7 @@ __global__ void __launch_bounds__(NT) k_cut_colour3v3(const __grid_constant__ CU
   }
   __syncthreads();
   const double* A = inv + d.inv_off;
-  for (int i = lane; i < m; i += NT) {
-    double z0 = 0.0, z1 = 0.0;
-    int q = 0;
-    for (; q + 1 < m; q += 2) {
-      z0 = fma(__ldg(A + (int64_t)q * m + i), Rr[q], z0);
-      z1 = fma(__ldg(A + (int64_t)(q + 1) * m + i), Rr[q + 1], z1);
-    }
-    if (q < m) z0 = fma(__ldg(A + (int64_t)q * m + i), Rr[q], z0);
-    zbuf[d.e0 + i] = z0 + z1;
-  }
+  for (int i = lane; i < m; i += NT) zbuf[d.e0 + i] = L.sym_packed ? packed_sym_row(A, Rr, m, i) : dense_col_dot(A, Rr, m, i);
 }
 
 }  // namespace cf

@@ -59,6 +59,7 @@ struct LevelArgs {
   int n, p, nl, ld;
   int dim;                           // 2 or 3
   int fitted;                        // fitted box: every cell Inside, no DoF on the box boundary
+  int sym_packed;                    // 3D local inverses packed symmetric (k_pack_sym) instead of dense
   double h, x0, y0, z0;
   double cx, cy, cz, r;
   double gDh;                        // gamma_D / h

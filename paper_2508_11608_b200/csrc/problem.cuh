@@ -80,6 +80,7 @@ struct Problem {
   int tile_apply_min_tiles = 148;   // TMA-tiled operator on levels with >= this many 16x16 tiles (env CUTFEM_TILEAPPLY_MIN)
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
+  bool sym_packed = false;  // 3D: always pack the local inverses symmetric (env CUTFEM_SYM_PACKED=1)
   // slab partition: comm != nullptr after partition()
   Comm* comm = nullptr;
   static constexpr int HALO = 4;   // halo width in cells (the fused Cartesian apron)
@@ -227,6 +228,7 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_WIDE_HALO")) wide_halo = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_CUTMAP")) cut_map = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_SYM_PACKED")) sym_packed = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
@@ -637,7 +639,7 @@ struct Problem {
         const long long nnz = d.map_off >= 0 ? (long long)(d.map_off >> 48) : 0;
         int ncut = 0;
         for (int q = 0; q < 4; ++q) ncut += d.cid[q] >= 0;
-        D.cut_method_bytes[c] += 8 * (m * m + (long long)ncut * e4 + 3 * m + nnz);
+        D.cut_method_bytes[c] += 8 * (m * (m + 1) / 2 + (long long)ncut * e4 + 3 * m + nnz);
       }
   }
 
@@ -658,7 +660,7 @@ struct Problem {
         for (int w = 0; w < 6; ++w) m += __builtin_popcountll(d.mask[w]);
         int ncut = 0;
         for (int q = 0; q < 8; ++q) ncut += d.cid[q] >= 0;
-        D.cut_method_bytes[c] += 8 * (m * m + (long long)ncut * e6 + bs3 + 2 * m);
+        D.cut_method_bytes[c] += 8 * (m * (m + 1) / 2 + (long long)ncut * e6 + bs3 + 2 * m);   // (symmetric A_j^{-1}: m (m+1) / 2)
       }
     }
   }
@@ -1765,38 +1767,79 @@ struct Problem {
                                                                  D.ent_loc, D.ent_patch);
         CF_LAUNCHED();
       }
-      int* msq = alloc<int>(ncp);
+      // local matrices and their inverses (P l.193, R10).  Dense m x m
+      // (default, coalesced apply) unless they would take more than 35 % of the
+      // free device memory (3D Q3 at 256^3): then they are built in chunks of
+      // <= 2 GB of dense matrices and packed symmetric (k_pack_sym, m (m+1) / 2
+      // doubles per patch; env CUTFEM_SYM_PACKED=1 forces it)
       D.cutp_inv = alloc<int64_t>(ncp + 1);
+      std::vector<int> hm(ncp);
+      if (ncp) CF_CUDA(cudaMemcpyAsync(hm.data(), mcount, sizeof(int) * ncp, cudaMemcpyDeviceToHost, st));
+      sync();
+      std::vector<int64_t> hpk(ncp + 1, 0), hfull(ncp + 1, 0), hent(ncp + 1, 0);
       int mmax = 0;
-      if (ncp) {
-        k_square<<<ceil_div(ncp, 128), 128, 0, st>>>(mcount, ncp, msq);
-        CF_LAUNCHED();
-        std::vector<int> hm(ncp);
-        CF_CUDA(cudaMemcpyAsync(hm.data(), mcount, sizeof(int) * ncp, cudaMemcpyDeviceToHost, st));
-        sync();
-        for (int v : hm) mmax = std::max(mmax, v);
+      for (int k = 0; k < ncp; ++k) {
+        hpk[k + 1] = hpk[k] + (int64_t)hm[k] * (hm[k] + 1) / 2;
+        hfull[k + 1] = hfull[k] + (int64_t)hm[k] * hm[k];
+        hent[k + 1] = hent[k] + hm[k];
+        mmax = std::max(mmax, hm[k]);
       }
-      D.n_inv = scan64(msq, ncp, D.cutp_inv);
+      size_t mfree = 0, mtot = 0;
+      CF_CUDA(cudaMemGetInfo(&mfree, &mtot));
+      const bool packed = sym_packed || (double)hfull[ncp] * 8.0 > 0.35 * (double)mfree;
+      L.sym_packed = packed;
+      const std::vector<int64_t>& hoff = packed ? hpk : hfull;
+      if (ncp) CF_CUDA(cudaMemcpy(D.cutp_inv, hoff.data(), sizeof(int64_t) * (ncp + 1), cudaMemcpyHostToDevice));
+      D.n_inv = hoff[ncp];
       D.inv = alloc<double>(D.n_inv);
       if (D.n_ent) {
-        CF_DISPATCH3(p, (k_local_matrix3<P><<<ceil_div(D.n_ent, 2), 64, 0, st>>>(
-                            L, D.cutp_list, D.cutp_ent, D.ent_loc, D.ent_patch, D.n_ent, D.cutp_inv, D.inv,
-                            prm.cut_mode)));
-        CF_LAUNCHED();
-        // local inverses in shared memory up to m = 160 (200 KB), larger ones
-        // (3D Q3: m up to 343) in global memory
-        int mfit = 1;
+        int mfit = 1;   // local inverses in shared memory up to m = 160 (200 KB), larger ones in global memory
         while ((size_t)((mfit + 1) * (mfit + 1) + 2 * (mfit + 1)) * sizeof(double) <= 200 * 1024) ++mfit;
         const int msm = std::min(mmax, mfit);
         const size_t smb = (size_t)(msm * msm + 2 * msm) * sizeof(double);
         CF_CUDA(cudaFuncSetAttribute(k_batched_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smb, 48 * 1024)));
-        k_batched_inverse<<<ncp, 256, smb, st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp);
-        CF_LAUNCHED();
-        if (mmax > mfit) {
-          k_batched_inverse_gmem<<<ncp, 512, 2 * mmax * sizeof(double), st>>>(D.cutp_ent, D.cutp_inv, D.inv, ncp,
-                                                                               mfit + 1);
-          CF_LAUNCHED();
+        // dense: one chunk built in place in D.inv; packed: chunks through a scratch buffer
+        const int64_t CHUNK = packed ? (256ll << 20) : hfull[ncp] + 1;   // doubles of dense matrices per chunk
+        int64_t maxfull = 0;
+        for (int k0 = 0, k1; k0 < ncp; k0 = k1) {
+          for (k1 = k0 + 1; k1 < ncp && hfull[k1 + 1] - hfull[k0] <= CHUNK; ++k1) {
+          }
+          maxfull = std::max(maxfull, hfull[k1] - hfull[k0]);
+        }
+        double* full = packed ? alloc<double>(maxfull) : D.inv;
+        int64_t* foff = alloc<int64_t>(ncp + 1);
+        std::vector<int64_t> hf(ncp + 1);
+        for (int k0 = 0, k1; k0 < ncp; k0 = k1) {
+          for (k1 = k0 + 1; k1 < ncp && hfull[k1 + 1] - hfull[k0] <= CHUNK; ++k1) {
+          }
+          const int nk = k1 - k0;
+          for (int k = k0; k <= k1; ++k) hf[k - k0] = hfull[k] - hfull[k0];
+          CF_CUDA(cudaMemcpyAsync(foff, hf.data(), sizeof(int64_t) * (nk + 1), cudaMemcpyHostToDevice, st));
+          const int64_t e_lo = hent[k0], ne = hent[k1] - hent[k0];
+          if (ne) {
+            CF_DISPATCH3(p, (k_local_matrix3<P><<<ceil_div(ne, 2), 64, 0, st>>>(
+                                L, D.cutp_list, D.cutp_ent, D.ent_loc, D.ent_patch, ne, foff, full, prm.cut_mode, e_lo,
+                                k0)));
+            CF_LAUNCHED();
+            k_batched_inverse<<<nk, 256, smb, st>>>(D.cutp_ent + k0, foff, full, nk);
+            CF_LAUNCHED();
+            if (mmax > mfit) {
+              k_batched_inverse_gmem<<<nk, 512, 2 * mmax * sizeof(double), st>>>(D.cutp_ent + k0, foff, full, nk,
+                                                                                   mfit + 1);
+              CF_LAUNCHED();
+            }
+            if (packed) {
+              k_pack_sym<<<nk, dim3(32, 8), 0, st>>>(D.cutp_ent + k0, foff, full, D.cutp_inv + k0, D.inv, nk);
+              CF_LAUNCHED();
+            }
+          }
+          sync();   // foff / full are reused by the next chunk
+        }
+        for (void* q : {packed ? (void*)full : nullptr, (void*)foff}) {
+          if (!q) continue;
+          cudaFree(q);
+          allocs.erase(std::remove(allocs.begin(), allocs.end(), q), allocs.end());
         }
       }
       D.desc = alloc<CutDesc3>(ncp);

@@ -110,11 +110,16 @@ def test_transfer_vcycle_cg_3d(w):
     assert rel_err(g.to_host(x)[lf.dof_nodes], xo) < 1e-7
 
 
-@pytest.mark.parametrize("env", [{"CUTFEM_CUT3": "2"}, {"CUTFEM_TMA": "0"}], ids=["cut3-v2", "cut3-no-tma"])
-def test_alternative_cut_kernels_3d(env, monkeypatch):
+@pytest.mark.parametrize("env,wi", [({"CUTFEM_CUT3": "2"}, 2), ({"CUTFEM_TMA": "0"}, 2), ({"CUTFEM_CUT3": "1"}, 2),
+                                    ({"CUTFEM_SYM_PACKED": "1"}, 2), ({"CUTFEM_SYM_PACKED": "1"}, 3),
+                                    ({"CUTFEM_SYM_PACKED": "1", "CUTFEM_CUT3": "2"}, 2)],
+                         ids=["cut3-v2", "cut3-no-tma", "cut3-v1", "sym-packed-q2", "sym-packed-q3", "sym-packed-v2"])
+def test_alternative_cut_kernels_3d(env, wi, monkeypatch):
+    # alternative 3D cut kernels and the packed symmetric local inverses (the
+    # storage large 3D Q3 problems switch to) vs the oracle's colour steps
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    w = CASES[2]
+    w = CASES[wi]
     o, g = oracle(w), gpu(w)
     l = len(o.levels) - 1
     ld = o.levels[l]

@@ -59,11 +59,11 @@ def sphere(name, n_coarse, n_levels, p, x0=-1.105, length=2.21, c=(0.0, 0.0, 0.0
 
 
 # BASELINE.json configs[3]: "3D sphere, Q3/Q4 higher order, 256^3 background
-# mesh, slab-partitioned over 2/4/8 B200": Q3 at 128^3 (23.1 M DoFs) is the
-# largest sphere whose dense cut-patch inverses (~30 GB) fit next to the
-# hierarchy on one B200; at 256^3 they would be ~4x that on every rank (the
-# setup is replicated under the slab partition).  3D Q4 is not supported.
-CONFIG3 = Workload("config3-sphere-Q3-128^3", -1.105, -1.105, 2.21, 2, 7, 0.0, 0.0, 1.0, 3, dim=3, z0=-1.105, cz=0.0)
+# mesh, slab-partitioned over 2/4/8 B200": Q3 at 256^3 (180 M DoFs; the
+# 641 k cut-patch inverses are stored packed symmetric, ~55 GB, and the whole
+# problem takes ~125 GB of one B200; under --gpus N the z-slab partition runs
+# it with the setup replicated on every rank).  3D Q4 is not supported.
+CONFIG3 = Workload("config3-sphere-Q3-256^3", -1.105, -1.105, 2.21, 2, 8, 0.0, 0.0, 1.0, 3, dim=3, z0=-1.105, cz=0.0)
 
 
 def fitted(name, n_coarse, n_levels, p, dim=2, x0=-1.105, length=2.21, tol=1e-8):
