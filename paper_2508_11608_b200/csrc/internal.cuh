@@ -126,7 +126,8 @@ struct LevelData {
   int tc = 16;                       // cells of the fused tiles of this level in y (rows)
   int tcx = 16;                      // ... and in x
   int* fused_ext = nullptr;          // fused tiles dilated by one tile (split sweep through xs)
-  unsigned long long* gbar = nullptr; // grid-barrier counter of the in-place fused sweep
+  unsigned* tflag = nullptr;         // in-place fused sweep: per-tile "region loaded" counters, (tx+2) x (ty+2)
+  int tflag_stride = 0;              //   with a border; tiles not launched hold 0x7fffffff
   int n_fused_ext = 0;
   int n_cutp[8] = {};
   int cutp_off[9] = {};

@@ -479,8 +479,9 @@ struct Problem {
           CF_LAUNCHED();
         }
         D.fused_ext = te;
-        D.gbar = alloc<unsigned long long>(1);
-        CF_CUDA(cudaMemsetAsync(D.gbar, 0, sizeof(unsigned long long), st));
+        D.tflag_stride = tx + 2;
+        D.tflag = alloc<unsigned>((int64_t)(tx + 2) * (ty + 2));
+        reset_tile_flags(D, ty);
       }
       D.cart_tiles = alloc<int>(tiles.size());
       if (!tiles.empty())
@@ -559,6 +560,21 @@ struct Problem {
     for (double* v : {cg_x, cg_r, cg_z, cg_p, cg_q}) CF_CUDA(cudaMemsetAsync(v, 0, nvf * 8, st));
     sync();
     built = true;
+  }
+
+  // tile counters of the in-place fused sweep (k_cart_fused_tma): 0 on the
+  // tiles of D.fused_tiles, 0x7fffffff elsewhere (border and absent tiles
+  // never hold a launch back); stream-ordered after every launch so far
+  void reset_tile_flags(LevelData& D, int ty) {
+    const int stride = D.tflag_stride;
+    std::vector<unsigned> h((size_t)stride * (ty + 2), 0x7fffffffu);
+    std::vector<int> t(D.n_fused_tiles);
+    if (D.n_fused_tiles) CF_CUDA(cudaMemcpyAsync(t.data(), D.fused_tiles, sizeof(int) * D.n_fused_tiles,
+                                                 cudaMemcpyDeviceToHost, st));
+    sync();
+    for (int v : t) h[(size_t)((v >> 16) + 1) * stride + (v & 0xffff) + 1] = 0u;
+    CF_CUDA(cudaMemcpyAsync(D.tflag, h.data(), sizeof(unsigned) * h.size(), cudaMemcpyHostToDevice, st));
+    sync();
   }
 
   // ping-pong copy lists (see k_cut_step): [prev][cur] = N_prev \ N_cur for
@@ -971,10 +987,8 @@ struct Problem {
       };
       own_tiles(D.fused_tiles, D.n_fused_tiles);
       own_tiles(D.fused_ext, D.n_fused_ext);
-      // the in-place sweep's grid barrier releases at the next multiple of the
-      // grid size: restart its counter for the new (smaller) grid (stream-
-      // ordered after every launch issued so far)
-      if (D.gbar) CF_CUDA(cudaMemsetAsync(D.gbar, 0, sizeof(unsigned long long), st));
+      // the in-place sweep's tile counters: only the rank's tiles take part now
+      if (D.tflag) reset_tile_flags(D, ceil_div(D.a.n, D.tc));
       // cut patches with vertex rows [c0 - 1, c1]
       const int ncp = D.cutp_off[4];
       std::vector<CutDesc> hd(ncp), kd;
@@ -1211,7 +1225,7 @@ struct Problem {
     }
     if (!cart_split && D.n_fused_tiles <= cap) {
       launch_ex(true, k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
-                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, D.gbar);
+                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, D.tflag, D.tflag_stride);
       CF_LAUNCHED();
       cart_done(l, x, reverse);
       return;
@@ -1219,11 +1233,11 @@ struct Problem {
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
     if (D.n_fused_ext)
       launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
-             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned long long*)nullptr);
+             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned*)nullptr, 0);
     CF_LAUNCHED();
     halo_n(l, D.xs);
     launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
-           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, (unsigned long long*)nullptr);
+           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, (unsigned*)nullptr, 0);
     CF_LAUNCHED();
     cart_done(l, x, reverse);
     return;

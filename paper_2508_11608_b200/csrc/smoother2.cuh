@@ -986,6 +986,15 @@ namespace cf {
 // configuration, never reset: the target is the next multiple of the grid
 // size).  Control only -- the CTAs' region loads have completed (TMA
 // mbarrier) before they arrive, which is all the in-place sweep needs.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1002,22 +1011,27 @@ struct CartTmaSmem {
   static constexpr int H = 4, RW = (TC + 2 * H) * P + 1, RWX = (TCX + 2 * H) * P + 1, RWP = (RWX + 1) & ~1;
   static constexpr int tile_doubles = (RW * RWP + 15) & ~15;   // 128-byte aligned tiles (TMA destination)
   static constexpr int maxp = ((TCX + 7) / 2 + 1) * ((TC + 7) / 2 + 1);
-  static constexpr int head = ((16 + 4 * maxp) + 127) & ~127;     // mbarrier, count, patch list
+  static constexpr int head = ((32 + 4 * 4 * maxp) + 127) & ~127;   // mbarrier, 4 counts, 4 pass patch lists
   static constexpr size_t bytes = head + 2 * tile_doubles * sizeof(double);
 };
 
 // Passes s0..s1-1 of the four colour passes (halo radius s1-1-s).  The tile
 // region is read from the tensor map `tmx` and the owned nodes are written to
-// `xout`.  In place (xout = the source of tmx) only with gsync = 1 in a
-// cooperative launch: the grid barrier before the write keeps every CTA's
-// apron load ahead of its neighbours' writes.  Otherwise the sweep is split
-// into two launches through the shadow buffer (passes 0-1 x -> xs, 2-3 xs -> x).
+// `xout`.  In place (xout = the source of tmx) only with tile flags in a
+// cooperative (co-resident) launch: a CTA publishes "my region is loaded" on
+// its tile's counter (st.release after the TMA load completed) and writes its
+// owned nodes back only after its 8 neighbour tiles -- the only ones whose
+// aprons (H = 4 < tile width) hold them -- have published (ld.acquire poll).
+// Counters advance by one per in-place launch on every launched tile, so a
+// launch reads its own counter as the base; tiles not in the launch hold
+// 0x7fffffff.  Otherwise the sweep is split into two launches through the
+// shadow buffer (passes 0-1 x -> xs, 2-3 xs -> x).
 template <int P, int TC, int NT = 256, int TCX = TC>
 __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* xout, int reverse, int s0, int s1,
-                                                        unsigned long long* gbar) {
+                                                        unsigned* tflag, int tstride) {
   using C = CartMMA<P>;
   using S = CartTmaSmem<P, TC, TCX>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
@@ -1027,8 +1041,8 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
   constexpr int MAXP = S::maxp;   // candidate patches of the widest pass
   extern __shared__ __align__(128) unsigned char smraw[];
   uint64_t* bar = (uint64_t*)smraw;
-  int* plist = (int*)(smraw + 16);             // compacted Cartesian patches of a pass (block origins)
-  int* pcount = (int*)(smraw + 8);
+  int* pcount = (int*)(smraw + 8);             // [4] patches per pass
+  int* plists = (int*)(smraw + 32);            // [4][MAXP] compacted Cartesian patches of each pass (block origins)
   double* Xs = (double*)(smraw + S::head);     // x tile [RW][RWP]; the b tile follows at Xs + TD
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = L.n;
   pdl_trigger();
@@ -1054,30 +1068,39 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
   const int tile = tiles[blockIdx.x];
   const int ci0 = (tile & 0xffff) * TCX, cj0 = (tile >> 16) * TC;
   const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
+  if (tid < 4) pcount[tid] = 0;
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
-  pdl_wait();
-  if (tid == 0) {
-    mbar_expect_tx(bar, 2u * RW * RWP * sizeof(double));
-    tma_load_2d(Xs, &tmx, a0, b0, bar);
-    tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
-  }
+  // compact the Cartesian patches of every pass (setup data: before the PDL
+  // wait, overlapping the predecessor's tail)
   for (int s = s0; s < s1; ++s) {
     const int c = reverse ? 3 - s : s, rad = s1 - 1 - s;
     const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
     const int nvx = (ci0 + TCX + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
-    // compact the Cartesian patches of this pass
-    if (tid == 0) *pcount = 0;
-    __syncthreads();
     for (int q = tid; q < nvx * nvy; q += NT) {
       const int pj = q / nvx, pi = q - pj * nvx;
       const int I = ilo + 2 * pi, J = jlo + 2 * pj;
       if (I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART)
-        plist[atomicAdd(pcount, 1)] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
+        plists[s * MAXP + atomicAdd(pcount + s, 1)] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
     }
-    if (s == s0) mbar_wait(bar, 0);
+  }
+  pdl_wait();
+  unsigned* myflag = tflag ? tflag + ((tile >> 16) + 1) * tstride + (tile & 0xffff) + 1 : nullptr;
+  unsigned fbase = 0;
+  if (tid == 0) {
+    mbar_expect_tx(bar, 2u * RW * RWP * sizeof(double));
+    tma_load_2d(Xs, &tmx, a0, b0, bar);
+    tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
+    if (myflag) fbase = *(volatile unsigned*)myflag;
+  }
+  for (int s = s0; s < s1; ++s) {
+    const int* plist = plists + s * MAXP;
+    if (s == s0) {
+      mbar_wait(bar, 0);
+      if (myflag && tid == 0) st_release_u32(myflag, fbase + 1u);   // region loaded: neighbours may write
+    }
     __syncthreads();
-    const int np = *pcount, ng = (np + 7) / 8;
+    const int np = pcount[s], ng = (np + 7) / 8;
 #ifndef CF_CART_GPW
 #define CF_CART_GPW 1   // groups of 8 patches per warp iteration (2: measured no faster, spills at 16-cell tiles)
 #endif
@@ -1129,8 +1152,19 @@ __global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_
     }
     __syncthreads();
   }
-  if (s1 == s0) mbar_wait(bar, 0);
-  if (gbar) grid_barrier(gbar);
+  if (s1 == s0) {
+    mbar_wait(bar, 0);
+    if (myflag && tid == 0) st_release_u32(myflag, fbase + 1u);
+  }
+  if (myflag) {   // the 8 neighbours have loaded their aprons (which hold our owned nodes)
+    const unsigned want = __shfl_sync(0xffffffffu, fbase, 0) + 1u;   // (warp 0: thread 0's base)
+    if (tid < 9 && tid != 4) {
+      const unsigned* f = myflag + (tid / 3 - 1) * tstride + (tid % 3 - 1);
+      while (ld_acquire_u32(f) < want) {
+      }
+    }
+    __syncthreads();
+  }
   // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
   const int ahi = (ci0 + TCX >= n) ? L.nl : P * (ci0 + TCX), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   for (int bb = P * cj0 + warp; bb < bhi; bb += NT / 32) {
