@@ -203,6 +203,19 @@ def main():
     if dist:
         dist.barrier()
     value = strong_throughput(n_dofs, args.steps, total_ms)
+    halo_info = None
+    if world > 1:   # NVLink bytes of the finest level's halo exchanges (this rank's sends), from the slab plan
+        try:
+            pi = g.partition_info(L)
+            if pi["part"]:
+                def sent(hc):
+                    plan = cutfem.slab_plan(info.n, w.p, world, rank, hc)
+                    return int(sum(x["send_n"] for x in plan["xfers"]) * 8)
+                halo_info = {"wide_halo_cells": pi["halo"], "bytes_per_wide_exchange": sent(pi["halo"]),
+                             "bytes_per_narrow_exchange": sent(4),
+                             "exchanges_per_smoothing_step": "2 (forward), 3 (reverse)", "rank": rank}
+        except Exception as e:  # noqa: BLE001  (reporting only)
+            halo_info = {"error": repr(e)}
 
     # ---- kernels of the step, timed alone (live, CUDA events, L2 flushed)
     p = w.p
@@ -401,7 +414,7 @@ def main():
                        "cells_per_side": info.n, "levels": w.n_levels, "n_dofs": int(n_dofs), "n_c": w.n_c,
                        "l2": "flushed (512 MB write) before every timed step",
                        "parallelism": f"slab{world} (NCCL halo exchange per colour sweep / residual)"
-                       if world > 1 else "single GPU"},
+                       if world > 1 else "single GPU", "halo": halo_info},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -1208,7 +1208,7 @@ struct Problem {
   template <int P, int TC, int TCX = TC>
   void cart_fused_tma(int l, double* x, const double* b, int reverse) {
     LevelData& D = lv[l];
-    constexpr int NT = TC >= 32 ? CF_CART_NT32 : 256;
+    constexpr int NT = P >= 3 ? 128 : (TC >= 32 ? CF_CART_NT32 : 256);   // (Q3: 152 registers of G fragments per thread)
     const double* G = host::cart_map(P);
     using S = CartTmaSmem<P, TC, TCX>;
     const CUtensorMap tmx = host::lattice_tmap(x, D.a.nl, D.a.ld, S::RWP, S::RW);

@@ -1027,7 +1027,7 @@ struct CartTmaSmem {
 // 0x7fffffff.  Otherwise the sweep is split into two launches through the
 // shadow buffer (passes 0-1 x -> xs, 2-3 xs -> x).
 template <int P, int TC, int NT = 256, int TCX = TC>
-__global__ void __launch_bounds__(NT, TC >= 32 ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k_cart_fused_tma(const __grid_constant__ CUtensorMap tmx,
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* xout, int reverse, int s0, int s1,
