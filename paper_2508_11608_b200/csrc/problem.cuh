@@ -276,6 +276,7 @@ struct Problem {
       CF_LAUNCHED();
       L.mask = D.mask;
       D.n_dofs = read_count();
+      require(D.n_dofs > 0, ERR_GEOMETRY, "a level has no DoF: the domain does not meet the background box");
       if (l > 0) {
         CF_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int), st));
         k_parent_check<<<gcell, b2, 0, st>>>(L, D.ctype, lv[l - 1].a.n, lv[l - 1].ctype, d_count);
@@ -1633,6 +1634,7 @@ struct Problem {
       CF_LAUNCHED();
       L.mask = D.mask;
       D.n_dofs = read_count();
+      require(D.n_dofs > 0, ERR_GEOMETRY, "a level has no DoF: the domain does not meet the background box");
       if (l > 0) {
         CF_CUDA(cudaMemsetAsync(d_count, 0, sizeof(int), st));
         k_parent_check3<<<ceil_div(n3, 256), 256, 0, st>>>(L, lv[l - 1].a, d_count);

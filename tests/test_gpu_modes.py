@@ -99,7 +99,12 @@ def test_sigma_plus_one_and_gamma():
     workloads.Workload("tiny-cuts", -1.0, -1.0, 2.0, 2, 5, 0.0312, 0.0, 0.7501, 1),
     workloads.Workload("Q3", -1.105, -1.105, 2.21, 2, 5, 0.0, 0.0, 1.0, 3),
     workloads.Workload("Q4", -1.105, -1.105, 2.21, 2, 4, 0.0, 0.0, 1.0, 4),
-], ids=["tangent-ish", "tiny-cuts", "Q3", "Q4"])
+    # the circle passes exactly through mesh vertices (fp64-exact ties: cells
+    # touching it in one point are Outside, R2) on every level
+    workloads.Workload("vertex-touch", -1.0, -1.0, 2.0, 2, 5, 0.0, 0.0, 0.5, 2),
+    # a domain inside one coarse cell: no Cartesian patch on the coarse levels
+    workloads.Workload("small-domain", -0.5, -0.5, 1.0, 2, 5, 0.1, 0.07, 0.12, 2),
+], ids=["tangent-ish", "tiny-cuts", "Q3", "Q4", "vertex-touch", "small-domain"])
 def test_edge_geometries_and_degrees(w):
     g, o = run_smoother(w)
     bl = lattice_random(w, 65, None)
@@ -133,3 +138,12 @@ def test_cart_split_equals_inplace_fullsize():
         outs.append(g.to_host(x))
         g.close()
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_domain_missing_the_box_fails_loudly():
+    # no active cell on some level: setup reports a geometry error (no silent
+    # empty problem)
+    from paper_2508_11608_b200 import cutfem
+    w = workloads.Workload("outside", -0.5, -0.5, 1.0, 2, 3, 5.0, 5.0, 0.3, 1)
+    with pytest.raises(cutfem.CutfemError, match="no DoF"):
+        cutfem.Problem.from_workload(w)
