@@ -31,6 +31,7 @@ W_Q2 = workloads.paper_level(2, 9)                 # 2 .. 128 cells per side
 W_Q1 = workloads.paper_level(1, 9)                 # 2 .. 256
 W_Q3 = workloads.paper_level(3, 9)
 W_OFF = Workload("offcentre-Q2-256", -1.105, -1.105, 2.21, 2, 8, 0.0137, -0.0211, 0.9071, 2)
+W_FIT = workloads.fitted("square-Q2-256", 2, 8, 2)   # configs[4] 2D analogue: fitted box, no cut patch
 
 
 def _cutfem():
@@ -168,6 +169,7 @@ NARROW = {"CUTFEM_WIDE_HALO": "0"}    # one exchange per cut step everywhere
 
 
 @pytest.mark.parametrize("w,world,env", [(W_Q2, 2, None), (W_Q2, 4, None), (W_Q1, 2, None), (W_Q1, 8, None),
+                                         (W_FIT, 2, None), (W_FIT, 4, None),
                                          (W_Q3, 2, None), (W_OFF, 4, None), (W_Q2, 2, TC32), (W_OFF, 4, TC32),
                                          (W_Q2, 4, SPLIT), (W_Q2, 2, NARROW), (W_OFF, 4, NARROW)])
 @pytest.mark.parametrize("reverse", [0, 1])
@@ -218,6 +220,7 @@ def test_operator_bitexact(w, world):
 
 
 @pytest.mark.parametrize("w,world,env", [(W_Q2, 2, None), (W_Q2, 4, None), (W_Q1, 2, None), (W_Q1, 8, None),
+                                         (W_FIT, 2, None), (W_FIT, 4, None),
                                          (W_Q3, 2, None), (W_OFF, 4, None), (W_OFF, 2, TC32), (W_OFF, 4, NARROW)])
 def test_vcycle_bitexact(w, world, env):
     b0 = workloads.lattice_vector(w, 31)
