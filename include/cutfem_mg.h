@@ -25,7 +25,9 @@
  *    and the padding columns a >= NL are ignored on input (they may hold any
  *    value, NaN included); output vectors (y of cutfem_apply_operator, x of
  *    cutfem_solve_cg_mg) are 0 there, vectors updated in place (x of
- *    cutfem_smooth / cutfem_vcycle) keep their non-DoF entries unchanged.
+ *    cutfem_smooth / cutfem_vcycle / cutfem_colour_step) keep their non-DoF
+ *    entries unchanged -- except on a fitted box (cutfem_params.domain = 1),
+ *    where their entries on the box boundary are set to 0.
  *    Vectors are owned by the caller; the library never frees them.
  *  - The problem handle owns all device memory it allocates (mesh data,
  *    patch data, local inverses, workspaces); cutfem_destroy releases it.
@@ -47,7 +49,8 @@ enum cutfem_status {
   CUTFEM_ERR_ARG = 1,      /* invalid argument (null pointer, bad level, ...) */
   CUTFEM_ERR_CUDA = 2,     /* a CUDA runtime call failed */
   CUTFEM_ERR_STATE = 3,    /* call out of order (e.g. smooth before build_patches) */
-  CUTFEM_ERR_GEOMETRY = 4, /* the hierarchy violates Omega_l ⊆ Omega_{l-1} (P l.128-129) */
+  CUTFEM_ERR_GEOMETRY = 4, /* the hierarchy violates Omega_l ⊆ Omega_{l-1} (P l.128-129), or a
+                              level has no DoF (the domain misses the background box) */
   CUTFEM_ERR_SIZE = 5      /* a size limit was exceeded (coarse DoFs, patch size) */
 };
 
@@ -67,7 +70,7 @@ typedef struct {
   int symmetric;        /* 1: post-smoother = reverse colour order (R9, needed by CG) */
   int cut_mode;         /* cut-cell operator: 0 = element matrix of bulk + Nitsche terms precomputed
                            from the cut quadrature at setup, 1 = quadrature on the fly */
-  int dim;              /* 2 (circle, default when 0) or 3 (sphere; degree 1..2) */
+  int dim;              /* 2 (circle, default when 0) or 3 (sphere; degree 1..3) */
   double z0, cz;        /* 3D: box corner z and sphere centre z (the box is a cube of side length) */
   int domain;           /* 0: the circle / sphere level set above (unfitted, cut cells, Nitsche +
                            ghost penalty); 1: FITTED box -- Omega = the open background box itself,
