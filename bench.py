@@ -243,24 +243,38 @@ def main():
     # A_j^{-1}, cut-cell element matrices, b_I, x read / written -- what the
     # paper's local solver streams, independent of the patch maps we apply
     cut_method = float(sum(info.cut_method_bytes[:4])) / 4.0 / world
+    one_sweep = info.sweep_ctas[0] > 0 and world == 1   # the cut sweep in one launch (k_cut_sweep)
     kernels = {
         "k_cart_fused_tma (4 Cartesian colours, one launch)": {
             "launches_per_step": 1, "avg_launch_ms": cart_ms, "bytes_per_launch": cart_bytes,
-            "achieved_gbs": cart_bytes / (cart_ms * 1e-3) / 1e9},
-        "k_cut_step7 (one cut colour)": {
+            "achieved_gbs": cart_bytes / (cart_ms * 1e-3) / 1e9}}
+    if one_sweep:
+        # method bytes of the 4 n_c colour steps; the maps the CTAs actually stream
+        # (their dependency cones, redundancy x sweep_redundancy) as implementation bytes
+        sweep_bytes = n_cut_launch * cut_method
+        kernels["k_cut_sweep (all 4 n_c cut colour steps, one launch)"] = {
+            "launches_per_step": 1, "avg_launch_ms": sweeps_ms, "bytes_per_launch": sweep_bytes,
+            "achieved_gbs": sweep_bytes / (sweeps_ms * 1e-3) / 1e9, "ctas": int(info.sweep_ctas[0]),
+            "cone_redundancy": float(info.sweep_redundancy[0]),
+            "implementation_bytes_per_launch": float(info.sweep_map_bytes[0]),
+            "implementation_gbs": float(info.sweep_map_bytes[0]) / (sweeps_ms * 1e-3) / 1e9}
+        cut_name, cut_b, cut_t = "k_cut_sweep (cut sweep, one launch)", sweep_bytes, sweeps_ms
+    else:
+        kernels["k_cut_step7 (one cut colour)"] = {
             "launches_per_step": n_cut_launch, "avg_launch_ms": cut_ms, "bytes_per_launch": cut_method,
             "achieved_gbs": cut_method / (cut_ms * 1e-3) / 1e9,
             "implementation_bytes_per_launch": cut_bytes,
-            "implementation_gbs": cut_bytes / (cut_ms * 1e-3) / 1e9}}
+            "implementation_gbs": cut_bytes / (cut_ms * 1e-3) / 1e9}
+        cut_name, cut_b, cut_t = "k_cut_step7<P=%d> (cut colour step, patch maps)" % p, cut_method, cut_ms
     if per_step["cart_sweep"] >= per_step["cut_sweeps"]:
         dom, d_bytes, d_ms = "k_cart_fused_tma<P=%d> (fused Cartesian sweep)" % p, cart_bytes, cart_ms
     else:
-        dom, d_bytes, d_ms = "k_cut_step7<P=%d> (cut colour step, patch maps)" % p, cut_method, cut_ms
+        dom, d_bytes, d_ms = cut_name, cut_b, cut_t
     achieved = d_bytes / (d_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dom.split("<")[0])
+        traffic = json.load(open(tp)).get(dom.split("<")[0].split(" ")[0])
     # the whole smoothing step on the method's bytes: Cartesian sweep + 4 n_c cut steps
     step_bytes = cart_bytes + n_cut_launch * cut_method
     step_ms = total_ms / args.steps

@@ -100,6 +100,12 @@ typedef struct {
                                   the implementation: per patch
                                   8 (m^2 [A_j^{-1}] + n_cut (p+1)^{2d} [cut-cell matrices]
                                   + 3 m + nnz [b_I, x_I read, x_I written, coupled x_E]) */
+  int sweep_ctas[2];           /* 2D: CTAs of the one-launch cut sweep (forward, reverse) of
+                                  cutfem_smooth on an unpartitioned level; 0 = not built (the
+                                  sweep then runs one launch per colour step) */
+  double sweep_redundancy[2];  /* map bytes the sweep's CTAs stream / map bytes of the 4 n_c
+                                  colour steps (>= 1: patches recomputed near CTA boundaries) */
+  int64_t sweep_map_bytes[2];  /* map bytes streamed by all CTAs of one sweep */
 } cutfem_level_info;
 
 /* ---- setup ------------------------------------------------------------ */

@@ -134,6 +134,11 @@ int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out) 
     }
     for (int c = 0; c < 8; ++c) out->cut_step_bytes[c] = D.gmap ? D.cut_bytes[c] : 0;
     for (int c = 0; c < 8; ++c) out->cut_method_bytes[c] = D.cut_method_bytes[c];
+    for (int d = 0; d < 2; ++d) {
+      out->sweep_ctas[d] = D.sw[d].ok ? D.sw[d].ncta : 0;
+      out->sweep_redundancy[d] = D.sw[d].ok ? D.sw[d].redundancy : 0.0;
+      out->sweep_map_bytes[d] = D.sw[d].ok ? D.sw[d].map_bytes_total : 0;
+    }
     out->n_vol_qp = D.n_vq;
     out->n_surf_qp = D.n_sq;
     out->h = D.a.h;

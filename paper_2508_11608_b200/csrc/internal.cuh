@@ -178,6 +178,16 @@ struct LevelData {
   std::vector<int> wd_off[2];        //   at wdesc + [wd_off[d][s], wd_off[d][s+1])
   int32_t* wcopy = nullptr;          //   copy lists at wcopy + wc_off[d][s], wc_n[d][s] nodes
   std::vector<int> wc_off[2], wc_n[2];
+  // one-launch cut sweeps (sweep.cuh), per direction (0 forward, 1 reverse);
+  // args points at device arrays owned by the problem
+  struct Sweep {
+    bool ok = false;
+    int ncta = 0;
+    size_t smem = 0;
+    double est_us = 0, redundancy = 0;
+    long long map_bytes_total = 0;
+    unsigned char args[160];   // SweepArgs (sweep.cuh), stored opaquely here
+  } sw[2];
 };
 
 struct Params {

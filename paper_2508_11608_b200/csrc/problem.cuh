@@ -8,6 +8,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +23,7 @@
 #include "dim3.cuh"
 #include "tables.cuh"
 #include "comm.cuh"
+#include "sweep.cuh"
 
 namespace cf {
 
@@ -81,6 +83,8 @@ struct Problem {
   int tcx_big = 24;         // ... TCX x 32 cells, TCX in {16, 24, 32} (env CUTFEM_TCX; 24: 18.5 us vs 21.5 us for 32 x 32 at config1)
   bool verbose = false;     // launch decisions on stderr (env CUTFEM_VERBOSE=1)
   bool sym_packed = false;  // 3D: always pack the local inverses symmetric (env CUTFEM_SYM_PACKED=1)
+  bool one_sweep = true;    // 2D cut sweeps in one launch (k_cut_sweep; env CUTFEM_SWEEP=0: one launch per step)
+  int sweep_ng = 0;         // force the CTA count of k_cut_sweep (env CUTFEM_SWEEP_NG)
   // slab partition: comm != nullptr after partition()
   Comm* comm = nullptr;
   static constexpr int HALO = 4;   // halo width in cells (the fused Cartesian apron)
@@ -229,6 +233,8 @@ struct Problem {
     if (const char* e = std::getenv("CUTFEM_CUTMAP")) cut_map = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_VERBOSE")) verbose = std::atoi(e) != 0;
     if (const char* e = std::getenv("CUTFEM_SYM_PACKED")) sym_packed = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_SWEEP")) one_sweep = std::atoi(e) != 0;
+    if (const char* e = std::getenv("CUTFEM_SWEEP_NG")) sweep_ng = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TC32_MIN_N")) tc_big_n = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TCX")) tcx_big = std::atoi(e);
     if (const char* e = std::getenv("CUTFEM_TILEAPPLY_MIN")) tile_apply_min_tiles = std::atoi(e);
@@ -545,6 +551,7 @@ struct Problem {
       for (int c = 0; c < 5; ++c) D.act_off[c] = D.cutp_off[c];
       build_copy_lists(D, D.ent_node, D.ent_col_off, (const CutDesc*)D.desc, ncp);
       if (ncp) method_bytes(D, ncp);
+      if (ncp && D.gmap && one_sweep) build_sweeps(D, ncp);
       sync();
     }
     build_coarse();
@@ -613,9 +620,21 @@ struct Problem {
         sync();
         int64_t off = 0;
         for (int c = 0; c < 8; ++c) D.cut_bytes[c] = 0;
-        for (int k = 0; k < ncp; ++k) {
+        // map blocks of each colour stored in the order of the vertex angle about the
+        // level-set centre: the cut patches along a stretch of the boundary have
+        // adjacent maps (k_cut_sweep moves a CTA's maps with a few large bulk copies)
+        std::vector<int> ord(ncp);
+        for (int k = 0; k < ncp; ++k) ord[k] = k;
+        auto angle = [&](int k) {
+          return std::atan2(D.a.y0 + hd[k].J * D.a.h - D.a.cy, D.a.x0 + hd[k].I * D.a.h - D.a.cx);
+        };
+        for (int c = 0; c < 4; ++c)
+          std::stable_sort(ord.begin() + D.cutp_off[c], ord.begin() + D.cutp_off[c + 1],
+                           [&](int a, int b2) { return angle(a) < angle(b2); });
+        for (int q = 0; q < ncp; ++q) {
+          const int k = ord[q];
           hd[k].map_off = off | ((int64_t)hn[k] << 48);
-          const int64_t blk = 1 + (hn[k] + 7) / 8 + (int64_t)hm[k] * (hm[k] + hn[k]);
+          const int64_t blk = map_hdr_d(hn[k]) + map_rows_d(hm[k], hm[k] + hn[k]);
           off += blk;
           // algorithmic bytes of the patch in its colour step: descriptor, map block,
           // gathered window and b values, written interior values
@@ -636,6 +655,101 @@ struct Problem {
       cudaFree(q);
       allocs.erase(std::remove(allocs.begin(), allocs.end(), q), allocs.end());
     }
+  }
+
+  // programs of the one-launch cut sweeps (sweep.cuh) of a 2D level, both
+  // directions: the patches (interior nodes in map row order, the coupled
+  // exterior nodes in map column order, map rows) go to the host builder,
+  // the program arrays come back to the device
+  void build_sweeps(LevelData& D, int ncp) {
+    const auto t_start = std::chrono::steady_clock::now();
+    const LevelArgs& L = D.a;
+    const int p = prm.p, BS = 2 * p + 1, WS = 4 * p + 1, WW = WS * WS;
+    std::vector<CutDesc> hd(ncp);
+    CF_CUDA(cudaMemcpy(hd.data(), D.desc, sizeof(CutDesc) * ncp, cudaMemcpyDeviceToHost));
+    uint8_t* dix = alloc<uint8_t>((int64_t)ncp * WW);
+    k_map_idx<<<ceil_div(ncp, 128), 128, 0, st>>>((const CutDesc*)D.desc, ncp, (const double*)D.gmap, WW, dix);
+    CF_LAUNCHED();
+    std::vector<uint8_t> hix((size_t)ncp * WW);
+    CF_CUDA(cudaMemcpyAsync(hix.data(), dix, hix.size(), cudaMemcpyDeviceToHost, st));
+    sync();
+    cudaFree(dix);
+    allocs.erase(std::remove(allocs.begin(), allocs.end(), (void*)dix), allocs.end());
+    std::vector<host::SweepPatch> P;
+    for (int k = 0; k < ncp; ++k) {
+      const CutDesc& d = hd[k];
+      const int nnz = (int)(d.map_off >> 48);
+      host::SweepPatch q;
+      q.I = d.I;
+      q.J = d.J;
+      q.colour = (d.I & 1) + 2 * (d.J & 1);
+      for (int loc = 0; loc < BS * BS; ++loc)
+        if ((d.mask[loc >> 6] >> (loc & 63)) & 1ull)
+          q.in.push_back((p * (d.J - 1) + loc / BS) * L.ld + p * (d.I - 1) + loc % BS);
+      if (q.in.empty()) continue;
+      for (int j = 0; j < nnz; ++j) {
+        const int w = hix[(size_t)k * WW + j];
+        q.ex.push_back((p * (d.J - 2) + w / WS) * L.ld + p * (d.I - 2) + w % WS);
+      }
+      q.blk0 = d.map_off & ((1ll << 48) - 1);
+      q.rows = q.blk0 + map_hdr_d(nnz);
+      q.blk1 = q.rows + map_rows_d((int)q.in.size(), (int)(q.in.size() + q.ex.size()));
+      P.push_back(std::move(q));
+    }
+    int dev = 0, nsm = 0, smax = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CF_CUDA(cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    static const char attr_key = 0;   // per-device attribute (dev_once)
+    dev_once(&attr_key, [&] {
+      CF_CUDA(cudaFuncSetAttribute(k_cut_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smax - 1024));
+    });
+    for (int dir = 0; dir < 2; ++dir) {
+      host::SweepProgram R = host::build_sweep(P, L.n, p, L.ld, 4 * prm.n_c, dir, nsm, (size_t)smax, sweep_ng, verbose,
+                                               (L.cx - L.x0) / L.h * p, (L.cy - L.y0) / L.h * p);
+      LevelData::Sweep& W = D.sw[dir];
+      W.ok = R.ok;
+      if (!R.ok) {
+        if (verbose) std::fprintf(stderr, "[cutfem] sweep n=%d dir=%d not built: %s\n", L.n, dir, R.why.c_str());
+        continue;
+      }
+      SweepArgs A = {};
+      auto up = [&](const auto& v) {
+        using T = typename std::decay_t<decltype(v)>::value_type;
+        T* d = alloc<T>((int64_t)v.size());
+        if (!v.empty()) CF_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+        return d;
+      };
+      A.cta = up(R.cta);
+      A.chunk = up(R.chunk);
+      A.run = up(R.run);
+      A.aux = (const unsigned char*)up(R.aux);
+      A.slot_node = up(R.slot_node);
+      A.own = up(R.own);
+      A.gmap = D.gmap;
+      A.gbar = alloc<unsigned long long>(1);
+      CF_CUDA(cudaMemsetAsync(A.gbar, 0, sizeof(unsigned long long), st));
+      A.S = R.S;
+      A.nch = R.nch;
+      A.cb = R.cb;
+      A.off_chunk = R.off_chunk;
+      A.off_run = R.off_run;
+      A.off_xs = R.off_xs;
+      A.off_bs = R.off_bs;
+      A.off_v = R.off_v;
+      A.off_ring = R.off_ring;
+      static_assert(sizeof(SweepArgs) <= sizeof(W.args), "SweepArgs fits LevelData::Sweep::args");
+      std::memcpy(W.args, &A, sizeof(A));
+      W.ncta = R.ncta;
+      W.smem = R.smem;
+      W.est_us = R.est_us;
+      W.redundancy = R.redundancy;
+      W.map_bytes_total = R.map_bytes_total;
+      sync();
+    }
+    if (verbose)
+      std::fprintf(stderr, "[cutfem] sweep programs n=%d built in %.1f ms\n", L.n,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
   }
 
   // method bytes of one cut colour step: per
@@ -1398,6 +1512,14 @@ struct Problem {
         cut_pp_launch(l, (const CutDesc*)D.wdesc + D.wd_off[d][s], D.wd_off[d][s + 1] - D.wd_off[d][s],
                       D.wcopy + D.wc_off[d][s], D.wc_n[d][s], bufs[s & 1], bufs[(s + 1) & 1], b);
       halo_n(l, x);
+      return;
+    }
+    if (!comm && one_sweep && D.sw[reverse ? 1 : 0].ok) {   // the whole cut sweep in one launch (sweep.cuh)
+      const LevelData::Sweep& W = D.sw[reverse ? 1 : 0];
+      SweepArgs A;
+      std::memcpy(&A, W.args, sizeof(A));
+      launch(k_cut_sweep, dim3(W.ncta), dim3(32 * (SW_NW + 1)), W.smem, A, x, b);
+      CF_LAUNCHED();
       return;
     }
     int prev = 4, s = 0;

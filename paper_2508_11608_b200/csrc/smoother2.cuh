@@ -57,6 +57,25 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 
+// patch-map block layout (R13): [int nnz, 0, 8 pad bytes][nnz uint8 window
+// indices, padded to 16 bytes][the m x K map, K = m + nnz].  A map row is
+// summed by tpr lanes (map_tpr: 4, 2 or 1 by m); lane h takes columns
+// h, h + 2 tpr, ... into one accumulator and h + tpr, h + 3 tpr, ... into a
+// second.  The map is stored in column blocks of B = 2 tpr columns, K padded
+// to a multiple of B with zeros: element (i, c), c = B j + h + e tpr (e = 0,
+// 1), at (j m + i) B + 2 h + e -- the two columns a lane needs next are one
+// 16-byte word, and the 8 rows x B columns that 8 row groups read at once
+// are consecutive (no shared-memory bank conflicts).  Blocks start 16-byte
+// aligned (bulk copies, k_cut_sweep).
+__host__ __device__ constexpr long long map_hdr_d(int nnz) { return 2 + 2 * ((nnz + 15) / 16); }
+__host__ __device__ constexpr int map_tpr(int m) { return m * 4 <= 128 ? 4 : (m * 2 <= 128 ? 2 : 1); }
+__host__ __device__ constexpr int map_kp(int m, int K) { return (K + 2 * map_tpr(m) - 1) / (2 * map_tpr(m)) * (2 * map_tpr(m)); }
+__host__ __device__ constexpr long long map_rows_d(int m, int K) { return (long long)m * map_kp(m, K); }
+__host__ __device__ constexpr long long map_index(int m, int i, int c) {
+  return ((long long)(c / (2 * map_tpr(m))) * m + i) * (2 * map_tpr(m)) + 2 * ((c % (2 * map_tpr(m))) % map_tpr(m)) +
+         (c % (2 * map_tpr(m))) / map_tpr(m);
+}
+
 __device__ __forceinline__ int desc_kind(const CutDesc& d, int wx, int wy) {
   return (d.kinds >> (2 * (wy * 4 + wx))) & 3;
 }
@@ -1607,23 +1626,25 @@ __global__ void k_map_compact(const CutDesc* desc, const int64_t* dense_off, con
     nnz = c;
     ((int*)out)[0] = c;
     ((int*)out)[1] = 0;
-    uint8_t* ob = (uint8_t*)(out + 1);
-    for (int q = 0; q < ((c + 7) & ~7); ++q) ob[q] = q < c ? idx[q] : 0;
+    out[1] = 0.0;
+    uint8_t* ob = (uint8_t*)(out + 2);
+    for (int q = 0; q < ((c + 15) & ~15); ++q) ob[q] = q < c ? idx[q] : 0;
   }
   __syncthreads();
-  const int Kc = m + nnz;
-  double* rows = out + 1 + (nnz + 7) / 8;
-  for (int e = threadIdx.x; e < m * Kc; e += blockDim.x) {
-    const int i = e / Kc, c = e - i * Kc;
-    rows[e] = c < m ? g[(size_t)i * K + c] : g[(size_t)i * K + m + idx[c - m]];
+  const int Kc = m + nnz, Kp = map_kp(m, Kc), tpr = map_tpr(m), B = 2 * tpr;
+  double* rows = out + map_hdr_d(nnz);
+  for (int e = threadIdx.x; e < m * Kp; e += blockDim.x) {
+    const int j = e / (B * m), rem = e - j * B * m, i = rem / B, pos = rem % B;
+    const int c = B * j + pos / 2 + (pos % 2) * tpr;
+    rows[e] = c >= Kc ? 0.0 : (c < m ? g[(size_t)i * K + c] : g[(size_t)i * K + m + idx[c - m]]);
   }
 }
 
 template <int P>
 struct CutMapSmem {
   static constexpr int BS = 2 * P + 1, WS = 4 * P + 1, MM = BS * BS, WW = WS * WS;
-  static constexpr int maxK = MM + WW;
-  // descriptor | v[maxK] | G_j rows [MM x maxK] | Lc[MM] shorts | exterior indices, window mask
+  static constexpr int maxK = MM + WW + 7;   // K padded to a multiple of 2 tpr <= 8 (map_kp)
+  // descriptor | v[maxK] | G_j [MM x maxK] | Lc[MM] shorts | exterior indices, window mask
   static constexpr size_t gs_off = 64 + (((size_t)maxK * 8 + 15) & ~(size_t)15);
   static constexpr size_t bytes = gs_off + (size_t)MM * maxK * 8 + 2 * MM + 2 * WW + 16;
 };
@@ -1651,14 +1672,14 @@ __device__ __forceinline__ void cut7_prologue(const CutDesc* desc, int k, const 
   // interior), so the gather needs no mask
   const double* blk = G + (d.map_off & ((1ll << 48) - 1));
   const int nnz = (int)(d.map_off >> 48), K = m + nnz;
-  const double* rows = blk + 1 + (nnz + 7) / 8;
-  for (int e = gt; e < m * K; e += NT) cp_async8(Gs + e, rows + e);
+  const double* rows = blk + map_hdr_d(nnz);
+  for (int e = gt; e < m * map_kp(m, K); e += NT) cp_async8(Gs + e, rows + e);
   for (int loc = gt; loc < MM; loc += NT) {
     const unsigned long long word = d.mask[loc >> 6];
     if ((word >> (loc & 63)) & 1ull)
       Lc[(loc >> 6 ? __popcll(d.mask[0]) : 0) + __popcll(word & ((1ull << (loc & 63)) - 1ull))] = (short)loc;
   }
-  for (int j = gt; j < nnz; j += NT) ix[j] = ((const uint8_t*)(blk + 1))[j];
+  for (int j = gt; j < nnz; j += NT) ix[j] = ((const uint8_t*)(blk + 2))[j];
   group_sync(bar, NT);   // Lc, ix visible (in k_cut_step7: before griddepcontrol.wait)
 }
 
@@ -1685,19 +1706,22 @@ __device__ __forceinline__ void cut7_main(const LevelArgs& L, const double* R, d
   }
   cp_async_wait_all();
   group_sync(bar, NT);
-  // x_I^new = G_j v: TPR threads per row (power of two), shuffle-reduced
-  const int tpr = m * 4 <= NT ? 4 : (m * 2 <= NT ? 2 : 1);
+  // x_I^new = G_j v: TPR threads per row (power of two), shuffle-reduced; lane
+  // h sums columns h + 2 tpr j (a0c) and h + tpr + 2 tpr j (a1c), j = 0, 1, ...
+  // (the map's column-block layout, map_index; the order k_cut_sweep repeats)
+  const int tpr = map_tpr(m);
+  static_assert(NT >= 128, "the map layout assumes 128-thread row groups (map_tpr)");
   for (int r0 = 0; r0 < m; r0 += NT / tpr) {
     const int i = r0 + gt / tpr, h = gt % tpr;
     double a0c = 0.0, a1c = 0.0;
     if (i < m) {
-      const double* g = Gs + (size_t)i * K;
+      const double* g = Gs + 2 * tpr * i + 2 * h;
       int c = h;
-      for (; c + tpr < K; c += 2 * tpr) {
-        a0c = fma(g[c], v[c], a0c);
-        a1c = fma(g[c + tpr], v[c + tpr], a1c);
+      for (; c + tpr < K; c += 2 * tpr, g += 2 * tpr * m) {
+        a0c = fma(g[0], v[c], a0c);
+        a1c = fma(g[1], v[c + tpr], a1c);
       }
-      if (c < K) a0c = fma(g[c], v[c], a0c);
+      if (c < K) a0c = fma(g[0], v[c], a0c);
     }
     double z = a0c + a1c;
     for (int o = tpr >> 1; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
