@@ -1338,9 +1338,15 @@ struct Problem {
       std::fprintf(stderr, "[cutfem] level %d: %d fused tiles (%d ext), %d co-resident -> %s\n", l,
                    D.n_fused_tiles, D.n_fused_ext, cap, (!cart_split && D.n_fused_tiles <= cap) ? "in place" : "split");
     }
+    // forward step followed by the one-launch cut sweep: its patch maps go towards
+    // L2 while the Cartesian sweep runs (the sweep streams them right after)
+    const bool pf = !reverse && !comm && one_sweep && D.sw[0].ok && D.gmap;
+    const unsigned char* pfp = pf ? (const unsigned char*)D.gmap : nullptr;
+    const unsigned long long pfb = pf ? (unsigned long long)D.n_gmap * 8ull : 0ull;
     if (!cart_split && D.n_fused_tiles <= cap) {
       launch_ex(true, k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
-                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, D.tflag, D.tflag_stride);
+                (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, D.tflag, D.tflag_stride, pfp,
+                pfb);
       CF_LAUNCHED();
       cart_done(l, x, reverse);
       return;
@@ -1348,11 +1354,12 @@ struct Problem {
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
     if (D.n_fused_ext)
       launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
-             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned*)nullptr, 0);
+             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned*)nullptr, 0, pfp, pfb);
     CF_LAUNCHED();
     halo_n(l, D.xs);
     launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
-           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, (unsigned*)nullptr, 0);
+           (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, (unsigned*)nullptr, 0,
+           (const unsigned char*)nullptr, 0ull);
     CF_LAUNCHED();
     cart_done(l, x, reverse);
     return;

@@ -1050,7 +1050,8 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
                                                         const __grid_constant__ CUtensorMap tmb, LevelArgs L,
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* xout, int reverse, int s0, int s1,
-                                                        unsigned* tflag, int tstride) {
+                                                        unsigned* tflag, int tstride, const unsigned char* pf,
+                                                        unsigned long long pf_bytes) {
   using C = CartMMA<P>;
   using S = CartTmaSmem<P, TC, TCX>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
@@ -1065,6 +1066,10 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
   double* Xs = (double*)(smraw + S::head);     // x tile [RW][RWP]; the b tile follows at Xs + TD
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n = L.n;
   pdl_trigger();
+  if (tid == 0 && pf_bytes) {   // this CTA's slice of [pf, pf + pf_bytes) towards L2 (the next kernel's data)
+    const unsigned long long sl = ((pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15ull, a = sl * blockIdx.x;
+    if (a < pf_bytes) prefetch_l2(pf + a, (size_t)(pf_bytes - a < sl ? pf_bytes - a : sl));
+  }
   int ko[KS];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {

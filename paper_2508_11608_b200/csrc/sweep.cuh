@@ -57,7 +57,8 @@ static_assert(sizeof(SweepRun) == 16, "SweepRun is 16 bytes");
 struct SweepChunk {       // one ring fill: consecutive tasks of one step
   unsigned run0;          // CTA-relative first run
   unsigned short nrun, nrows;
-  unsigned ngat;          // gather entries (first chunk of a step), else 0
+  unsigned short ngat;    // gather entries (first chunk of a step), else 0
+  unsigned short row0;    // rows of the step's earlier chunks (round-robin row assignment)
   unsigned bytes;         // bytes landing in the slot (runs + row jobs + gather list)
   unsigned rj_soff;       // slot-relative offset of [row jobs | gather list] (the aux copy)
   unsigned gat_soff;      // slot-relative offset of the gather list
@@ -200,7 +201,8 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
     __threadfence();
     ticket = atomicAdd(A.gbar, 1ull);
   }
-  int s = -1;
+  int s = -1, sl = 0;
+  unsigned par = 0;
 #ifdef CF_TIMING
   long long tacc[4] = {0, 0, 0, 0}, tq = clock64();
 #define SW_LAP(i)                      \
@@ -216,10 +218,10 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
 #endif
   for (int k = 0; k < C.nchunk; ++k) {
     SW_LAP(3);
-    mbar_wait(&full[k % A.nch], (k / A.nch) & 1);
+    mbar_wait(&full[sl], par);
     SW_LAP(0);
     const SweepChunk& ch = CH[k];
-    const unsigned char* slot = ring + (size_t)(k % A.nch) * A.cb;
+    const unsigned char* slot = ring + (size_t)sl * A.cb;
     if (ch.ngat) {   // first chunk of a step: v = [b_I ; x_E] of its tasks, from the state after the previous step
       ++s;
       if (s == 1) SW_TSTAMP(2);
@@ -234,13 +236,16 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
     }
     SW_LAP(1);
     const unsigned long long* rj = (const unsigned long long*)(slot + ch.rj_soff);
-    const int nrows = ch.nrows;
-    // rows over 4-lane groups (warp-uniform trip count: every lane reaches the shuffles).
-    // x_I^new[i] = G_j[i,:] v in cut7_main's order (lane h: columns h + 2 tpr j into
-    // a0c, h + tpr + 2 tpr j into a1c) and shuffle tree: bit-identical to k_cut_step7
-    for (int Rb = warp * 8; Rb < nrows; Rb += NT / 4) {
-      const int R = Rb + (lane >> 2);
-      const bool act = R < nrows;
+    const int nrows = ch.nrows, row0 = ch.row0;
+    // rows over 4-lane groups, round-robin over the step (group warp*8 + lane/4
+    // takes the step's rows congruent to it mod NT/4; warp-uniform trip count:
+    // every lane reaches the shuffles).  x_I^new[i] = G_j[i,:] v in cut7_main's
+    // order (lane h: columns h + 2 tpr j into a0c, h + tpr + 2 tpr j into a1c)
+    // and shuffle tree: bit-identical to k_cut_step7
+    const int first = row0 - ((row0 - warp * 8) % (NT / 4) + (NT / 4)) % (NT / 4);
+    for (int Rb = first; Rb < row0 + nrows; Rb += NT / 4) {
+      const int R = Rb + (lane >> 2) - row0;
+      const bool act = R >= 0 && R < nrows;
       const unsigned long long job = act ? rj[R] : 0ull;
       const int K = (int)((job >> 32) & 0xffu), m = (int)((job >> 40) & 0x3fu);
       const int tpr = 1 << (int)((job >> 46) & 3u), h = lane & 3, B = 2 * tpr;
@@ -266,7 +271,11 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
     }
     SW_LAP(2);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[k % A.nch]);
+    if (lane == 0) mbar_arrive(&empty[sl]);
+    if (++sl == A.nch) {
+      sl = 0;
+      par ^= 1u;
+    }
   }
   consumer_sync();
 #ifdef CF_TIMING
@@ -620,6 +629,7 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     c.own0 = (int)R.own.size();
     c.nown = (int)best.owned[g].size();
     std::vector<unsigned> voff;
+    size_t step_rows = 0;
     int cur_step = -1;
     for (int ci = 0; ci < (int)chunks[g].size(); ++ci) {
       const TmpChunk& tc = chunks[g][ci];
@@ -663,6 +673,9 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
                                       (unsigned)t.slot_of[P[k].in[r]]));
       }
       ch.nrows = (unsigned short)rows.size();
+      if (tc.first) step_rows = 0;
+      ch.row0 = (unsigned short)step_rows;
+      step_rows += rows.size();
       ch.rj_soff = off;
       const size_t aux0 = R.aux.size();
       ch.aux_src = (long long)aux0;
@@ -683,7 +696,11 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
             else gl.push_back((uint16_t)t.slot_of[P[k].ex[c - m]]);
           }
         }
-        ch.ngat = (unsigned)gl.size();
+        if (gl.size() > 65535) {
+          R.why = "a step's gather list exceeds 65535 entries";
+          return R;
+        }
+        ch.ngat = (unsigned short)gl.size();
         ch.gat_soff = off;
         const size_t a1 = R.aux.size();
         R.aux.resize(a1 + r16(2ll * gl.size()), 0);

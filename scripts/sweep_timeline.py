@@ -29,7 +29,10 @@ for it in range(4):
     if not os.environ.get("NOFLUSH"):
         flush.fill_(1.0)
     torch.cuda.synchronize()
-    g.colour_step(lvl, 3, 0, x, b)
+    if os.environ.get("STEP"):
+        g.smooth(lvl, x, b)
+    else:
+        g.colour_step(lvl, 3, 0, x, b)
     torch.cuda.synchronize()
 buf = np.zeros((n, 8), dtype=np.uint64)
 assert lib.cutfem_debug_timers(buf.ctypes.data, n) == 0
