@@ -129,6 +129,9 @@ struct LevelData {
   unsigned* tflag = nullptr;         // in-place fused sweep: per-tile "region loaded" counters, (tx+2) x (ty+2)
   int tflag_stride = 0;              //   with a border; tiles not launched hold 0x7fffffff
   int n_fused_ext = 0;
+  int* fpl = nullptr;                // in-place fused sweep: precomputed patch lists [dir][tile][4][maxp] (k_fused_plists)
+  int* fpc = nullptr;                //   and counts [dir][tile][4], tiles of the tx x ty grid
+  int fpl_tx = 0, fpl_nt = 0, fpl_maxp = 0;
   int n_cutp[8] = {};
   int cutp_off[9] = {};
   int* cutp_list = nullptr;          // packed I + (n+1) J

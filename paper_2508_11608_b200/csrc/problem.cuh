@@ -488,6 +488,18 @@ struct Problem {
         D.fused_ext = te;
         D.tflag_stride = tx + 2;
         D.tflag = alloc<unsigned>((int64_t)(tx + 2) * (ty + 2));
+        if (p <= 3) {   // patch lists of every (direction, tile, pass) of the in-place TMA sweep
+          const int H = 4, RWX = (TCX + 2 * H) * p + 1, RWP = (RWX + 1) & ~1;
+          const int maxp = ((TCX + 7) / 2 + 1) * ((TC + 7) / 2 + 1);
+          D.fpl_tx = tx;
+          D.fpl_nt = nt;
+          D.fpl_maxp = maxp;
+          D.fpl = alloc<int>((int64_t)2 * nt * 4 * maxp);
+          D.fpc = alloc<int>((int64_t)2 * nt * 4);
+          k_fused_plists<<<ceil_div(2 * nt * 4, 128), 128, 0, st>>>(n, p, TC, TCX, H, RWP, maxp, D.vkind, tx, ty, D.fpl,
+                                                                     D.fpc);
+          CF_LAUNCHED();
+        }
         reset_tile_flags(D, ty);
       }
       D.cart_tiles = alloc<int>(tiles.size());
@@ -1346,7 +1358,9 @@ struct Problem {
     if (!cart_split && D.n_fused_tiles <= cap) {
       launch_ex(true, k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tmx, tmb, D.a,
                 (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 0, 4, D.tflag, D.tflag_stride, pfp,
-                pfb);
+                pfb, D.fpl && D.fpl_maxp == S::maxp ? (const int*)D.fpl + (size_t)(reverse ? 1 : 0) * D.fpl_nt * 4 * D.fpl_maxp
+                                                    : (const int*)nullptr,
+                (const int*)D.fpc + (size_t)(reverse ? 1 : 0) * D.fpl_nt * 4, D.fpl_tx);
       CF_LAUNCHED();
       cart_done(l, x, reverse);
       return;
@@ -1354,12 +1368,13 @@ struct Problem {
     const CUtensorMap tms = host::lattice_tmap(D.xs, D.a.nl, D.a.ld, S::RWP, S::RW);
     if (D.n_fused_ext)
       launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_ext), dim3(NT), S::bytes, tmx, tmb, D.a,
-             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned*)nullptr, 0, pfp, pfb);
+             (const int*)D.fused_ext, (const uint8_t*)D.vkind, G, D.xs, reverse, 0, 2, (unsigned*)nullptr, 0, pfp, pfb,
+             (const int*)nullptr, (const int*)nullptr, 0);
     CF_LAUNCHED();
     halo_n(l, D.xs);
     launch(k_cart_fused_tma<P, TC, NT, TCX>, dim3(D.n_fused_tiles), dim3(NT), S::bytes, tms, tmb, D.a,
            (const int*)D.fused_tiles, (const uint8_t*)D.vkind, G, x, reverse, 2, 4, (unsigned*)nullptr, 0,
-           (const unsigned char*)nullptr, 0ull);
+           (const unsigned char*)nullptr, 0ull, (const int*)nullptr, (const int*)nullptr, 0);
     CF_LAUNCHED();
     cart_done(l, x, reverse);
     return;

@@ -1024,13 +1024,40 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* ctr) {
   __syncthreads();
 }
 
+// setup: the compacted Cartesian patch lists of every (direction, tile of the
+// fused grid, pass) of the in-place fused sweep (passes 0..3, radius 3 - s),
+// as k_cart_fused_tma would compact them, in vertex order: lists
+// [dir][tile][4][maxp] (block origins in the region), counts [dir][tile][4]
+__global__ void k_fused_plists(int n, int P, int TC, int TCX, int H, int RWP, int maxp, const uint8_t* vk, int tx,
+                               int ty, int* lists, int* counts) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = tx * ty;
+  if (q >= 2 * nt * 4) return;
+  const int s = q % 4, t = (q / 4) % nt, dir = q / (4 * nt);
+  const int ci0 = (t % tx) * TCX, cj0 = (t / tx) * TC;
+  const int c = dir ? 3 - s : s, rad = 3 - s;
+  const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
+  const int nvx = (ci0 + TCX + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
+  int* out = lists + ((size_t)(dir * nt + t) * 4 + s) * maxp;
+  int cnt = 0;
+  for (int pj = 0; pj < nvy; ++pj)
+    for (int pi = 0; pi < nvx; ++pi) {
+      const int I = ilo + 2 * pi, J = jlo + 2 * pj;
+      if (I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART)
+        out[cnt++] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
+    }
+  counts[(dir * nt + t) * 4 + s] = cnt;
+}
+
 template <int P, int TC, int TCX = TC>
 struct CartTmaSmem {
   // TC = cells per tile in y (rows: the partitioned direction), TCX in x
   static constexpr int H = 4, RW = (TC + 2 * H) * P + 1, RWX = (TCX + 2 * H) * P + 1, RWP = (RWX + 1) & ~1;
   static constexpr int tile_doubles = (RW * RWP + 15) & ~15;   // 128-byte aligned tiles (TMA destination)
   static constexpr int maxp = ((TCX + 7) / 2 + 1) * ((TC + 7) / 2 + 1);
-  static constexpr int head = ((32 + 4 * 4 * maxp) + 127) & ~127;   // mbarrier, 4 counts, 4 pass patch lists
+  static constexpr int VW = TCX + 7, VH = TC + 7;   // vertex kinds of the region (widest pass: radius 3)
+  static constexpr int vk_off = 32 + 4 * 4 * maxp;
+  static constexpr int head = ((vk_off + VW * VH) + 127) & ~127;   // mbarrier, 4 counts, 4 pass patch lists, vertex kinds
   static constexpr size_t bytes = head + 2 * tile_doubles * sizeof(double);
 };
 
@@ -1051,7 +1078,8 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
                                                         const int* tiles, const uint8_t* vk, const double* G,
                                                         double* xout, int reverse, int s0, int s1,
                                                         unsigned* tflag, int tstride, const unsigned char* pf,
-                                                        unsigned long long pf_bytes) {
+                                                        unsigned long long pf_bytes, const int* gpl,
+                                                        const int* gpc, int gtx) {
   using C = CartMMA<P>;
   using S = CartTmaSmem<P, TC, TCX>;
   constexpr int NE = C::NE, NI = C::NI, NINT = C::NINT, K = C::K, KS = C::KS;
@@ -1092,38 +1120,82 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
   const int tile = tiles[blockIdx.x];
   const int ci0 = (tile & 0xffff) * TCX, cj0 = (tile >> 16) * TC;
   const int a0 = P * (ci0 - H), b0 = P * (cj0 - H);
-  if (tid < 4) pcount[tid] = 0;
-  if (tid == 0) mbar_init(bar, 1);
-  __syncthreads();
-  // compact the Cartesian patches of every pass (setup data: before the PDL
-  // wait, overlapping the predecessor's tail)
-  for (int s = s0; s < s1; ++s) {
-    const int c = reverse ? 3 - s : s, rad = s1 - 1 - s;
-    const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
-    const int nvx = (ci0 + TCX + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
-    for (int q = tid; q < nvx * nvy; q += NT) {
-      const int pj = q / nvx, pi = q - pj * nvx;
-      const int I = ilo + 2 * pi, J = jlo + 2 * pj;
-      if (I >= 0 && J >= 0 && I <= n && J <= n && vk[J * (n + 1) + I] == V_CART)
-        plists[s * MAXP + atomicAdd(pcount + s, 1)] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
+  CF_TSTAMP(0);
+  unsigned* myflag = tflag ? tflag + ((tile >> 16) + 1) * tstride + (tile & 0xffff) + 1 : nullptr;
+  unsigned fbase = 0;
+  if (gpl && s0 == 0 && s1 == 4) {
+    // x and b regions by TMA right away (after the predecessor completed) while
+    // every thread loads the tile's patch lists, precomputed at setup
+    // (k_fused_plists) in one round of independent loads
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      pdl_wait();
+      mbar_expect_tx(bar, 2u * RW * RWP * sizeof(double));
+      tma_load_2d(Xs, &tmx, a0, b0, bar);
+      tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
+      if (myflag) fbase = *(volatile unsigned*)myflag;
+    }
+    const int gt = (tile >> 16) * gtx + (tile & 0xffff);
+    const int* src = gpl + (size_t)gt * 4 * MAXP;
+    constexpr int NL = (4 * MAXP + NT - 1) / NT;
+    int r[NL];
+#pragma unroll
+    for (int u = 0; u < NL; ++u) r[u] = (tid + u * NT < 4 * MAXP) ? __ldg(src + tid + u * NT) : 0;
+    const int cn = tid < 4 ? __ldg(gpc + gt * 4 + tid) : 0;
+#pragma unroll
+    for (int u = 0; u < NL; ++u)
+      if (tid + u * NT < 4 * MAXP) plists[tid + u * NT] = r[u];
+    if (tid < 4) pcount[tid] = cn;
+    __syncthreads();
+    CF_TSTAMP(1);
+  } else {
+    if (tid < 4) pcount[tid] = 0;
+    if (tid == 0) mbar_init(bar, 1);
+    uint8_t* vks = smraw + S::vk_off;   // vertex kinds of [ci0 - 3, ci0 + TCX + 3] x [cj0 - 3, cj0 + TC + 3]
+    // the region's vertex kinds (setup data: before the PDL wait; outside the mesh: none)
+    constexpr int NVK = (S::VW * S::VH + NT - 1) / NT;
+    uint8_t r[NVK];
+#pragma unroll
+    for (int u = 0; u < NVK; ++u) {
+      const int q = tid + u * NT, I = ci0 - 3 + q % S::VW, J = cj0 - 3 + q / S::VW;
+      r[u] = (q < S::VW * S::VH && I >= 0 && J >= 0 && I <= n && J <= n) ? __ldg(vk + J * (n + 1) + I) : (uint8_t)V_NONE;
+    }
+#pragma unroll
+    for (int u = 0; u < NVK; ++u)
+      if (tid + u * NT < S::VW * S::VH) vks[tid + u * NT] = r[u];
+    __syncthreads();
+    CF_TSTAMP(1);
+    if (tid == 0) {   // x and b regions by TMA (after the predecessor completed); the patch lists are compacted meanwhile
+      pdl_wait();
+      mbar_expect_tx(bar, 2u * RW * RWP * sizeof(double));
+      tma_load_2d(Xs, &tmx, a0, b0, bar);
+      tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
+      if (myflag) fbase = *(volatile unsigned*)myflag;
+    }
+    // compact the Cartesian patches of every pass
+    for (int s = s0; s < s1; ++s) {
+      const int c = reverse ? 3 - s : s, rad = s1 - 1 - s;
+      const int ilo = ci0 - rad + ((ci0 - rad - (c & 1)) & 1), jlo = cj0 - rad + ((cj0 - rad - (c >> 1)) & 1);
+      const int nvx = (ci0 + TCX + rad - ilo) / 2 + 1, nvy = (cj0 + TC + rad - jlo) / 2 + 1;
+      for (int q = tid; q < nvx * nvy; q += NT) {
+        const int pj = q / nvx, pi = q - pj * nvx;
+        const int I = ilo + 2 * pi, J = jlo + 2 * pj;
+        if (vks[(J - cj0 + 3) * S::VW + I - ci0 + 3] == V_CART)
+          plists[s * MAXP + atomicAdd(pcount + s, 1)] = P * (J - 1 - (cj0 - H)) * RWP + P * (I - 1 - (ci0 - H));
+      }
     }
   }
   pdl_wait();
-  unsigned* myflag = tflag ? tflag + ((tile >> 16) + 1) * tstride + (tile & 0xffff) + 1 : nullptr;
-  unsigned fbase = 0;
-  if (tid == 0) {
-    mbar_expect_tx(bar, 2u * RW * RWP * sizeof(double));
-    tma_load_2d(Xs, &tmx, a0, b0, bar);
-    tma_load_2d(Xs + TD, &tmb, a0, b0, bar);
-    if (myflag) fbase = *(volatile unsigned*)myflag;
-  }
+  CF_TSTAMP(2);
   for (int s = s0; s < s1; ++s) {
     const int* plist = plists + s * MAXP;
     if (s == s0) {
       mbar_wait(bar, 0);
+      CF_TSTAMP(3);
       if (myflag && tid == 0) st_release_u32(myflag, fbase + 1u);   // region loaded: neighbours may write
     }
     __syncthreads();
+    if (s == s0 + 2) CF_TSTAMP(4);
     const int np = pcount[s], ng = (np + 7) / 8;
 #ifndef CF_CART_GPW
 #define CF_CART_GPW 1   // groups of 8 patches per warp iteration (2: measured no faster, spills at 16-cell tiles)
@@ -1180,6 +1252,7 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
     mbar_wait(bar, 0);
     if (myflag && tid == 0) st_release_u32(myflag, fbase + 1u);
   }
+  CF_TSTAMP(5);
   if (myflag) {   // the 8 neighbours have loaded their aprons (which hold our owned nodes)
     const unsigned want = __shfl_sync(0xffffffffu, fbase, 0) + 1u;   // (warp 0: thread 0's base)
     if (tid < 9 && tid != 4) {
@@ -1189,6 +1262,7 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
     }
     __syncthreads();
   }
+  CF_TSTAMP(6);
   // owned nodes [P ci0, P (ci0 + TC)) (+ the last lattice line), warp per row
   const int ahi = (ci0 + TCX >= n) ? L.nl : P * (ci0 + TCX), bhi = (cj0 + TC >= n) ? L.nl : P * (cj0 + TC);
   for (int bb = P * cj0 + warp; bb < bhi; bb += NT / 32) {
@@ -1196,6 +1270,7 @@ __global__ void __launch_bounds__(NT, (TC >= 32 || P >= 3) ? 2 : CF_CART_MINB) k
     double* dst = xout + (size_t)bb * L.ld;
     for (int a = P * ci0 + lane; a < ahi; a += 32) dst[a] = src[a];
   }
+  CF_TSTAMP(7);
 }
 
 }  // namespace cf
