@@ -1540,7 +1540,7 @@ struct Problem {
       const LevelData::Sweep& W = D.sw[reverse ? 1 : 0];
       SweepArgs A;
       std::memcpy(&A, W.args, sizeof(A));
-      launch(k_cut_sweep, dim3(W.ncta), dim3(32 * (SW_NW + 1)), W.smem, A, x, b);
+      launch_ex(true, k_cut_sweep, dim3(W.ncta), dim3(32 * (SW_NW + 1)), W.smem, A, x, b);   // co-resident (ticket wait)
       CF_LAUNCHED();
       return;
     }
