@@ -207,6 +207,12 @@ struct Problem {
     cfg.numAttrs = na;
     CF_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
   }
+  int num_sms() {
+    int dev = 0, nsm = 0;
+    CF_CUDA(cudaGetDevice(&dev));
+    CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    return nsm;
+  }
   // CTAs of `kern` (256 threads, smem bytes) that fit on the device at once
   template <typename K>
   int coresident(K kern, size_t smem, int threads = 256) {
@@ -673,7 +679,7 @@ struct Problem {
   // directions: the patches (interior nodes in map row order, the coupled
   // exterior nodes in map column order, map rows) go to the host builder,
   // the program arrays come back to the device
-  void build_sweeps(LevelData& D, int ncp) {
+  void build_sweeps(LevelData& D, int ncp, int own_b0 = -1, int own_b1 = -1, int max_ctas = 0) {
     const auto t_start = std::chrono::steady_clock::now();
     const LevelArgs& L = D.a;
     const int p = prm.p, BS = 2 * p + 1, WS = 4 * p + 1, WW = WS * WS;
@@ -712,13 +718,14 @@ struct Problem {
     CF_CUDA(cudaGetDevice(&dev));
     CF_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CF_CUDA(cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (max_ctas > 0) nsm = std::min(nsm, max_ctas);
     static const char attr_key = 0;   // per-device attribute (dev_once)
     dev_once(&attr_key, [&] {
       CF_CUDA(cudaFuncSetAttribute(k_cut_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smax - 1024));
     });
     for (int dir = 0; dir < 2; ++dir) {
       host::SweepProgram R = host::build_sweep(P, L.n, p, L.ld, 4 * prm.n_c, dir, nsm, (size_t)smax, sweep_ng, verbose,
-                                               (L.cx - L.x0) / L.h * p, (L.cy - L.y0) / L.h * p);
+                                               (L.cx - L.x0) / L.h * p, (L.cy - L.y0) / L.h * p, own_b0, own_b1);
       LevelData::Sweep& W = D.sw[dir];
       W.ok = R.ok;
       if (!R.ok) {
@@ -1144,6 +1151,12 @@ struct Problem {
       D.act_desc = dd;
       build_copy_lists(D, dn, col_off, dd, (int)kd.size());
       if (D.wide) build_wide(D, hd, he, hn);
+      // the one-launch cut sweep over the rank's owned rows (wide halo: every
+      // cone input is valid after the one exchange before the sweep); ranks that
+      // share a GPU (LocalComm) split its SMs, so every cooperative grid fits
+      for (int d2 = 0; d2 < 2; ++d2) D.sw[d2].ok = false;
+      if (D.wide && one_sweep && D.gmap && ncp)
+        build_sweeps(D, ncp, D.r0, D.r1, dynamic_cast<LocalComm*>(c) ? std::max(1, num_sms() / W) : 0);
       // k_band ranges: cut cells and x-faces in cell rows [c0 - HALO, c1 + HALO),
       // y-faces (j | j+1) with j in [c0 - HALO, c1 + HALO - 1); the lists are sorted by j n + i
       const int lo = std::max(0, D.c0 - HALO), hi = std::min(n, D.c1 + HALO);
@@ -1164,6 +1177,13 @@ struct Problem {
       D.at0 = std::max(0, (D.c0 - 2) / 16);
       D.at1 = std::min(nt, ceil_div(D.c1 + 2, 16));
     }
+    // replicated (coarser) levels keep their whole-level one-launch sweeps; ranks
+    // sharing a GPU rebuild them on their share of the SMs
+    if (dynamic_cast<LocalComm*>(c) && W > 1)
+      for (int l = 1; l < prm.n_levels; ++l) {
+        LevelData& D = lv[l];
+        if (!D.part && D.sw[0].ok && D.gmap) build_sweeps(D, D.cutp_off[4], -1, -1, std::max(1, num_sms() / W));
+      }
     comm = c;
   }
 
@@ -1352,7 +1372,7 @@ struct Problem {
     }
     // forward step followed by the one-launch cut sweep: its patch maps go towards
     // L2 while the Cartesian sweep runs (the sweep streams them right after)
-    const bool pf = !reverse && !comm && one_sweep && D.sw[0].ok && D.gmap;
+    const bool pf = !reverse && one_sweep && D.sw[0].ok && D.gmap && (!D.part || D.wide);
     const unsigned char* pfp = pf ? (const unsigned char*)D.gmap : nullptr;
     const unsigned long long pfb = pf ? (unsigned long long)D.n_gmap * 8ull : 0ull;
     if (!cart_split && D.n_fused_tiles <= cap) {
@@ -1525,6 +1545,18 @@ struct Problem {
   void cut_sweeps(int l, double* x, const double* b, int reverse) {
     double* bufs[2] = {x, lv[l].xs};
     LevelData& D = lv[l];
+    if (comm && D.wide && one_sweep && D.sw[reverse ? 1 : 0].ok) {
+      // wide halo: one exchange, the one-launch sweep over the rank's owned
+      // nodes and their cones, then the narrow halo
+      halo(l, x);
+      const LevelData::Sweep& W = D.sw[reverse ? 1 : 0];
+      SweepArgs A;
+      std::memcpy(&A, W.args, sizeof(A));
+      launch_ex(true, k_cut_sweep, dim3(W.ncta), dim3(32 * (SW_NW + 1)), W.smem, A, x, b);
+      CF_LAUNCHED();
+      halo_n(l, x);
+      return;
+    }
     if (comm && D.wide) {
       // wide halo: one exchange, then every step on the rank's shrinking
       // redundant patch sets (partition()), then the narrow halo
@@ -1536,7 +1568,7 @@ struct Problem {
       halo_n(l, x);
       return;
     }
-    if (!comm && one_sweep && D.sw[reverse ? 1 : 0].ok) {   // the whole cut sweep in one launch (sweep.cuh)
+    if ((!comm || !D.part) && one_sweep && D.sw[reverse ? 1 : 0].ok) {   // the whole cut sweep in one launch (sweep.cuh)
       const LevelData::Sweep& W = D.sw[reverse ? 1 : 0];
       SweepArgs A;
       std::memcpy(&A, W.args, sizeof(A));

@@ -391,7 +391,9 @@ inline std::vector<std::vector<int>> sweep_cone(const std::vector<SweepPatch>& P
 //   P: the cut patches with maps (nodes = b * ld + a); n, p, ld: the level;
 //   S = 4 n_c; nsm: SMs; smem_max: opt-in shared memory per block;
 //   force_ng > 0 forces the CTA count; (ca, cb): the level-set centre in
-//   lattice coordinates.
+//   lattice coordinates; [own_b0, own_b1): the owned lattice rows of a slab
+//   partition (the CTAs own the dynamic nodes there; their cones reach into
+//   the wide halo, which the exchange before the launch makes valid).
 // Ownership: the dynamic nodes are ordered by their angle about the level-set
 // centre and cut into contiguous runs of equal work (the map doubles of their
 // patches, shared among the patch interior's nodes); a run is one CTA.  The
@@ -401,7 +403,8 @@ inline std::vector<std::vector<int>> sweep_cone(const std::vector<SweepPatch>& P
 // The CTA count minimises an estimate of the sweep time: the largest cone's
 // map bytes / per-SM shared-memory throughput + all cones' bytes / L2 bandwidth.
 inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, int ld, int S, int reverse,
-                                int nsm, size_t smem_max, int force_ng, bool verbose, double ca, double cb) {
+                                int nsm, size_t smem_max, int force_ng, bool verbose, double ca, double cb,
+                                int own_b0 = -1, int own_b1 = -1) {
   SweepProgram R;
   R.S = S;
   if (S > SW_MAXS) {
@@ -422,8 +425,13 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
   std::unordered_map<int, double> work;
   for (int k = 0; k < (int)P.size(); ++k)
     for (int nd : P[k].in) work[nd] += (double)map_d(k) / P[k].in.size();
-  for (auto& kv : node_patches)
-    byang.push_back({std::atan2((kv.first / ld) - cb, (kv.first % ld) - ca), kv.first});
+  for (auto& kv : node_patches)   // (slab partition: only the nodes of the owned lattice rows)
+    if (own_b0 < 0 || (kv.first / ld >= own_b0 && kv.first / ld < own_b1))
+      byang.push_back({std::atan2((kv.first / ld) - cb, (kv.first % ld) - ca), kv.first});
+  if (byang.empty()) {
+    R.why = "no owned cut-patch interior nodes";
+    return R;
+  }
   std::sort(byang.begin(), byang.end());
   double wtot = 0;
   for (auto& q : byang) wtot += work[q.second];

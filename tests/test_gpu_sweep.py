@@ -140,3 +140,37 @@ def test_sweep_config1_fullsize_bitidentical():
         _, _, a, b = smooth_pair(g, h, w, l, rev, seed=95)
         dn = dofs(g, l)
         assert np.array_equal(a[dn], b[dn]), rev
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sweep_partitioned_bitexact(world):
+    """Slab partition (in-process ranks on one GPU): the wide-halo levels run
+    the one-launch sweep over each rank's owned rows, on its share of the SMs,
+    bit-identical to one rank."""
+    from test_gpu_slab import owned, run_ranks
+    import torch
+    w = workloads.paper_level(2, 9)   # 128^2 finest
+    L = w.n_levels - 1
+    x0 = workloads.lattice_vector(w, 21)
+    b0 = workloads.lattice_vector(w, 22)
+    g1 = problem(w, {})
+    x1 = g1.to_device(x0)
+    for rev in (False, True):
+        g1.smooth(L, x1, g1.to_device(b0), reverse=rev)
+    torch.cuda.synchronize()
+
+    def fn(r, g, s):
+        x = g.to_device(x0)
+        b = g.to_device(b0)
+        for rev in (False, True):
+            g.smooth(L, x, b, reverse=rev, stream=s.cuda_stream)
+        return x
+
+    xs, gs = run_ranks(w, world, fn)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    ref = x1.cpu().numpy().reshape(-1, g1.lattice_shape(L)[1])[:, :g1.lattice_shape(L)[0]]
+    for g, x in zip(gs, xs):
+        info = g.level_info(L)
+        assert g.partition_info(L)["part"] and 0 < info.sweep_ctas[0] <= nsm // world
+        r0, r1, a = owned(g, x, L)
+        np.testing.assert_array_equal(a, ref[r0:r1])
