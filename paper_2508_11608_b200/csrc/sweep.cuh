@@ -17,20 +17,23 @@
 // (cut7_main: same row split, accumulation order and shuffle tree), so the
 // result is bit-identical to the launch-per-step chain.
 //
-// Data movement: the CTA's task and chunk lists are bulk-copied into shared
-// memory before griddepcontrol.wait (setup data), and every map of its cone is
-// prefetched towards L2.  A producer warp streams the "chunks" through a ring
-// of NCH shared-memory slots with cp.async.bulk (full / empty mbarriers): a
-// chunk is the map rows of consecutive tasks of one step, their row jobs (one
-// 8-byte record per matrix row: where its map row and input vector are, its
-// length and output slot) and, for the first chunk of a step, the step's
-// gather list (the slot of every entry of the step's input vectors).  Consumer
-// warps: load the slots of x and b (after the wait); per step wait for the
-// first chunk, gather v = [b_I ; x_E] of every task from the slots, barrier,
-// then per chunk every 4-lane group takes rows, barrier.  At the end the owned
-// slots are stored to x -- after a grid-wide counter says every CTA has read
-// its initial slots (a CTA must not overwrite a node another CTA has not
-// loaded yet; the grid is at most one CTA per SM, so all CTAs are resident).
+// Data movement: the CTA's chunk and run lists are bulk-copied into shared
+// memory before griddepcontrol.wait (setup data).  A producer warp streams the
+// "chunks" through a ring of NCH shared-memory slots with cp.async.bulk (full
+// / empty mbarriers): a chunk is the maps of consecutive tasks of one step (as
+// 1-2 "runs" of adjacent map blocks: the maps of a colour are stored in angle
+// order, and one bulk copy costs ~130 cycles of issue however small), their
+// row jobs (one 8-byte record per matrix row: where its map row and input
+// vector are, its length and output slot) and, for the first chunk of a step,
+// the step's gather list (the slot of every entry of the step's input
+// vectors).  The 16 consumer warps: load the slots of x and b (after the
+// wait); per step wait for its first chunk, gather v = [b_I ; x_E] of every
+// task from the slots, barrier, then the step's rows round-robin over 4-lane
+// groups, barrier.  At the end the owned slots are stored to x -- after a
+// grid-wide ticket counter says every CTA has read its initial slots (a CTA
+// must not overwrite a node another CTA has not loaded yet; the launch is
+// cooperative, at most one CTA per SM, so all CTAs are resident).  The
+// forward Cartesian sweep before it prefetches the level's maps towards L2.
 #pragma once
 #include <algorithm>
 #include <cstdio>
@@ -46,7 +49,7 @@ namespace cf {
 
 constexpr int SW_MAXS = 16;    // steps per sweep (4 n_c, n_c <= 4)
 constexpr int SW_MAXNCH = 8;   // ring slots
-constexpr int SW_NW = 16;      // warps per CTA
+constexpr int SW_NW = 16;      // consumer warps per CTA (+ 1 producer warp)
 
 struct SweepRun {         // one bulk copy of adjacent map blocks into a ring slot
   long long src;          // byte offset into gmap (16-byte aligned)

@@ -58,9 +58,9 @@ def smooth_pair(g, h, w, l, rev, seed=70, nan=False):
 
 
 @pytest.mark.parametrize("w", [workloads.paper_level(1, 7), workloads.paper_level(2, 7),
-                               workloads.paper_level(3, 7), workloads.paper_level(2, 7, n_c=1), OFFC,
-                               workloads.CONFIG0],
-                         ids=["Q1", "Q2", "Q3", "Q2-nc1", "offcentre", "config0"])
+                               workloads.paper_level(3, 7), workloads.paper_level(2, 7, n_c=1),
+                               workloads.paper_level(2, 7, n_c=4), OFFC, workloads.CONFIG0],
+                         ids=["Q1", "Q2", "Q3", "Q2-nc1", "Q2-nc4", "offcentre", "config0"])
 def test_sweep_bitidentical_every_level(w):
     g = problem(w, {})
     h = problem(w, {"CUTFEM_SWEEP": "0"})
