@@ -59,7 +59,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // patch-map block layout (R13): [int nnz, 0, 8 pad bytes][nnz uint8 window
 // indices, padded to 16 bytes][the m x K map, K = m + nnz].  A map row is
-// summed by tpr lanes (map_tpr: 4, 2 or 1 by m); lane h takes columns
+// summed by tpr lanes (map_tpr, now 1: a 4-lane split measured 1.5x more
+// instructions per row in k_cut_sweep); lane h takes columns
 // h, h + 2 tpr, ... into one accumulator and h + tpr, h + 3 tpr, ... into a
 // second.  The map is stored in column blocks of B = 2 tpr columns, K padded
 // to a multiple of B with zeros: element (i, c), c = B j + h + e tpr (e = 0,
@@ -68,7 +69,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // are consecutive (no shared-memory bank conflicts).  Blocks start 16-byte
 // aligned (bulk copies, k_cut_sweep).
 __host__ __device__ constexpr long long map_hdr_d(int nnz) { return 2 + 2 * ((nnz + 15) / 16); }
-__host__ __device__ constexpr int map_tpr(int m) { return m * 4 <= 128 ? 4 : (m * 2 <= 128 ? 2 : 1); }
+__host__ __device__ constexpr int map_tpr(int) { return 1; }   // one lane per row (k_cut_sweep is instruction-issue bound: no shuffles)
 __host__ __device__ constexpr int map_kp(int m, int K) { return (K + 2 * map_tpr(m) - 1) / (2 * map_tpr(m)) * (2 * map_tpr(m)); }
 __host__ __device__ constexpr long long map_rows_d(int m, int K) { return (long long)m * map_kp(m, K); }
 __host__ __device__ constexpr long long map_index(int m, int i, int c) {

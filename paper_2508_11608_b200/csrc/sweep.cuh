@@ -133,16 +133,23 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 #endif
 
 // chunk k of the CTA into ring slot k % nch (its runs of adjacent map
-// blocks, then its row jobs and gather list), completing on full[k % nch]
+// blocks, then its row jobs and gather list), completing on full[k % nch].
+// Executed by the whole producer warp: one bulk copy costs ~130 cycles of
+// issue even when small, so the copies of a chunk go out from different lanes
+// (lane 0 expects the bytes first; lanes 0.. the runs, lane 31 the aux copy)
 __device__ __forceinline__ void sweep_fill(const SweepArgs& A, const SweepChunk* CH, const SweepRun* RU, int k,
-                                           unsigned char* ring, uint64_t* full) {
+                                           unsigned char* ring, uint64_t* full, int lane) {
   const SweepChunk& ch = CH[k];
   const int sl = k % A.nch;
   unsigned char* slot = ring + (size_t)sl * A.cb;
-  mbar_expect_tx(&full[sl], ch.bytes);
+  if (lane == 0) mbar_expect_tx(&full[sl], ch.bytes);
+  __syncwarp();
   const unsigned char* gm = (const unsigned char*)A.gmap;
-  for (unsigned r = ch.run0; r < ch.run0 + ch.nrun; ++r) bulk_g2s(slot + RU[r].dst, gm + RU[r].src, RU[r].bytes, &full[sl]);
-  bulk_g2s(slot + ch.rj_soff, A.aux + ch.aux_src, ch.bytes - ch.rj_soff, &full[sl]);
+  for (int q = lane; q < (int)ch.nrun && lane < 31; q += 31) {
+    const SweepRun& r = RU[ch.run0 + q];
+    bulk_g2s(slot + r.dst, gm + r.src, r.bytes, &full[sl]);
+  }
+  if (lane == 31) bulk_g2s(slot + ch.rj_soff, A.aux + ch.aux_src, ch.bytes - ch.rj_soff, &full[sl]);
 }
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * SW_NW) : "memory"); }
@@ -179,11 +186,14 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
       mbar_expect_tx(pbar, chb + rub);
       if (chb) bulk_g2s(CH, A.chunk + C.chunk0, chb, pbar);
       if (rub) bulk_g2s(RU, A.run + C.run0, rub, pbar);
-      mbar_wait(pbar, 0);
-      for (int k = 0; k < C.nchunk; ++k) {
-        if (k >= A.nch) mbar_wait(&empty[k % A.nch], ((k / A.nch) - 1) & 1);
-        sweep_fill(A, CH, RU, k, ring, full);
-      }
+    }
+    mbar_wait(pbar, 0);
+    for (int k = 0; k < C.nchunk; ++k) {
+      if (k >= A.nch) mbar_wait(&empty[k % A.nch], ((k / A.nch) - 1) & 1);
+#ifdef CF_TIMING
+      if (lane == 0 && blockIdx.x == 0 && k < 32) g_dbg[5000 + k / 8][k % 8] = clock64();
+#endif
+      sweep_fill(A, CH, RU, k, ring, full, lane);
     }
     return;
   }
@@ -223,6 +233,9 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
     SW_LAP(3);
     mbar_wait(&full[sl], par);
     SW_LAP(0);
+#ifdef CF_TIMING
+    if (blockIdx.x == 0 && tid == 0 && k < 32) g_dbg[5004 + k / 8][k % 8] = clock64();
+#endif
     const SweepChunk& ch = CH[k];
     const unsigned char* slot = ring + (size_t)sl * A.cb;
     if (ch.ngat) {   // first chunk of a step: v = [b_I ; x_E] of its tasks, from the state after the previous step
@@ -231,9 +244,19 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
       if (s == A.S / 2) SW_TSTAMP(3);
       if (k) consumer_sync();   // the previous step's rows are done (they read v, write xs)
       const uint16_t* gl = (const uint16_t*)(slot + ch.gat_soff);
-      for (int e = tid; e < (int)ch.ngat; e += NT) {
-        const unsigned src = gl[e];
-        v[e] = (src & 0x8000u) ? bs[src & 0x7fffu] : xs[src];
+      const int ng = ch.ngat;
+      // four independent entries per thread and round (loads before stores:
+      // the smem latency is paid once per round, not per entry)
+      for (int e0 = tid; e0 < ng; e0 += 4 * NT) {
+        unsigned src[4];
+        double val[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) src[u] = e0 + u * NT < ng ? gl[e0 + u * NT] : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) val[u] = (src[u] & 0x8000u) ? bs[src[u] & 0x7fffu] : xs[src[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * NT < ng) v[e0 + u * NT] = val[u];
       }
       consumer_sync();
     }
@@ -245,35 +268,36 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
     // every lane reaches the shuffles).  x_I^new[i] = G_j[i,:] v in cut7_main's
     // order (lane h: columns h + 2 tpr j into a0c, h + tpr + 2 tpr j into a1c)
     // and shuffle tree: bit-identical to k_cut_step7
-    const int first = row0 - ((row0 - warp * 8) % (NT / 4) + (NT / 4)) % (NT / 4);
-    for (int Rb = first; Rb < row0 + nrows; Rb += NT / 4) {
-      const int R = Rb + (lane >> 2) - row0;
-      const bool act = R >= 0 && R < nrows;
-      const unsigned long long job = act ? rj[R] : 0ull;
+    // one lane per row (map_tpr = 1), round-robin over the step (thread t takes
+    // the step's rows congruent to t mod NT).  x_I^new[i] = G_j[i,:] v in
+    // cut7_main's order (columns 2j into a0c, 2j + 1 into a1c; a 16-byte read of
+    // the map's column pair and of v per FMA pair): bit-identical to k_cut_step7
+    const int first = row0 - ((row0 - tid) % NT + NT) % NT;
+    for (int R = first - row0; R < nrows; R += NT) {
+      if (R < 0) continue;
+#ifdef CF_SKIP_ROWS
+      if (R >= 0) continue;
+#endif
+      const unsigned long long job = rj[R];
       const int K = (int)((job >> 32) & 0xffu), m = (int)((job >> 40) & 0x3fu);
-      const int tpr = 1 << (int)((job >> 46) & 3u), h = lane & 3, B = 2 * tpr;
-      const double* g = ringd + (unsigned)(job & 0xffffu) + 2 * h;
-      const double* q = v + (unsigned)((job >> 16) & 0xffffu) + 2 * h;
+      const double* g = ringd + (unsigned)(job & 0xffffu);
+      const double* q = v + (unsigned)((job >> 16) & 0xffffu);
       double a0c = 0.0, a1c = 0.0;
-      if (act && h < tpr) {
-        int c = h;
+      int c = 0;
 #pragma unroll 4
-        for (; c + tpr < K; c += B, g += B * m, q += B) {
-          const double2 gg = *(const double2*)g, vv = *(const double2*)q;
-          a0c = fma(gg.x, vv.x, a0c);
-          a1c = fma(gg.y, vv.y, a1c);
-        }
-        if (c < K) a0c = fma(g[0], q[0], a0c);
+      for (; c + 1 < K; c += 2, g += 2 * m, q += 2) {
+        const double2 gg = *(const double2*)g, vv = *(const double2*)q;
+        a0c = fma(gg.x, vv.x, a0c);
+        a1c = fma(gg.y, vv.y, a1c);
       }
-      double z = a0c + a1c;
-      const double z2 = __shfl_xor_sync(0xffffffffu, z, 2, 4);
-      if (tpr == 4) z += z2;
-      const double z1 = __shfl_xor_sync(0xffffffffu, z, 1, 4);
-      if (tpr >= 2) z += z1;
-      if (act && h == 0) xs[(unsigned)(job >> 48)] = z;
+      if (c < K) a0c = fma(g[0], q[0], a0c);
+      xs[(unsigned)(job >> 48)] = a0c + a1c;
     }
     SW_LAP(2);
     __syncwarp();
+#ifdef CF_TIMING
+    if (blockIdx.x == 0 && tid == 0 && k < 32) g_dbg[5008 + k / 8][k % 8] = clock64();
+#endif
     if (lane == 0) mbar_arrive(&empty[sl]);
     if (++sl == A.nch) {
       sl = 0;

@@ -21,7 +21,7 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned 
                    (unsigned)__cvta_generic_to_shared(smem)), "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
 }
 
-__global__ void k_bulk(const char* src, long long stride_cta, int bytes, int ncopy, int rounds, long long* out, int lanes) {
+__global__ void k_bulk(const char* src, long long stride_cta, int bytes, int ncopy, int rounds, long long* out, int lanes, int mis) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ uint64_t bar;
   if (threadIdx.x == 0) mbar_init(&bar, 1);
@@ -32,7 +32,7 @@ __global__ void k_bulk(const char* src, long long stride_cta, int bytes, int nco
     __syncwarp();
     if (threadIdx.x < lanes)
       for (int c = threadIdx.x; c < ncopy; c += lanes)
-        bulk_g2s(sm + (size_t)c * bytes, src + blockIdx.x * stride_cta + (size_t)((c + r * 7) % 64) * bytes, bytes, &bar);
+        bulk_g2s(sm + (size_t)c * bytes + mis, src + blockIdx.x * stride_cta + (size_t)((c + r * 7) % 64) * bytes + mis, bytes, &bar);
     mbar_wait(&bar, r & 1);
   }
   long long t1 = clock64();
@@ -42,21 +42,22 @@ __global__ void k_bulk(const char* src, long long stride_cta, int bytes, int nco
 int main() {
   char* src; long long* out;
   cudaMalloc(&src, 256 << 20); cudaMemset(src, 1, 256 << 20); cudaMalloc(&out, 8 * 1024);
-  cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
   long long h[148];
-  struct { int bytes, ncopy, lanes, ctas; } cfg[] = {{3072, 40, 1, 1}, {3072, 40, 1, 148}, {3072, 40, 32, 148}, {3072, 10, 1, 148},
-                                                    {16384, 8, 1, 148}, {32768, 4, 1, 148}, {1024, 128, 1, 148}, {1024, 128, 32, 148}};
+  struct { int bytes, ncopy, lanes, ctas, mis; } cfg[] = {{3072, 40, 1, 1, 0}, {3072, 40, 1, 148, 0}, {3072, 40, 32, 148, 0}, {3072, 10, 1, 148, 0},
+                                                    {16384, 8, 1, 148, 0}, {32768, 4, 1, 148, 0}, {1024, 128, 1, 148, 0}, {1024, 128, 32, 148, 0},
+                                                    {24576, 6, 1, 148, 0}, {24576, 6, 1, 148, 16}, {24576, 6, 1, 148, 48}, {3072, 40, 1, 148, 16}};
   for (auto c : cfg) {
     const int rounds = 50;
-    k_bulk<<<c.ctas, 32, c.bytes * c.ncopy>>>(src, 0, c.bytes, c.ncopy, 2, out, c.lanes);   // warm L2 (shared source)
-    k_bulk<<<c.ctas, 32, c.bytes * c.ncopy>>>(src, 0, c.bytes, c.ncopy, rounds, out, c.lanes);
+    k_bulk<<<c.ctas, 32, c.bytes * c.ncopy + 128>>>(src, 0, c.bytes, c.ncopy, 2, out, c.lanes, c.mis);   // warm L2 (shared source)
+    k_bulk<<<c.ctas, 32, c.bytes * c.ncopy + 128>>>(src, 0, c.bytes, c.ncopy, rounds, out, c.lanes, c.mis);
     cudaDeviceSynchronize();
     cudaMemcpy(h, out, 8 * c.ctas, cudaMemcpyDeviceToHost);
     double mx = 0, sum = 0;
     for (int i = 0; i < c.ctas; ++i) { mx = h[i] > mx ? h[i] : mx; sum += h[i]; }
     const double cyc = mx / rounds, kb = c.bytes * c.ncopy / 1024.0;
-    printf("%3d CTAs, %2d lanes issue %3d x %5d B (%6.1f KB) per round: %7.0f cycles/round (max CTA) = %6.1f B/clk/SM, %.2f us\n",
-           c.ctas, c.lanes, c.ncopy, c.bytes, kb, cyc, c.bytes * c.ncopy / cyc, cyc / 1965.0);
+    printf("%3d CTAs, %2d lanes issue %3d x %5d B (%6.1f KB, +%2d B misalign) per round: %7.0f cycles/round (max CTA) = %6.1f B/clk/SM, %.2f us\n",
+           c.ctas, c.lanes, c.ncopy, c.bytes, kb, c.mis, cyc, c.bytes * c.ncopy / cyc, cyc / 1965.0);
   }
   return 0;
 }

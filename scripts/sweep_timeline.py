@@ -49,6 +49,14 @@ for i, nm in enumerate(["data wait", "gather", "rows", "arrive"]):
     print(f"consumer 0 cycles in {nm:10s}: med {np.median(acc[:, i]):8.0f} max {acc[:, i].max():8.0f}")
 print(f"chunks per CTA: med {np.median(acc[:, 4]):.0f} max {acc[:, 4].max():.0f}; runs med {np.median(acc[:, 5]):.0f} "
       f"max {acc[:, 5].max():.0f}; bytes med {np.median(acc[:, 6]) / 1e3:.0f} KB max {acc[:, 6].max() / 1e3:.0f} KB")
+b3 = np.zeros((5012, 8), dtype=np.uint64)
+assert lib.cutfem_debug_timers(b3.ctypes.data, 5012) == 0
+iss, ful, don = (b3[5000:5004].ravel().astype(np.int64), b3[5004:5008].ravel().astype(np.int64),
+                 b3[5008:5012].ravel().astype(np.int64))
+base = iss[0]
+for k in range(min(32, int(acc[0, 4]))):
+    print(f"chunk {k:2d}: issued {iss[k] - base:7d}  landed+seen {ful[k] - base:7d}  done {don[k] - base:7d}  "
+          f"lat {ful[k] - iss[k]:6d}")
 d = np.diff(t, axis=1)
 for k in range(6):
     print(f"{names[k]}->{names[k + 1]:9s} med {np.median(d[:, k]):7.2f} max {d[:, k].max():7.2f}")
