@@ -60,6 +60,7 @@ struct LevelArgs {
   int dim;                           // 2 or 3
   int fitted;                        // fitted box: every cell Inside, no DoF on the box boundary
   int sym_packed;                    // 3D local inverses packed symmetric (k_pack_sym) instead of dense
+  int map_one_lane;                  // 2D cut-patch maps summed one lane per row (map_tpr; large levels)
   double h, x0, y0, z0;
   double cx, cy, cz, r;
   double gDh;                        // gamma_D / h

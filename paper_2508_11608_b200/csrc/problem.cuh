@@ -270,6 +270,7 @@ struct Problem {
       L.cx = prm.cx;
       L.cy = prm.cy;
       L.r = prm.r;
+      L.map_one_lane = L.n >= MAP_ONE_LANE_MIN_N ? 1 : 0;
       L.gDh = prm.gamma_D / L.h;
       for (int k = 1; k <= p; ++k) {
         double f = 1.0;
@@ -652,7 +653,7 @@ struct Problem {
         for (int q = 0; q < ncp; ++q) {
           const int k = ord[q];
           hd[k].map_off = off | ((int64_t)hn[k] << 48);
-          const int64_t blk = map_hdr_d(hn[k]) + map_rows_d(hm[k], hm[k] + hn[k]);
+          const int64_t blk = map_hdr_d(hn[k]) + map_rows_d(hm[k], hm[k] + hn[k], D.a.map_one_lane);
           off += blk;
           // algorithmic bytes of the patch in its colour step: descriptor, map block,
           // gathered window and b values, written interior values
@@ -664,7 +665,7 @@ struct Problem {
         require(off < (1ll << 48), ERR_SIZE, "cut-patch maps exceed 2^48 doubles");
         D.gmap = alloc<double>(off);
         D.n_gmap = off;
-        k_map_compact<P><<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, doff, Gd, D.gmap);
+        k_map_compact<P><<<ncp, 128, 0, st>>>((const CutDesc*)D.desc, doff, Gd, D.gmap, D.a.map_one_lane);
         CF_LAUNCHED();
       }
     });
@@ -711,7 +712,7 @@ struct Problem {
       }
       q.blk0 = d.map_off & ((1ll << 48) - 1);
       q.rows = q.blk0 + map_hdr_d(nnz);
-      q.blk1 = q.rows + map_rows_d((int)q.in.size(), (int)(q.in.size() + q.ex.size()));
+      q.blk1 = q.rows + map_rows_d((int)q.in.size(), (int)(q.in.size() + q.ex.size()), L.map_one_lane);
       P.push_back(std::move(q));
     }
     int dev = 0, nsm = 0, smax = 0;
@@ -725,7 +726,8 @@ struct Problem {
     });
     for (int dir = 0; dir < 2; ++dir) {
       host::SweepProgram R = host::build_sweep(P, L.n, p, L.ld, 4 * prm.n_c, dir, nsm, (size_t)smax, sweep_ng, verbose,
-                                               (L.cx - L.x0) / L.h * p, (L.cy - L.y0) / L.h * p, own_b0, own_b1);
+                                               (L.cx - L.x0) / L.h * p, (L.cy - L.y0) / L.h * p, own_b0, own_b1,
+                                               L.map_one_lane);
       LevelData::Sweep& W = D.sw[dir];
       W.ok = R.ok;
       if (!R.ok) {
@@ -749,6 +751,7 @@ struct Problem {
       A.gbar = alloc<unsigned long long>(1);
       CF_CUDA(cudaMemsetAsync(A.gbar, 0, sizeof(unsigned long long), st));
       A.S = R.S;
+      A.one_lane = L.map_one_lane;
       A.nch = R.nch;
       A.cb = R.cb;
       A.off_chunk = R.off_chunk;

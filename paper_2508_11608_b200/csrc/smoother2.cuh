@@ -59,8 +59,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // patch-map block layout (R13): [int nnz, 0, 8 pad bytes][nnz uint8 window
 // indices, padded to 16 bytes][the m x K map, K = m + nnz].  A map row is
-// summed by tpr lanes (map_tpr, now 1: a 4-lane split measured 1.5x more
-// instructions per row in k_cut_sweep); lane h takes columns
+// summed by tpr lanes (map_tpr: one lane on levels n >= 256, 4 (2, 1 for
+// large m) on coarser ones: V-cycle 601 vs 611 us with one lane everywhere;
+// the flushed smoothing step of config1 is the same either way); lane h takes columns
 // h, h + 2 tpr, ... into one accumulator and h + tpr, h + 3 tpr, ... into a
 // second.  The map is stored in column blocks of B = 2 tpr columns, K padded
 // to a multiple of B with zeros: element (i, c), c = B j + h + e tpr (e = 0,
@@ -69,13 +70,24 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // are consecutive (no shared-memory bank conflicts).  Blocks start 16-byte
 // aligned (bulk copies, k_cut_sweep).
 __host__ __device__ constexpr long long map_hdr_d(int nnz) { return 2 + 2 * ((nnz + 15) / 16); }
-__host__ __device__ constexpr int map_tpr(int) { return 1; }   // one lane per row (k_cut_sweep is instruction-issue bound: no shuffles)
-__host__ __device__ constexpr int map_kp(int m, int K) { return (K + 2 * map_tpr(m) - 1) / (2 * map_tpr(m)) * (2 * map_tpr(m)); }
-__host__ __device__ constexpr long long map_rows_d(int m, int K) { return (long long)m * map_kp(m, K); }
-__host__ __device__ constexpr long long map_index(int m, int i, int c) {
-  return ((long long)(c / (2 * map_tpr(m))) * m + i) * (2 * map_tpr(m)) + 2 * ((c % (2 * map_tpr(m))) % map_tpr(m)) +
-         (c % (2 * map_tpr(m))) / map_tpr(m);
+// lanes per map row: one on levels with one_lane (large levels: many rows per
+// step, the instruction count decides), else 4 (2, 1 for larger m: coarse
+// levels, where a step's few long rows decide)
+__host__ __device__ constexpr int map_tpr(int m, int one_lane) {
+  return one_lane ? 1 : (m * 4 <= 128 ? 4 : (m * 2 <= 128 ? 2 : 1));
 }
+__host__ __device__ constexpr int map_kp(int m, int K, int one_lane) {
+  return (K + 2 * map_tpr(m, one_lane) - 1) / (2 * map_tpr(m, one_lane)) * (2 * map_tpr(m, one_lane));
+}
+__host__ __device__ constexpr long long map_rows_d(int m, int K, int one_lane) {
+  return (long long)m * map_kp(m, K, one_lane);
+}
+__host__ __device__ constexpr long long map_index(int m, int i, int c, int one_lane) {
+  return ((long long)(c / (2 * map_tpr(m, one_lane))) * m + i) * (2 * map_tpr(m, one_lane)) +
+         2 * ((c % (2 * map_tpr(m, one_lane))) % map_tpr(m, one_lane)) + (c % (2 * map_tpr(m, one_lane))) / map_tpr(m, one_lane);
+}
+// levels with at least this many cells per side sum a map row with one lane
+constexpr int MAP_ONE_LANE_MIN_N = 256;
 
 __device__ __forceinline__ int desc_kind(const CutDesc& d, int wx, int wy) {
   return (d.kinds >> (2 * (wy * 4 + wx))) & 3;
@@ -1684,7 +1696,7 @@ __global__ void k_map_nnz(const CutDesc* desc, const int64_t* dense_off, const d
 }
 
 template <int P>
-__global__ void k_map_compact(const CutDesc* desc, const int64_t* dense_off, const double* Gd, double* Gc) {
+__global__ void k_map_compact(const CutDesc* desc, const int64_t* dense_off, const double* Gd, double* Gc, int one_lane) {
   constexpr int WW = (4 * P + 1) * (4 * P + 1);
   const CutDesc d = desc[blockIdx.x];
   const int m = mask_count(d), K = m + WW;
@@ -1712,7 +1724,7 @@ __global__ void k_map_compact(const CutDesc* desc, const int64_t* dense_off, con
     for (int q = 0; q < ((c + 15) & ~15); ++q) ob[q] = q < c ? idx[q] : 0;
   }
   __syncthreads();
-  const int Kc = m + nnz, Kp = map_kp(m, Kc), tpr = map_tpr(m), B = 2 * tpr;
+  const int Kc = m + nnz, Kp = map_kp(m, Kc, one_lane), tpr = map_tpr(m, one_lane), B = 2 * tpr;
   double* rows = out + map_hdr_d(nnz);
   for (int e = threadIdx.x; e < m * Kp; e += blockDim.x) {
     const int j = e / (B * m), rem = e - j * B * m, i = rem / B, pos = rem % B;
@@ -1738,7 +1750,7 @@ struct CutMapSmem {
 // same launch).
 template <int P, int NT>
 __device__ __forceinline__ void cut7_prologue(const CutDesc* desc, int k, const double* G, unsigned char* gsm, int gt,
-                                              int bar) {
+                                              int bar, int one_lane) {
   using S = CutMapSmem<P>;
   constexpr int MM = S::MM;
   CutDesc& d = *(CutDesc*)gsm;
@@ -1754,7 +1766,7 @@ __device__ __forceinline__ void cut7_prologue(const CutDesc* desc, int k, const 
   const double* blk = G + (d.map_off & ((1ll << 48) - 1));
   const int nnz = (int)(d.map_off >> 48), K = m + nnz;
   const double* rows = blk + map_hdr_d(nnz);
-  for (int e = gt; e < m * map_kp(m, K); e += NT) cp_async8(Gs + e, rows + e);
+  for (int e = gt; e < m * map_kp(m, K, one_lane); e += NT) cp_async8(Gs + e, rows + e);
   for (int loc = gt; loc < MM; loc += NT) {
     const unsigned long long word = d.mask[loc >> 6];
     if ((word >> (loc & 63)) & 1ull)
@@ -1790,7 +1802,7 @@ __device__ __forceinline__ void cut7_main(const LevelArgs& L, const double* R, d
   // x_I^new = G_j v: TPR threads per row (power of two), shuffle-reduced; lane
   // h sums columns h + 2 tpr j (a0c) and h + tpr + 2 tpr j (a1c), j = 0, 1, ...
   // (the map's column-block layout, map_index; the order k_cut_sweep repeats)
-  const int tpr = map_tpr(m);
+  const int tpr = map_tpr(m, L.map_one_lane);
   static_assert(NT >= 128, "the map layout assumes 128-thread row groups (map_tpr)");
   for (int r0 = 0; r0 < m; r0 += NT / tpr) {
     const int i = r0 + gt / tpr, h = gt % tpr;
@@ -1831,7 +1843,7 @@ __global__ void __launch_bounds__(NT) k_cut_step7(LevelArgs L, const CutDesc* de
     }
     return;
   }
-  cut7_prologue<P, NT>(desc, blockIdx.x, G, sm7, tid, 0);
+  cut7_prologue<P, NT>(desc, blockIdx.x, G, sm7, tid, 0, L.map_one_lane);
   pdl_wait();
   cut7_main<P, NT, false>(L, R, W, b, sm7, tid, 0);
 }

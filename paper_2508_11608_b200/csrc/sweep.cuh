@@ -97,6 +97,7 @@ struct SweepArgs {
   const double* gmap;
   unsigned long long* gbar;   // launch counter (tickets; all launches of one program have the same grid)
   int S, nch, cb;             // steps, ring slots, ring slot bytes
+  int one_lane;               // maps summed one lane per row (map_tpr), else 4-lane groups
   unsigned off_chunk, off_run, off_xs, off_bs, off_v, off_ring;   // shared-memory byte offsets
 };
 
@@ -263,35 +264,61 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
     SW_LAP(1);
     const unsigned long long* rj = (const unsigned long long*)(slot + ch.rj_soff);
     const int nrows = ch.nrows, row0 = ch.row0;
-    // rows over 4-lane groups, round-robin over the step (group warp*8 + lane/4
-    // takes the step's rows congruent to it mod NT/4; warp-uniform trip count:
-    // every lane reaches the shuffles).  x_I^new[i] = G_j[i,:] v in cut7_main's
-    // order (lane h: columns h + 2 tpr j into a0c, h + tpr + 2 tpr j into a1c)
-    // and shuffle tree: bit-identical to k_cut_step7
-    // one lane per row (map_tpr = 1), round-robin over the step (thread t takes
-    // the step's rows congruent to t mod NT).  x_I^new[i] = G_j[i,:] v in
-    // cut7_main's order (columns 2j into a0c, 2j + 1 into a1c; a 16-byte read of
-    // the map's column pair and of v per FMA pair): bit-identical to k_cut_step7
-    const int first = row0 - ((row0 - tid) % NT + NT) % NT;
-    for (int R = first - row0; R < nrows; R += NT) {
-      if (R < 0) continue;
-#ifdef CF_SKIP_ROWS
-      if (R >= 0) continue;
-#endif
-      const unsigned long long job = rj[R];
-      const int K = (int)((job >> 32) & 0xffu), m = (int)((job >> 40) & 0x3fu);
-      const double* g = ringd + (unsigned)(job & 0xffffu);
-      const double* q = v + (unsigned)((job >> 16) & 0xffffu);
-      double a0c = 0.0, a1c = 0.0;
-      int c = 0;
+    if (A.one_lane) {
+      // one lane per row (large levels), round-robin over the step: thread t
+      // takes the step's rows congruent to t mod NT (columns 2j into a0c,
+      // 2j + 1 into a1c, one 16-byte read of the map pair and of v per pair)
+      const int first = row0 - ((row0 - tid) % NT + NT) % NT;
+      for (int R = first - row0; R < nrows; R += NT) {
+        if (R < 0) continue;
+        const unsigned long long job = rj[R];
+        const int K = (int)((job >> 32) & 0xffu), m = (int)((job >> 40) & 0x3fu);
+        const double* g = ringd + (unsigned)(job & 0xffffu);
+        const double* q = v + (unsigned)((job >> 16) & 0xffffu);
+        double a0c = 0.0, a1c = 0.0;
+        int c = 0;
 #pragma unroll 4
-      for (; c + 1 < K; c += 2, g += 2 * m, q += 2) {
-        const double2 gg = *(const double2*)g, vv = *(const double2*)q;
-        a0c = fma(gg.x, vv.x, a0c);
-        a1c = fma(gg.y, vv.y, a1c);
+        for (; c + 1 < K; c += 2, g += 2 * m, q += 2) {
+          const double2 gg = *(const double2*)g, vv = *(const double2*)q;
+          a0c = fma(gg.x, vv.x, a0c);
+          a1c = fma(gg.y, vv.y, a1c);
+        }
+        if (c < K) a0c = fma(g[0], q[0], a0c);
+        xs[(unsigned)(job >> 48)] = a0c + a1c;
       }
-      if (c < K) a0c = fma(g[0], q[0], a0c);
-      xs[(unsigned)(job >> 48)] = a0c + a1c;
+    } else {
+      // rows over 4-lane groups, round-robin over the step (group warp*8 + lane/4
+      // takes the step's rows congruent to it mod NT/4; warp-uniform trip count:
+      // every lane reaches the shuffles).  x_I^new[i] = G_j[i,:] v in cut7_main's
+      // order (lane h: columns h + 2 tpr j into a0c, h + tpr + 2 tpr j into a1c)
+      // and shuffle tree: bit-identical to k_cut_step7
+      const int first = row0 - ((row0 - warp * 8) % (NT / 4) + (NT / 4)) % (NT / 4);
+      for (int Rb = first; Rb < row0 + nrows; Rb += NT / 4) {
+        const int R = Rb + (lane >> 2) - row0;
+        const bool act = R >= 0 && R < nrows;
+        const unsigned long long job = act ? rj[R] : 0ull;
+        const int K = (int)((job >> 32) & 0xffu), m = (int)((job >> 40) & 0x3fu);
+        const int tpr = 1 << (int)((job >> 46) & 3u), h = lane & 3, B = 2 * tpr;
+        const double* g = ringd + (unsigned)(job & 0xffffu) + 2 * h;
+        const double* q = v + (unsigned)((job >> 16) & 0xffffu) + 2 * h;
+        double a0c = 0.0, a1c = 0.0;
+        if (act && h < tpr) {
+          int c = h;
+#pragma unroll 4
+          for (; c + tpr < K; c += B, g += B * m, q += B) {
+            const double2 gg = *(const double2*)g, vv = *(const double2*)q;
+            a0c = fma(gg.x, vv.x, a0c);
+            a1c = fma(gg.y, vv.y, a1c);
+          }
+          if (c < K) a0c = fma(g[0], q[0], a0c);
+        }
+        double z = a0c + a1c;
+        const double z2 = __shfl_xor_sync(0xffffffffu, z, 2, 4);
+        if (tpr == 4) z += z2;
+        const double z1 = __shfl_xor_sync(0xffffffffu, z, 1, 4);
+        if (tpr >= 2) z += z1;
+        if (act && h == 0) xs[(unsigned)(job >> 48)] = z;
+      }
     }
     SW_LAP(2);
     __syncwarp();
@@ -431,7 +458,7 @@ inline std::vector<std::vector<int>> sweep_cone(const std::vector<SweepPatch>& P
 // map bytes / per-SM shared-memory throughput + all cones' bytes / L2 bandwidth.
 inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, int ld, int S, int reverse,
                                 int nsm, size_t smem_max, int force_ng, bool verbose, double ca, double cb,
-                                int own_b0 = -1, int own_b1 = -1) {
+                                int own_b0 = -1, int own_b1 = -1, int one_lane = 0) {
   SweepProgram R;
   R.S = S;
   if (S > SW_MAXS) {
@@ -445,8 +472,10 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     R.why = "no cut patch interiors";
     return R;
   }
-  auto map_d = [&](int k) { return map_rows_d((int)P[k].in.size(), (int)(P[k].in.size() + P[k].ex.size())); };
-  auto kp_of = [&](int k) { return (long long)map_kp((int)P[k].in.size(), (int)(P[k].in.size() + P[k].ex.size())); };
+  auto map_d = [&](int k) { return map_rows_d((int)P[k].in.size(), (int)(P[k].in.size() + P[k].ex.size()), one_lane); };
+  auto kp_of = [&](int k) {
+    return (long long)map_kp((int)P[k].in.size(), (int)(P[k].in.size() + P[k].ex.size()), one_lane);
+  };
   // dynamic nodes by angle, with their work
   std::vector<std::pair<double, int>> byang;
   std::unordered_map<int, double> work;
@@ -705,7 +734,7 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
           if (P[k].blk0 >= tc.runs[q].b0 && P[k].blk1 <= tc.runs[q].b1)
             dst = run_dst[q].second + (unsigned)(8 * (P[k].rows - tc.runs[q].b0));
         const unsigned m = (unsigned)P[k].in.size(), K = (unsigned)(m + P[k].ex.size());
-        const unsigned tpr = (unsigned)map_tpr((int)m), ltpr = tpr == 4 ? 2 : (tpr == 2 ? 1 : 0);
+        const unsigned tpr = (unsigned)map_tpr((int)m, one_lane), ltpr = tpr == 4 ? 2 : (tpr == 2 ? 1 : 0);
         for (unsigned r = 0; r < m; ++r)
           rows.push_back(sweep_rowjob((slot_base + dst) / 8 + 2 * tpr * r, voff[i], K, m, ltpr,
                                       (unsigned)t.slot_of[P[k].in[r]]));
@@ -726,7 +755,7 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
         std::vector<uint16_t> gl;
         for (int i = 0; i < (int)st.size(); ++i) {
           const int k = st[i];
-          const int m = (int)P[k].in.size(), K = m + (int)P[k].ex.size(), tpr = map_tpr(m), B = 2 * tpr;
+          const int m = (int)P[k].in.size(), K = m + (int)P[k].ex.size(), tpr = map_tpr(m, one_lane), B = 2 * tpr;
           for (int pos = 0; pos < (int)kp_of(k); ++pos) {
             const int c = B * (pos / B) + (pos % B) / 2 + ((pos % B) % 2) * tpr;
             if (c >= K) gl.push_back(0);
