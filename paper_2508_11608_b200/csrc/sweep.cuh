@@ -85,7 +85,14 @@ struct SweepCta {
   int run0, nrun;         // into the run array
   int slot0, nslot;       // into slot_node
   int own0, nown;         // into own: (slot, lattice node)
+  // chunk 0 repeated here, so the producer can issue it before the chunk and
+  // run lists have arrived (f_nrun < 0: more runs than fit, issue it later)
+  int f_nrun, f_bytes, f_rj_soff, f_pad;
+  long long f_aux_src;
+  SweepRun f_run[4];
+  long long f_pad2;
 };
+static_assert(sizeof(SweepCta) == 128, "SweepCta is 128 bytes");
 
 struct SweepArgs {
   const SweepCta* cta;
@@ -163,11 +170,11 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
   uint64_t* full = (uint64_t*)swm;
   uint64_t* empty = full + SW_MAXNCH;
   uint64_t* pbar = empty + SW_MAXNCH;
-  __shared__ SweepCta C;
+  __shared__ __align__(16) SweepCta C;
   __shared__ unsigned long long ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int NT = 32 * SW_NW;
-  if (tid < (int)(sizeof(SweepCta) / 4)) ((int*)&C)[tid] = ((const int*)(A.cta + blockIdx.x))[tid];
+  if (tid < (int)(sizeof(SweepCta) / 16)) ((int4*)&C)[tid] = ((const int4*)(A.cta + blockIdx.x))[tid];
   if (tid == 0) {
     for (int k = 0; k < A.nch; ++k) {
       mbar_init(&full[k], 1);
@@ -182,14 +189,21 @@ __global__ void __launch_bounds__(32 * (SW_NW + 1), 1) k_cut_sweep(SweepArgs A, 
   unsigned char* ring = swm + A.off_ring;
   SW_TSTAMP(0);
   if (warp == SW_NW) {   // producer: the program, then every chunk as its ring slot frees up
+    const bool early = C.nchunk > 0 && C.f_nrun >= 0;
     if (lane == 0) {
       const unsigned chb = 32u * C.nchunk, rub = 16u * C.nrun;
       mbar_expect_tx(pbar, chb + rub);
       if (chb) bulk_g2s(CH, A.chunk + C.chunk0, chb, pbar);
       if (rub) bulk_g2s(RU, A.run + C.run0, rub, pbar);
+      if (early) {   // chunk 0 from the CTA record, without waiting for the lists
+        mbar_expect_tx(&full[0], (unsigned)C.f_bytes);
+        const unsigned char* gm = (const unsigned char*)A.gmap;
+        for (int q = 0; q < C.f_nrun; ++q) bulk_g2s(ring + C.f_run[q].dst, gm + C.f_run[q].src, C.f_run[q].bytes, &full[0]);
+        bulk_g2s(ring + C.f_rj_soff, A.aux + C.f_aux_src, (unsigned)(C.f_bytes - C.f_rj_soff), &full[0]);
+      }
     }
     mbar_wait(pbar, 0);
-    for (int k = 0; k < C.nchunk; ++k) {
+    for (int k = early ? 1 : 0; k < C.nchunk; ++k) {
       if (k >= A.nch) mbar_wait(&empty[k % A.nch], ((k / A.nch) - 1) & 1);
 #ifdef CF_TIMING
       if (lane == 0 && blockIdx.x == 0 && k < 32) g_dbg[5000 + k / 8][k % 8] = clock64();
@@ -782,6 +796,17 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
       R.chunk.push_back(ch);
     }
     c.nrun = (int)(R.run.size() - c.run0);
+    c.f_nrun = -1;
+    if (c.nchunk) {
+      const SweepChunk& f0 = R.chunk[c.chunk0];
+      if (f0.nrun <= 4) {
+        c.f_nrun = f0.nrun;
+        for (int q = 0; q < (int)f0.nrun; ++q) c.f_run[q] = R.run[c.run0 + f0.run0 + q];
+        c.f_bytes = (int)f0.bytes;
+        c.f_rj_soff = (int)f0.rj_soff;
+        c.f_aux_src = f0.aux_src;
+      }
+    }
     R.slot_node.insert(R.slot_node.end(), t.slots.begin(), t.slots.end());
     for (int i = 0; i < c.nown; ++i) R.own.push_back(make_int2(i, best.owned[g][i]));   // owned nodes are slots 0..nown-1
     R.cta.push_back(c);
