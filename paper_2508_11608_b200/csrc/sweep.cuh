@@ -36,6 +36,7 @@
 // forward Cartesian sweep before it prefetches the level's maps towards L2.
 #pragma once
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -503,8 +504,6 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     return R;
   }
   std::sort(byang.begin(), byang.end());
-  double wtot = 0;
-  for (auto& q : byang) wtot += work[q.second];
 
   struct Plan {
     int ng = 0;
@@ -513,15 +512,18 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     long long tot = 0, mx = 0;
     double est = 1e30;
   };
-  auto make_plan = [&](int ng) {
+  // split the angle-ordered nodes into ng arcs of equal weight (wt: per-node
+  // weights, indexed like byang)
+  auto make_plan = [&](int ng, const std::vector<double>& wt) {
     Plan pl;
     pl.owned.assign(ng, {});
-    double acc = 0;
-    for (auto& q : byang) {
-      const double w = work[q.second];
-      const int g = (int)std::min<double>(ng - 1, std::floor((acc + 0.5 * w) / wtot * ng));
+    double acc = 0, tot = 0;
+    for (double w : wt) tot += w;
+    for (size_t i = 0; i < byang.size(); ++i) {
+      const double w = wt[i];
+      const int g = (int)std::min<double>(ng - 1, std::floor((acc + 0.5 * w) / tot * ng));
       acc += w;
-      pl.owned[g].push_back(q.second);
+      pl.owned[g].push_back(byang[i].second);
     }
     pl.owned.erase(std::remove_if(pl.owned.begin(), pl.owned.end(), [](const std::vector<int>& v) { return v.empty(); }),
                    pl.owned.end());
@@ -540,6 +542,31 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     pl.est = (pl.mx / 60e9 + pl.tot / 40e12) * 1e6;
     return pl;
   };
+  std::vector<double> wt0(byang.size());
+  for (size_t i = 0; i < byang.size(); ++i) wt0[i] = work[byang[i].second];
+  // equal own work leaves the cones unequal (an arc's cone also covers its
+  // neighbourhood); rebalance: scale each arc's node weights by its cone bytes
+  // over the mean and split again, keeping the plan with the smallest largest cone
+  auto balanced_plan = [&](int ng) {
+    std::vector<double> wt = wt0;
+    Plan bestp = make_plan(ng, wt);
+    for (int it = 0; it < 3 && bestp.ng > 1; ++it) {
+      const Plan& cur = bestp;
+      const double mean = (double)cur.tot / cur.ng;
+      std::unordered_map<int, double> f;
+      for (int g = 0; g < cur.ng; ++g) {
+        long long b = 0;
+        for (auto& st : cur.cones[g])
+          for (int k : st) b += 8 * map_d(k);
+        for (int nd : cur.owned[g]) f[nd] = std::sqrt(b / mean);   // damped
+      }
+      for (size_t i = 0; i < byang.size(); ++i) wt[i] *= f[byang[i].second];
+      Plan pl = make_plan(ng, wt);
+      if (pl.mx < bestp.mx) bestp = std::move(pl);
+      else break;
+    }
+    return bestp;
+  };
   Plan best;
   std::vector<int> cands;
   if (force_ng > 0) cands.push_back(std::min(force_ng, nsm));
@@ -552,12 +579,23 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
   }
   long long once = 0;
   for (int k = 0; k < (int)P.size(); ++k) once += 8 * map_d(k) * (S / 4);
+  std::vector<std::pair<double, int>> ranked;   // (estimate, CTA count) of the plain splits
   for (int g : cands) {
     if (g > (int)byang.size() && g != cands.front()) continue;
-    Plan pl = make_plan(g);
+    Plan pl = make_plan(g, wt0);
     if (verbose)
       std::fprintf(stderr, "[cutfem] sweep plan n=%d dir=%d: %d CTAs, cone map bytes max %.0f KB total %.1f MB (x%.2f), est %.2f us\n",
                    n, reverse, pl.ng, pl.mx / 1e3, pl.tot / 1e6, (double)pl.tot / std::max(1ll, once), pl.est);
+    ranked.push_back({pl.est, g});
+    if (pl.est < best.est) best = std::move(pl);
+  }
+  // the two best CTA counts with their arcs rebalanced; the better one is kept
+  std::sort(ranked.begin(), ranked.end());
+  for (size_t r = 0; r < ranked.size() && r < 2; ++r) {
+    Plan pl = balanced_plan(ranked[r].second);
+    if (verbose)
+      std::fprintf(stderr, "[cutfem] sweep plan n=%d dir=%d: %d CTAs rebalanced, cone max %.0f KB, est %.2f us\n", n,
+                   reverse, pl.ng, pl.mx / 1e3, pl.est);
     if (pl.est < best.est) best = std::move(pl);
   }
   const int ng = best.ng;
