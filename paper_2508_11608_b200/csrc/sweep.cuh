@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -646,7 +647,12 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     }
     mx_slot = std::max(mx_slot, t.slots.size());
   }
-  R.cb = (int)std::max<long long>(32 * 1024, (mx_one + mx_gat + 127) & ~127ll);
+  // ring slots: the largest of 96, 80, 64, 48, 32 KB for which two slots fit
+  // (large slots: about one chunk per step, the fewest fills; config1 cut sweep
+  // 24.7 us with 6 x 32 KB, 21.8 us with 2 x 96 KB; env CUTFEM_SWEEP_CB_KB fixes it)
+  const long long need = (mx_one + mx_gat + 127) & ~127ll;
+  std::vector<long long> cb_try = {96 * 1024, 80 * 1024, 64 * 1024, 48 * 1024, 32 * 1024};
+  if (const char* e = std::getenv("CUTFEM_SWEEP_CB_KB")) cb_try = {std::max(8, std::atoi(e)) * 1024ll};
   // chunks: consecutive tasks of one step whose runs, row jobs and (first chunk)
   // gather list fit one ring slot; runs: adjacent map blocks (gaps <= GAP bridged)
   struct TmpRun {
@@ -658,83 +664,89 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     long long run_bytes = 0, rows = 0;
     bool first = false;
   };
-  std::vector<std::vector<TmpChunk>> chunks(ng);
-  size_t mx_chunk = 0, mx_run = 0;
-  for (int g = 0; g < ng; ++g) {
-    Tmp& t = tmp[g];
-    size_t nrun = 0;
-    for (int s = 0; s < S; ++s) {
-      const std::vector<int>& st = t.steps[s];
-      long long nv = 0;
-      for (int k : st) nv += kp_of(k);
-      const long long gb = r16(2 * nv);
-      TmpChunk cur;
-      cur.step = s;
-      cur.t0 = 0;
-      cur.nt = 0;
-      cur.first = true;
-      for (int i = 0; i < (int)st.size(); ++i) {
-        const int k = st[i];
-        const long long kb0 = P[k].blk0, kb1 = P[k].blk1;
-        // bytes if appended: extend the last run or open a new one
-        long long add;
-        const bool extend = !cur.runs.empty() && kb0 >= cur.runs.back().b1 && 8 * (kb0 - cur.runs.back().b1) <= GAP;
-        add = extend ? 8 * (kb1 - cur.runs.back().b1) : 8 * (kb1 - kb0);
-        const long long used = cur.run_bytes + add + r16(8 * (cur.rows + (long long)P[k].in.size())) + (cur.first ? gb : 0);
-        if (cur.nt && used > R.cb) {
+  std::vector<std::vector<TmpChunk>> chunks;
+  auto al = [](size_t v, size_t a2) { return (v + a2 - 1) / a2 * a2; };
+  const size_t static_smem = 1024;   // __shared__ SweepCta + ticket, margin
+  size_t o = 0, mx_chunk = 0, mx_run = 0;
+  bool fits = false;
+  for (long long cbt : cb_try) {
+    R.cb = (int)std::max<long long>(cbt, need);
+    chunks.assign(ng, {});
+    mx_chunk = 0;
+    mx_run = 0;
+    for (int g = 0; g < ng; ++g) {
+      Tmp& t = tmp[g];
+      size_t nrun = 0;
+      for (int s = 0; s < S; ++s) {
+        const std::vector<int>& st = t.steps[s];
+        long long nv = 0;
+        for (int k : st) nv += kp_of(k);
+        const long long gb = r16(2 * nv);
+        TmpChunk cur;
+        cur.step = s;
+        cur.t0 = 0;
+        cur.nt = 0;
+        cur.first = true;
+        for (int i = 0; i < (int)st.size(); ++i) {
+          const int k = st[i];
+          const long long kb0 = P[k].blk0, kb1 = P[k].blk1;
+          // bytes if appended: extend the last run or open a new one
+          const bool extend = !cur.runs.empty() && kb0 >= cur.runs.back().b1 && 8 * (kb0 - cur.runs.back().b1) <= GAP;
+          const long long add = extend ? 8 * (kb1 - cur.runs.back().b1) : 8 * (kb1 - kb0);
+          const long long used = cur.run_bytes + add + r16(8 * (cur.rows + (long long)P[k].in.size())) + (cur.first ? gb : 0);
+          if (cur.nt && used > R.cb) {
+            nrun += cur.runs.size();
+            chunks[g].push_back(cur);
+            TmpChunk nx;
+            nx.step = s;
+            nx.t0 = i;
+            nx.nt = 0;
+            cur = nx;
+          }
+          const bool ext2 = !cur.runs.empty() && kb0 >= cur.runs.back().b1 && 8 * (kb0 - cur.runs.back().b1) <= GAP;
+          if (ext2) {
+            cur.run_bytes += 8 * (kb1 - cur.runs.back().b1);
+            cur.runs.back().b1 = kb1;
+          } else {
+            cur.runs.push_back({kb0, kb1});
+            cur.run_bytes += 8 * (kb1 - kb0);
+          }
+          if (!cur.nt) cur.t0 = i;
+          ++cur.nt;
+          cur.rows += (long long)P[k].in.size();
+        }
+        if (cur.nt) {
           nrun += cur.runs.size();
           chunks[g].push_back(cur);
-          TmpChunk nx;
-          nx.step = s;
-          nx.t0 = i;
-          nx.nt = 0;
-          cur = nx;
         }
-        const bool ext2 = !cur.runs.empty() && kb0 >= cur.runs.back().b1 && 8 * (kb0 - cur.runs.back().b1) <= GAP;
-        if (ext2) {
-          cur.run_bytes += 8 * (kb1 - cur.runs.back().b1);
-          cur.runs.back().b1 = kb1;
-        } else {
-          cur.runs.push_back({kb0, kb1});
-          cur.run_bytes += 8 * (kb1 - kb0);
-        }
-        if (!cur.nt) cur.t0 = i;
-        ++cur.nt;
-        cur.rows += (long long)P[k].in.size();
       }
-      if (cur.nt) {
-        nrun += cur.runs.size();
-        chunks[g].push_back(cur);
-      }
+      mx_chunk = std::max(mx_chunk, chunks[g].size());
+      mx_run = std::max(mx_run, nrun);
     }
-    mx_chunk = std::max(mx_chunk, chunks[g].size());
-    mx_run = std::max(mx_run, nrun);
+    // shared-memory layout: barriers | chunks | runs | xs | bs | v | ring
+    o = 256;
+    R.off_chunk = (unsigned)o;
+    o = al(o + 32 * mx_chunk, 128);
+    R.off_run = (unsigned)o;
+    o = al(o + 16 * mx_run, 128);
+    R.off_xs = (unsigned)o;
+    o = al(o + 8 * mx_slot, 128);
+    R.off_bs = (unsigned)o;
+    o = al(o + 8 * mx_slot, 128);
+    R.off_v = (unsigned)o;
+    o = al(o + 8 * mx_v, 128);
+    R.off_ring = (unsigned)o;
+    if (o + static_smem + 2 * (size_t)R.cb <= smem_max && 2 * (size_t)R.cb / 8 <= 65535) {
+      fits = true;
+      break;
+    }
   }
-  // shared-memory layout: barriers | chunks | runs | xs | bs | v | ring
-  auto al = [](size_t v, size_t a2) { return (v + a2 - 1) / a2 * a2; };
-  size_t o = 256;
-  R.off_chunk = (unsigned)o;
-  o = al(o + 32 * mx_chunk, 128);
-  R.off_run = (unsigned)o;
-  o = al(o + 16 * mx_run, 128);
-  R.off_xs = (unsigned)o;
-  o = al(o + 8 * mx_slot, 128);
-  R.off_bs = (unsigned)o;
-  o = al(o + 8 * mx_slot, 128);
-  R.off_v = (unsigned)o;
-  o = al(o + 8 * mx_v, 128);
-  R.off_ring = (unsigned)o;
-  const size_t static_smem = 1024;   // __shared__ SweepCta + ticket, margin
-  if (o + static_smem + 2 * (size_t)R.cb > smem_max) {
+  if (!fits) {
     R.why = "shared memory: program + two ring slots exceed the per-block limit";
     return R;
   }
   R.nch = (int)std::min<size_t>(SW_MAXNCH, (smem_max - static_smem - o) / R.cb);
   while (R.nch > 2 && (size_t)R.nch * R.cb / 8 > 65535) --R.nch;   // 16-bit row offsets from the ring base
-  if ((size_t)R.nch * R.cb / 8 > 65535) {
-    R.why = "ring too large for 16-bit row offsets";
-    return R;
-  }
   R.smem = o + (size_t)R.nch * R.cb;
   // emit
   for (int g = 0; g < ng; ++g) {
