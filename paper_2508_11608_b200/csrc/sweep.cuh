@@ -572,9 +572,10 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
   std::vector<int> cands;
   if (force_ng > 0) cands.push_back(std::min(force_ng, nsm));
   else {
-    // (large levels: few CTAs are never competitive and their cones are the
-    // costliest to build, so the search starts at nsm / 8)
-    const int g0 = P.size() > 50 * (size_t)nsm ? std::max(1, nsm / 8) : 1;
+    // (large levels: few CTAs are never competitive -- every level with more
+    // than 10 nsm patches chose >= 92 of 148 -- and their cones are the costliest
+    // to build, so the search starts at nsm / 4)
+    const int g0 = P.size() > 10 * (size_t)nsm ? std::max(1, nsm / 4) : 1;
     for (int g = g0; g < nsm; g = g * 3 / 2 + 1) cands.push_back(g);
     cands.push_back(nsm);
   }
