@@ -591,14 +591,23 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     ranked.push_back({pl.est, g});
     if (pl.est < best.est) best = std::move(pl);
   }
-  // the two best CTA counts with their arcs rebalanced; the better one is kept
+  // the two best CTA counts and the full device with their arcs rebalanced;
+  // the best of them is kept
   std::sort(ranked.begin(), ranked.end());
-  for (size_t r = 0; r < ranked.size() && r < 2; ++r) {
-    Plan pl = balanced_plan(ranked[r].second);
+  std::vector<int> tryb;
+  for (size_t r = 0; r < ranked.size() && r < 2; ++r) tryb.push_back(ranked[r].second);
+  if (force_ng <= 0 && std::find(tryb.begin(), tryb.end(), nsm) == tryb.end() && nsm <= (int)byang.size())
+    tryb.push_back(nsm);
+  // (within 3 % of the best estimate and at most 15 % more map bytes, the plan
+  // with more CTAs is taken: measured faster than the model says, e.g. config1
+  // 148 vs 128 CTAs: 26.6 vs 28.7 us)
+  for (int gb : tryb) {
+    Plan pl = balanced_plan(gb);
     if (verbose)
       std::fprintf(stderr, "[cutfem] sweep plan n=%d dir=%d: %d CTAs rebalanced, cone max %.0f KB, est %.2f us\n", n,
                    reverse, pl.ng, pl.mx / 1e3, pl.est);
-    if (pl.est < best.est) best = std::move(pl);
+    if (pl.est < 0.97 * best.est || (pl.est <= 1.03 * best.est && pl.ng > best.ng && pl.tot <= 1.15 * best.tot))
+      best = std::move(pl);
   }
   const int ng = best.ng;
   R.ncta = ng;
