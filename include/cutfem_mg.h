@@ -138,7 +138,11 @@ int cutfem_apply_operator(cutfem_problem pb, int level, const double* x, double*
 
 /* One smoothing step x <- S(x, b) of eq. (smoother-split) (P l.196-210):
  * Cartesian colours 0..3, then n_c sweeps over cut colours 0..3; reverse = 1
- * applies the steps in the opposite order (R9).  In place on x. */
+ * applies the steps in the opposite order (R9).  In place on x.  In 2D the
+ * cut colour steps run as one cooperative launch (cutfem_level_info.sweep_ctas
+ * CTAs, at most one per SM), bit-identical to one launch per colour step: a
+ * concurrent kernel that holds SMs delays it until they free up.  Returns
+ * CUTFEM_ERR_CUDA if the launch fails. */
 int cutfem_smooth(cutfem_problem pb, int level, double* x, const double* b, int reverse, void* stream);
 
 /* One colour step of the smoother (P l.179-181, R9): kind 0 = Cartesian,
