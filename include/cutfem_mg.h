@@ -231,6 +231,23 @@ int cutfem_partition_info(cutfem_problem pb, int level, int* out);
  * rows; peer = -1 for an unused slot).  ERR_ARG unless n_cells % world == 0
  * and n_cells / world >= halo_cells + 1. */
 int cutfem_slab_plan(int n_cells, int degree, int world, int rank, int halo_cells, int64_t* out);
+/* The planner of the one-launch cut sweep (host only, no device; exposed for
+ * the CPU tests of its dependency cones).  Input: npatch cut patches of a 2D
+ * level (n cells per side, degree p, lattice row stride ld), patch k with
+ * vertex (ijc[3k], ijc[3k+1]), colour ijc[3k+2], interior lattice nodes
+ * in_nodes[in_off[k] .. in_off[k+1]) and coupled exterior window nodes
+ * ex_nodes[ex_off[k] .. ex_off[k+1]); S = 4 n_c colour steps, reverse = the
+ * adjoint order; nsm = CTA limit, force_ng > 0 forces the count; (ca, cb) =
+ * the level-set centre in lattice coordinates.  Output: the CTA count
+ * (*ncta), per CTA g its owned nodes own_nodes[own_off[g] .. own_off[g+1])
+ * and per (g, step s) the cone's patches task_patch[task_off[g S + s] ..
+ * task_off[g S + s + 1]).  The caller sizes the arrays (own_off: nsm + 1,
+ * task_off: nsm S + 1, own_nodes / task_patch: own_cap / task_cap entries);
+ * ERR_SIZE if they are too small, ERR_ARG for bad arguments. */
+int cutfem_sweep_plan(int n, int p, int ld, int S, int reverse, int nsm, int force_ng, int npatch, const int* ijc,
+                      const int* in_off, const int* in_nodes, const int* ex_off, const int* ex_nodes, double ca,
+                      double cb, int* ncta, int* own_off, int* own_nodes, int own_cap, int* task_off, int* task_patch,
+                      int task_cap);
 /* exchange the halo rows of a lattice vector of `level` with the neighbours */
 int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream);
 

@@ -285,6 +285,56 @@ int cutfem_slab_plan(int n_cells, int degree, int world, int rank, int halo_cell
   });
 }
 
+int cutfem_sweep_plan(int n, int p, int ld, int S, int reverse, int nsm, int force_ng, int npatch, const int* ijc,
+                      const int* in_off, const int* in_nodes, const int* ex_off, const int* ex_nodes, double ca,
+                      double cb, int* ncta, int* own_off, int* own_nodes, int own_cap, int* task_off, int* task_patch,
+                      int task_cap) {
+  return guarded([&]() {
+    cf::require(n >= 1 && p >= 1 && p <= 3 && ld >= n * p + 1 && S >= 4 && S % 4 == 0 && nsm >= 1 && npatch >= 0,
+                cf::ERR_ARG, "bad sweep plan arguments");
+    cf::require(ijc && in_off && ex_off && ncta && own_off && own_nodes && task_off && task_patch, cf::ERR_ARG,
+                "null argument");
+    std::vector<cf::host::SweepPatch> P(npatch);
+    long long blk = 0;
+    for (int k = 0; k < npatch; ++k) {
+      cf::host::SweepPatch& q = P[k];
+      q.I = ijc[3 * k];
+      q.J = ijc[3 * k + 1];
+      q.colour = ijc[3 * k + 2];
+      q.in.assign(in_nodes + in_off[k], in_nodes + in_off[k + 1]);
+      q.ex.assign(ex_nodes + ex_off[k], ex_nodes + ex_off[k + 1]);
+      cf::require(!q.in.empty(), cf::ERR_ARG, "a patch without interior nodes");
+      // map blocks laid out consecutively (the planner only needs their sizes)
+      q.blk0 = blk;
+      q.rows = blk + cf::map_hdr_d((int)q.ex.size());
+      q.blk1 = q.rows + cf::map_rows_d((int)q.in.size(), (int)(q.in.size() + q.ex.size()), 0);
+      blk = q.blk1;
+    }
+    cf::host::SweepPlan plan;
+    const cf::host::SweepProgram R = cf::host::build_sweep(P, n, p, ld, S, reverse, nsm, 232448, force_ng, false, ca, cb,
+                                                          -1, -1, 0, &plan);
+    cf::require(plan.ng > 0, cf::ERR_ARG, "no plan: " + R.why);
+    *ncta = plan.ng;
+    int no = 0, nt = 0;
+    own_off[0] = 0;
+    task_off[0] = 0;
+    for (int g = 0; g < plan.ng; ++g) {
+      for (int nd : plan.owned[g]) {
+        cf::require(no < own_cap, cf::ERR_SIZE, "own_cap too small");
+        own_nodes[no++] = nd;
+      }
+      own_off[g + 1] = no;
+      for (int s2 = 0; s2 < S; ++s2) {
+        for (int k : plan.cones[g][s2]) {
+          cf::require(nt < task_cap, cf::ERR_SIZE, "task_cap too small");
+          task_patch[nt++] = k;
+        }
+        task_off[g * S + s2 + 1] = nt;
+      }
+    }
+  });
+}
+
 int cutfem_halo_exchange(cutfem_problem pb, int level, double* v, void* stream) {
   return guarded([&]() {
     check_level(pb, level);

@@ -472,9 +472,19 @@ inline std::vector<std::vector<int>> sweep_cone(const std::vector<SweepPatch>& P
 // bytes at 139 CTAs on config1, x2.5 for Hilbert-ordered 4x4-cell atoms).
 // The CTA count minimises an estimate of the sweep time: the largest cone's
 // map bytes / per-SM shared-memory throughput + all cones' bytes / L2 bandwidth.
+// The chosen split: per CTA its owned dynamic nodes and, per step, the
+// patches of its dependency cone.
+struct SweepPlan {
+  int ng = 0;
+  std::vector<std::vector<int>> owned;
+  std::vector<std::vector<std::vector<int>>> cones;
+  long long tot = 0, mx = 0;
+  double est = 1e30;
+};
+
 inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, int ld, int S, int reverse,
                                 int nsm, size_t smem_max, int force_ng, bool verbose, double ca, double cb,
-                                int own_b0 = -1, int own_b1 = -1, int one_lane = 0) {
+                                int own_b0 = -1, int own_b1 = -1, int one_lane = 0, SweepPlan* plan_out = nullptr) {
   SweepProgram R;
   R.S = S;
   if (S > SW_MAXS) {
@@ -506,13 +516,7 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
   }
   std::sort(byang.begin(), byang.end());
 
-  struct Plan {
-    int ng = 0;
-    std::vector<std::vector<int>> owned;
-    std::vector<std::vector<std::vector<int>>> cones;
-    long long tot = 0, mx = 0;
-    double est = 1e30;
-  };
+  using Plan = SweepPlan;
   // split the angle-ordered nodes into ng arcs of equal weight (wt: per-node
   // weights, indexed like byang)
   auto make_plan = [&](int ng, const std::vector<double>& wt) {
@@ -609,6 +613,7 @@ inline SweepProgram build_sweep(const std::vector<SweepPatch>& P, int n, int p, 
     if (pl.est < 0.97 * best.est || (pl.est <= 1.03 * best.est && pl.ng > best.ng && pl.tot <= 1.15 * best.tot))
       best = std::move(pl);
   }
+  if (plan_out) *plan_out = best;
   const int ng = best.ng;
   R.ncta = ng;
   R.est_us = best.est;

@@ -78,6 +78,8 @@ _sig = {
     "cutfem_partition": [_P, _P],
     "cutfem_partition_info": [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
     "cutfem_halo_exchange": [_P, ctypes.c_int, _D, _P],
+    "cutfem_sweep_plan": [ctypes.c_int] * 8 + [_D] * 5 + [ctypes.c_double, ctypes.c_double, _D, _D, _D, ctypes.c_int,
+                                               _D, _D, ctypes.c_int],
     "cutfem_slab_plan": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                          ctypes.POINTER(ctypes.c_int64)],
 }
@@ -123,6 +125,37 @@ def make_params(x0, y0, length, n_coarse, n_levels, degree, cx, cy, r, gamma_D=0
 
 
 NCCL_ID_BYTES = 128
+
+
+def sweep_plan(n, p, ld, S, reverse, nsm, force_ng, ijc, in_lists, ex_lists, ca, cb):
+    """Host-only planner of the one-launch cut sweep (cutfem_sweep_plan):
+    patches given as ijc (k, 3) = (I, J, colour) and per-patch lists of
+    interior / coupled exterior lattice nodes (b * ld + a).  Returns (owned,
+    cones): owned[g] = nodes of CTA g, cones[g][s] = patch indices of its
+    step-s cone."""
+    npatch = len(in_lists)
+    ijc = np.ascontiguousarray(np.asarray(ijc, dtype=np.int32).reshape(npatch, 3))
+    in_off = np.zeros(npatch + 1, np.int32)
+    ex_off = np.zeros(npatch + 1, np.int32)
+    in_off[1:] = np.cumsum([len(v) for v in in_lists])
+    ex_off[1:] = np.cumsum([len(v) for v in ex_lists])
+    in_nodes = np.ascontiguousarray(np.concatenate([np.asarray(v, np.int32) for v in in_lists] or [np.zeros(0, np.int32)]))
+    ex_nodes = np.ascontiguousarray(np.concatenate([np.asarray(v, np.int32) for v in ex_lists] or [np.zeros(0, np.int32)]))
+    own_cap = int(in_off[-1]) + 1
+    task_cap = max(1, npatch * S * nsm)
+    ncta = ctypes.c_int(0)
+    own_off = np.zeros(nsm + 1, np.int32)
+    own_nodes = np.zeros(own_cap, np.int32)
+    task_off = np.zeros(nsm * S + 1, np.int32)
+    task_patch = np.zeros(task_cap, np.int32)
+    d = lambda a: a.ctypes.data_as(_D)
+    _check(_lib.cutfem_sweep_plan(n, p, ld, S, int(reverse), nsm, force_ng, npatch, d(ijc), d(in_off), d(in_nodes),
+                                  d(ex_off), d(ex_nodes), float(ca), float(cb), ctypes.byref(ncta), d(own_off),
+                                  d(own_nodes), own_cap, d(task_off), d(task_patch), task_cap))
+    g = ncta.value
+    owned = [own_nodes[own_off[i]:own_off[i + 1]].tolist() for i in range(g)]
+    cones = [[task_patch[task_off[i * S + s]:task_off[i * S + s + 1]].tolist() for s in range(S)] for i in range(g)]
+    return owned, cones
 
 
 def slab_plan(n_cells, degree, world, rank, halo_cells):
