@@ -327,8 +327,16 @@ def main():
     for _ in range(e2e_steps):
         g.smooth_host(L, xn, bn)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, dist, "cuda")
-    e2e = {"value": n_dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * nl * ld * 8 * world,
-           "d2h_bytes_per_step": nl * ld * 8 * world}
+    # pinned host vectors: the library moves only the DoF span of every lattice
+    # row (k_copy_spans, 3 launches around the step's own), else whole vectors
+    lc0 = cutfem.launch_count()
+    g.smooth_host(L, xn, bn)
+    spans = cutfem.launch_count() - lc0 > launches // args.steps
+    vec_doubles = int(g.level_info(L).host_span_doubles) if spans else nl * ld
+    e2e = {"value": n_dofs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * vec_doubles * 8 * world,
+           "d2h_bytes_per_step": vec_doubles * 8 * world,
+           "host_copy": "DoF spans of the lattice rows (pinned memory read / written over PCIe by kernels)" if spans
+           else "whole lattice vectors (cudaMemcpyAsync)"}
 
     # ---- BASELINE configs[2]: 3D sphere, Q2, 128^3 (secondary line, same timing rules)
     cfg3 = None

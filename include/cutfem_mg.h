@@ -106,6 +106,8 @@ typedef struct {
   double sweep_redundancy[2];  /* map bytes the sweep's CTAs stream / map bytes of the 4 n_c
                                   colour steps (>= 1: patches recomputed near CTA boundaries) */
   int64_t sweep_map_bytes[2];  /* map bytes streamed by all CTAs of one sweep */
+  int64_t host_span_doubles;   /* 2D: doubles of the DoF spans of the lattice rows (what
+                                  cutfem_smooth_host moves per vector for pinned host memory) */
 } cutfem_level_info;
 
 /* ---- setup ------------------------------------------------------------ */
@@ -168,7 +170,11 @@ int cutfem_solve_cg_mg(cutfem_problem pb, double* x, const double* b, double tol
 
 /* Same as the calls above with HOST (pageable or pinned) lattice vectors:
  * host->device copy of the inputs, the device call, device->host copy of the
- * result, all on `stream`; blocks until the result is on the host. */
+ * result, all on `stream`; blocks until the result is on the host.  For
+ * pinned, device-mapped host memory (cudaHostAlloc, cudaHostRegister) on a 2D
+ * level-set problem, cutfem_smooth_host moves only the DoF span of every
+ * lattice row, read and written by kernels over PCIe
+ * (cutfem_level_info.host_span_doubles per vector); otherwise whole vectors. */
 int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const double* b_host, int reverse,
                        void* stream);
 int cutfem_solve_cg_mg_host(cutfem_problem pb, double* x_host, const double* b_host, double tol,

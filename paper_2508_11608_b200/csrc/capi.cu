@@ -134,6 +134,8 @@ int cutfem_level_info_get(cutfem_problem pb, int level, cutfem_level_info* out) 
     }
     for (int c = 0; c < 8; ++c) out->cut_step_bytes[c] = D.gmap ? D.cut_bytes[c] : 0;
     for (int c = 0; c < 8; ++c) out->cut_method_bytes[c] = D.cut_method_bytes[c];
+    if (pb->p.prm.dim == 2) pb->p.build_spans(const_cast<cf::LevelData&>(D));
+    out->host_span_doubles = D.span_doubles;
     for (int d = 0; d < 2; ++d) {
       out->sweep_ctas[d] = D.sw[d].ok ? D.sw[d].ncta : 0;
       out->sweep_redundancy[d] = D.sw[d].ok ? D.sw[d].redundancy : 0.0;
@@ -376,6 +378,17 @@ static void host_buffers(cutfem_problem pb) {
   }
 }
 
+// host memory the device can address directly (pinned, mapped: cudaHostAlloc /
+// cudaHostRegister under unified addressing): its device pointer, else null
+static const double* mapped(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer ? (const double*)a.devicePointer : nullptr;
+}
+
 int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const double* b_host, int reverse,
                        void* stream) {
   return guarded([&]() {
@@ -385,6 +398,19 @@ int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const doubl
     use_stream(pb, stream);
     host_buffers(pb);
     const size_t bytes = (size_t)pb->p.vsize(level) * sizeof(double);
+    const double *mx = mapped(x_host), *mb = mapped(b_host);
+    if (mx && mb && pb->p.prm.dim == 2 && pb->p.prm.domain == 0) {
+      // pinned host vectors: only the DoF span of every row crosses PCIe (the
+      // library ignores non-DoF entries on input and leaves them unchanged)
+      pb->p.copy_spans(level, mx, pb->p.hx);
+      pb->p.copy_spans(level, mb, pb->p.hb);
+      double* dx = pb->p.hx;
+      const double* db = pb->p.hb;
+      pb->p.graphed(1, dx, db, level * 2 + (reverse ? 1 : 0), [&]() { pb->p.smooth(level, dx, db, reverse); });
+      pb->p.copy_spans(level, pb->p.hx, (double*)mx);
+      pb->p.sync();
+      return;
+    }
     CF_CUDA(cudaMemcpyAsync(pb->p.hx, x_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
     CF_CUDA(cudaMemcpyAsync(pb->p.hb, b_host, bytes, cudaMemcpyHostToDevice, pb->p.st));
     double* dx = pb->p.hx;

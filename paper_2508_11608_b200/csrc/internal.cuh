@@ -182,6 +182,10 @@ struct LevelData {
   std::vector<int> wd_off[2];        //   at wdesc + [wd_off[d][s], wd_off[d][s+1])
   int32_t* wcopy = nullptr;          //   copy lists at wcopy + wc_off[d][s], wc_n[d][s] nodes
   std::vector<int> wc_off[2], wc_n[2];
+  // DoF span [a0, a1) of every lattice row (host-vector copies, k_copy_spans);
+  // built on first use; span_doubles = the doubles they cover
+  int* span = nullptr;
+  int64_t span_doubles = 0;
   // one-launch cut sweeps (sweep.cuh), per direction (0 forward, 1 reverse);
   // args points at device arrays owned by the problem
   struct Sweep {

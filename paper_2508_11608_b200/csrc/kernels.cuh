@@ -15,6 +15,18 @@
 
 namespace cf {
 
+// host <-> device copy of the DoF span of every lattice row (host pointers of
+// pinned, mapped memory are read / written directly over PCIe): block per
+// row, span [a0, a1) of row b from span[2 b], span[2 b + 1]; rows of LD doubles
+__global__ void k_copy_spans(const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ span,
+                             int ld, int row0) {
+  const int b = row0 + blockIdx.x;
+  const int a0 = span[2 * b], a1 = span[2 * b + 1];
+  const size_t o = (size_t)b * ld;
+  for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) dst[o + a] = src[o + a];
+}
+
+
 // 1D tables staged in shared memory where lanes index them with different
 // (runtime) indices; constant memory serialises divergent addresses.
 struct SmTab {

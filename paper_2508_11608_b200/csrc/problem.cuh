@@ -676,6 +676,45 @@ struct Problem {
     }
   }
 
+  // DoF spans of the lattice rows of a 2D level (from the DoF mask; rows
+  // without DoF: empty), for the host-vector paths
+  void build_spans(LevelData& D) {
+    if (D.span) return;
+    const LevelArgs& L = D.a;
+    const int64_t rows = prm.dim == 3 ? (int64_t)L.nl * L.nl : L.nl;
+    std::vector<uint8_t> m((size_t)rows * L.ld);
+    CF_CUDA(cudaMemcpy(m.data(), D.mask, m.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> sp(2 * rows, 0);
+    int64_t tot = 0;
+    for (int64_t b = 0; b < rows; ++b) {
+      int a0 = -1, a1 = -1;
+      for (int a = 0; a < L.nl; ++a)
+        if (m[(size_t)b * L.ld + a]) {
+          if (a0 < 0) a0 = a;
+          a1 = a + 1;
+        }
+      if (a0 < 0) a0 = a1 = 0;
+      sp[2 * b] = a0;
+      sp[2 * b + 1] = a1;
+      tot += a1 - a0;
+    }
+    D.span = alloc<int>(2 * rows);
+    CF_CUDA(cudaMemcpy(D.span, sp.data(), sizeof(int) * sp.size(), cudaMemcpyHostToDevice));
+    D.span_doubles = tot;
+  }
+  // copy the DoF spans of a lattice vector of level l (src / dst: device or
+  // mapped pinned host memory)
+  void copy_spans(int l, const double* src, double* dst) {
+    LevelData& D = lv[l];
+    build_spans(D);
+    const int64_t rows = prm.dim == 3 ? (int64_t)D.a.nl * D.a.nl : D.a.nl;
+    for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+      const int nb = (int)std::min<int64_t>(65535, rows - r0);
+      k_copy_spans<<<nb, 128, 0, st>>>(src, dst, D.span, D.a.ld, (int)r0);
+      CF_LAUNCHED();
+    }
+  }
+
   // programs of the one-launch cut sweeps (sweep.cuh) of a 2D level, both
   // directions: the patches (interior nodes in map row order, the coupled
   // exterior nodes in map column order, map rows) go to the host builder,

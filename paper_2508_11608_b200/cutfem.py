@@ -45,7 +45,8 @@ class LevelInfo(ctypes.Structure):
                 ("n_cart", ctypes.c_int * 8), ("n_cutp", ctypes.c_int * 8), ("n_vol_qp", ctypes.c_int64),
                 ("n_surf_qp", ctypes.c_int64), ("h", ctypes.c_double), ("cut_step_bytes", ctypes.c_int64 * 8),
                 ("cut_method_bytes", ctypes.c_int64 * 8), ("sweep_ctas", ctypes.c_int * 2),
-                ("sweep_redundancy", ctypes.c_double * 2), ("sweep_map_bytes", ctypes.c_int64 * 2)]
+                ("sweep_redundancy", ctypes.c_double * 2), ("sweep_map_bytes", ctypes.c_int64 * 2),
+                ("host_span_doubles", ctypes.c_int64)]
 
 
 _P = ctypes.c_void_p

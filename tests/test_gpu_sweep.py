@@ -174,3 +174,36 @@ def test_sweep_partitioned_bitexact(world):
         assert g.partition_info(L)["part"] and 0 < info.sweep_ctas[0] <= nsm // world
         r0, r1, a = owned(g, x, L)
         np.testing.assert_array_equal(a, ref[r0:r1])
+
+
+def test_smooth_host_pinned_spans():
+    """cutfem_smooth_host with pinned host vectors moves only the DoF span of
+    every lattice row (k_copy_spans): same DoF results as the device call,
+    non-DoF host entries untouched (NaN stays NaN), the span kernels launched."""
+    import torch
+    from paper_2508_11608_b200 import cutfem
+    w = workloads.paper_level(2, 8)
+    g = problem(w, {})
+    L = w.n_levels - 1
+    nl, ld = g.lattice_shape(L)
+    mask = np.zeros((nl, ld), bool)
+    mask[:, :nl] = g.dof_mask(L)
+    xl = np.zeros((nl, ld))
+    bl = np.zeros((nl, ld))
+    xl[:, :nl] = workloads.lattice_vector(w, 31, L).reshape(nl, nl)
+    bl[:, :nl] = workloads.lattice_vector(w, 32, L).reshape(nl, nl)
+    xl[~mask] = np.nan
+    bl[~mask] = np.nan
+    xh = torch.from_numpy(xl.ravel().copy()).pin_memory()
+    bh = torch.from_numpy(bl.ravel().copy()).pin_memory()
+    x = g.to_device(np.nan_to_num(xl[:, :nl]).ravel(), L)
+    g.smooth(L, x, g.to_device(np.nan_to_num(bl[:, :nl]).ravel(), L), False)
+    ref = x.cpu().numpy().reshape(nl, ld)
+    l0 = cutfem.launch_count()
+    g.smooth_host(L, xh.numpy(), bh.numpy())
+    assert cutfem.launch_count() - l0 >= 3   # the span copies ran
+    out = xh.numpy().reshape(nl, ld)
+    assert np.array_equal(out[mask], ref[mask])
+    assert np.isnan(out[~mask]).all()
+    info = g.level_info(L)
+    assert int(mask.sum()) <= info.host_span_doubles < nl * ld
