@@ -328,7 +328,7 @@ def main():
         g.smooth_host(L, xn, bn)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, dist, "cuda")
     # pinned host vectors: the library moves only the DoF span of every lattice
-    # row (k_copy_spans, 3 launches around the step's own), else whole vectors
+    # row (k_copy_spans, 2 launches around the step's own), else whole vectors
     lc0 = cutfem.launch_count()
     g.smooth_host(L, xn, bn)
     spans = cutfem.launch_count() - lc0 > launches // args.steps

@@ -402,8 +402,7 @@ int cutfem_smooth_host(cutfem_problem pb, int level, double* x_host, const doubl
     if (mx && mb && pb->p.prm.dim == 2 && pb->p.prm.domain == 0) {
       // pinned host vectors: only the DoF span of every row crosses PCIe (the
       // library ignores non-DoF entries on input and leaves them unchanged)
-      pb->p.copy_spans(level, mx, pb->p.hx);
-      pb->p.copy_spans(level, mb, pb->p.hb);
+      pb->p.copy_spans(level, mx, pb->p.hx, mb, pb->p.hb);
       double* dx = pb->p.hx;
       const double* db = pb->p.hb;
       pb->p.graphed(1, dx, db, level * 2 + (reverse ? 1 : 0), [&]() { pb->p.smooth(level, dx, db, reverse); });

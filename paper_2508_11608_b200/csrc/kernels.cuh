@@ -19,10 +19,14 @@ namespace cf {
 // pinned, mapped memory are read / written directly over PCIe): block per
 // row, span [a0, a1) of row b from span[2 b], span[2 b + 1]; rows of LD doubles
 __global__ void k_copy_spans(const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ span,
-                             int ld, int row0) {
+                             int ld, int row0, const double* __restrict__ src2, double* __restrict__ dst2) {
   const int b = row0 + blockIdx.x;
   const int a0 = span[2 * b], a1 = span[2 * b + 1];
   const size_t o = (size_t)b * ld;
+  if (blockIdx.y) {   // a second vector in the same launch (x and b together)
+    src = src2;
+    dst = dst2;
+  }
   for (int a = a0 + threadIdx.x; a < a1; a += blockDim.x) dst[o + a] = src[o + a];
 }
 

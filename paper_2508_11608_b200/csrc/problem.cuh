@@ -703,14 +703,14 @@ struct Problem {
     D.span_doubles = tot;
   }
   // copy the DoF spans of a lattice vector of level l (src / dst: device or
-  // mapped pinned host memory)
-  void copy_spans(int l, const double* src, double* dst) {
+  // mapped pinned host memory); src2 / dst2: a second vector in the same launch
+  void copy_spans(int l, const double* src, double* dst, const double* src2 = nullptr, double* dst2 = nullptr) {
     LevelData& D = lv[l];
     build_spans(D);
     const int64_t rows = prm.dim == 3 ? (int64_t)D.a.nl * D.a.nl : D.a.nl;
     for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
       const int nb = (int)std::min<int64_t>(65535, rows - r0);
-      k_copy_spans<<<nb, 128, 0, st>>>(src, dst, D.span, D.a.ld, (int)r0);
+      k_copy_spans<<<dim3(nb, src2 ? 2 : 1), 256, 0, st>>>(src, dst, D.span, D.a.ld, (int)r0, src2, dst2);
       CF_LAUNCHED();
     }
   }

@@ -201,7 +201,7 @@ def test_smooth_host_pinned_spans():
     ref = x.cpu().numpy().reshape(nl, ld)
     l0 = cutfem.launch_count()
     g.smooth_host(L, xh.numpy(), bh.numpy())
-    assert cutfem.launch_count() - l0 >= 3   # the span copies ran
+    assert cutfem.launch_count() - l0 >= 2 + 2   # the span copies (x and b in, x out) ran with the step
     out = xh.numpy().reshape(nl, ld)
     assert np.array_equal(out[mask], ref[mask])
     assert np.isnan(out[~mask]).all()
